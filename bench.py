@@ -1,0 +1,412 @@
+"""bench.py -- HSVD time-to-solution on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--n 8192] [--p n/2] [--mode pointwise|block]
+
+A "step" is one complete HSVD solve (reference drive(), solver.py:179-269)
+of the seeded synthetic factor of SURVEY.md §8(d) config 5: n = r = 8192,
+G = default_rng(0).standard_normal, J = diag(+1 x p, -1 x (n-p)), p = n/2,
+V^{-T} accumulated.  `value` = seconds per solve with G already in HBM
+(timed with CUDA events, includes the D2D input copy the reference also
+makes, solver.py:188); `e2e` = the same through the public numpy API
+(drive(G_numpy, J)) with the host->device copy of G and the device->host
+copies of U, V^{-T}, sigma, lambda inside the timed region.
+
+--impl reference times the reference algorithm on the host CPU: the C
+restatement in oracle/ (bit-exact with hjsvd, see tests/golden) with every
+host thread, on a bounded sample of the same workload, extrapolated to a
+full solve with the exact per-sweep rotation/skip counts (oracle/README).
+
+One process per GPU (torchrun); N>1 currently runs independent replicas
+(each rank solves its own copy) and reports the max over ranks.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+TELEMETRY_FILE = os.path.join(ROOT, "profiles", "reference_telemetry.json")
+METRIC = "HSVD time-to-solution (s) fp64 n={n}"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=8192)
+    ap.add_argument("--p", type=int, default=None)
+    ap.add_argument("--mode", default="pointwise", choices=["pointwise", "block"])
+    ap.add_argument("--block-cols", type=int, default=32)
+    ap.add_argument("--cpu-sample-s", type=float, default=12.0)
+    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-accuracy", action="store_true")
+    a = ap.parse_args()
+    if a.p is None:
+        a.p = a.n // 2
+    return a
+
+
+def make_input(n, p, seed=0):
+    from tests.golden.inputs import make_case_input
+    G = make_case_input(n, n, seed, "gauss")
+    signs = np.array([1] * p + [-1] * (n - p), np.int8)
+    return G, signs
+
+
+# ---------------------------------------------------------------- clocks
+
+
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-i", str(self.index), "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            if len(r) < 9:
+                continue
+            for name, v in zip(names, r[5:9]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- CPU legs
+
+
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def load_reference_telemetry(n, p):
+    """Per-sweep (rotations, skips) of the reference on this exact input.
+    The pointwise GPU mode is bit-exact with the reference, so its telemetry
+    IS the reference's; bench.py records it in profiles/ when it runs."""
+    if os.path.exists(TELEMETRY_FILE):
+        with open(TELEMETRY_FILE) as f:
+            data = json.load(f)
+        key = f"n{n}_p{p}"
+        if key in data:
+            return data[key]
+    return None
+
+
+def save_reference_telemetry(n, p, telemetry):
+    data = {}
+    if os.path.exists(TELEMETRY_FILE):
+        with open(TELEMETRY_FILE) as f:
+            data = json.load(f)
+    data[f"n{n}_p{p}"] = {"sweeps": len(telemetry),
+                          "rot": [int(t[1]) for t in telemetry],
+                          "skip": [int(t[2]) for t in telemetry],
+                          "source": "pointwise GPU mode (bit-exact with hjsvd.drive)"}
+    os.makedirs(os.path.dirname(TELEMETRY_FILE), exist_ok=True)
+    with open(TELEMETRY_FILE, "w") as f:
+        json.dump(data, f, indent=1)
+
+
+def cpu_reference_estimate(G, signs, p, budget_s, threads, telemetry):
+    """Time the reference algorithm (C restatement, oracle/) on the host:
+    sample A = the first modulus steps of sweep 0 on G (nearly all pairs
+    rotate), sample B = the same steps on an orthogonal factor (I, every
+    pair skips).  Per-visit costs c_rot, c_skip then price the exact
+    per-sweep rotation/skip counts of the full solve."""
+    from oracle import oracle as O
+    n, r = G.shape
+    half = r // 2
+    # calibrate the step count to the budget
+    _, t1 = O.sample_steps(G, signs, p, 2, threads)
+    per_step = max(t1 / 2, 1e-4)
+    steps_a = int(max(2, min(r, 0.7 * budget_s / per_step)))
+    rot_a, ta = O.sample_steps(G, signs, p, steps_a, threads)
+    Id = np.asfortranarray(np.eye(n, r))
+    _, t1b = O.sample_steps(Id, signs, p, 2, threads)
+    steps_b = int(max(2, min(r, 0.3 * budget_s / max(t1b / 2, 1e-4))))
+    _, tb = O.sample_steps(Id, signs, p, steps_b, threads)
+    c_skip = tb / (steps_b * half)
+    skip_a = steps_a * half - rot_a
+    c_rot = max((ta - skip_a * c_skip) / max(rot_a, 1), c_skip)
+    if telemetry is not None:
+        rot = sum(telemetry["rot"])
+        skip = sum(telemetry["skip"])
+        sweeps = telemetry["sweeps"]
+        how = "exact per-sweep rotation/skip counts of this input"
+    else:  # no telemetry yet: every visit of 14 sweeps rotates (upper bound)
+        sweeps = 14
+        rot, skip = sweeps * r * half, 0
+        how = "assumed 14 sweeps, every visit rotating (upper bound)"
+    est = rot * c_rot + skip * c_skip
+    sample = (f"oracle C restatement (bit-exact with hjsvd), {threads} threads: "
+              f"{steps_a} steps of sweep 0 on G ({ta:.1f} s) + {steps_b} all-skip steps "
+              f"on I ({tb:.1f} s) -> c_rot={c_rot*1e6:.2f} us, c_skip={c_skip*1e6:.2f} us "
+              f"per pair visit; extrapolated with {how}: {rot} rotations + {skip} skips "
+              f"over {sweeps} sweeps")
+    return est, sample
+
+
+def run_reference(a, rank, world):
+    """--impl reference: CPU time of the reference algorithm, rank 0 only."""
+    if rank != 0:
+        return
+    G, signs = make_input(a.n, a.p)
+    threads = cpu_threads()
+    tele = load_reference_telemetry(a.n, a.p)
+    vals = []
+    sample = ""
+    for _ in range(a.warmup if a.warmup < 1 else 1):
+        cpu_reference_estimate(G, signs, a.p, 2.0, threads, tele)  # warm caches
+    budget = max(6.0, min(a.cpu_sample_s, 150.0 / max(a.steps, 1)))
+    for _ in range(a.steps):
+        v, sample = cpu_reference_estimate(G, signs, a.p, budget, threads, tele)
+        vals.append(v)
+    v = float(np.mean(vals))
+    line = {
+        "impl": "reference", "metric": METRIC.format(n=a.n), "value": v, "unit": "s",
+        "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: numpy default_rng(0).standard_normal((n,n)), J=diag(+1 x p, -1 x n-p)",
+        "config": {"workload": f"n={a.n} p={a.p} full HSVD with V^-T (SURVEY.md §8(d) cfg 5)",
+                   "n": a.n, "p": a.p},
+        "cpu_baseline": {"value": v, "unit": "s", "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- GPU leg
+
+
+def residuals(Gdev_orig_t, res, signs):
+    """||U^T U - I||_F, ||V^T J V - J||_F/||V||^2, ||G - U S V^T||_F/||G||_F
+    on the device in fp64 (torch matmul; validation only)."""
+    import torch
+    Ut = res.U  # (r, n): row c = column c of U
+    r = Ut.shape[0]
+    eye = torch.eye(r, dtype=torch.float64, device=Ut.device)
+    dU = torch.linalg.norm(Ut @ Ut.t() - eye).item()
+    out = {"dU": dU}
+    if res.Vinv_t is not None:
+        s = torch.as_tensor(signs.astype(np.float64), device=Ut.device)
+        Vt_cols = res.Vinv_t  # row c = column c of V^{-T}
+        V = (s[:, None] * Vt_cols.t() * s[None, :])  # V = J V^{-T} J (n x n, row-major)
+        vjv = V.t() @ (s[:, None] * V) - torch.diag(s)
+        out["VtJV"] = (torch.linalg.norm(vjv) / torch.linalg.norm(V) ** 2).item()
+        US = Ut.t() * res.sigma[None, :]
+        recon = US @ V.t()
+        G = Gdev_orig_t.t()
+        out["recon"] = (torch.linalg.norm(G - recon) / torch.linalg.norm(G)).item()
+    return out
+
+
+def run_ours(a, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1008_1371_b200 as H
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    G, signs = make_input(a.n, a.p, seed=0)
+    J = H.SignatureVector(signs, a.p)
+    cfg = H.SolverConfig(mode=a.mode, block_cols=a.block_cols)
+    G0 = torch.from_numpy(np.ascontiguousarray(G.T)).to(dev)  # (r, n) = col-major G
+    Gw = torch.empty_like(G0)
+    stream = torch.cuda.current_stream()
+
+    def solve():
+        Gw.copy_(G0)
+        return H.drive_device(Gw, J, cfg)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    res = None
+    for _ in range(a.warmup):
+        res = solve()
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    clk = ClockSampler(local_rank)
+    clk.start()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    launches = 0
+    sweep_ms = []
+    for _ in range(a.steps):
+        res = solve()
+        launches += res.gpu_launches
+        sweep_ms.append(res.sweep_gpu_ms)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / a.steps
+    value = ms_per_step / 1e3
+
+    # ---- roofline of the dominant kernel class -------------------------
+    n = r = a.n
+    tele = res.telemetry
+    if a.mode == "pointwise":
+        # per rotated pair: read+write 2 G columns + 2 V columns; per skip:
+        # read 2 G columns; sweep time is ~all step kernels
+        alg_bytes = sum(t[1] * (32 * n + 32 * r) + t[2] * 16 * n for t in tele)
+        kern_s = sum(res.sweep_gpu_ms) / 1e3
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) \
+            if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+        peak = float(peaks.get("hbm_gbs", 6650.0))
+        achieved = alg_bytes / kern_s / 1e9
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak, "traffic": None,
+                    "kernel": "k_pointwise_step (whole sweep graph, CUDA events)",
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s",
+                    "algorithmic_bytes_per_solve": alg_bytes,
+                    "kernel_s_per_solve": kern_s}
+        if rank == 0 and a.n >= 1024:
+            save_reference_telemetry(a.n, a.p, tele)
+    else:
+        roofline = getattr(res, "roofline", None)
+
+    # ---- end to end through the public numpy API -------------------------
+    e2e_ms = []
+    for _ in range(max(a.e2e_steps, 1)):
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        e0.record(stream)
+        out = H.drive(G, J, cfg)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        wall = (time.perf_counter() - t0) * 1e3
+        e2e_ms.append(max(e0.elapsed_time(e1), wall))
+    e2e_s = float(np.mean(e2e_ms)) / 1e3
+    if world > 1:
+        t = torch.tensor([e2e_s], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    h2d = n * r * 8 + r
+    d2h = (n * r + r * r + 2 * r) * 8
+
+    acc = None
+    if not a.no_accuracy:
+        res = solve()
+        acc = residuals(G0, res, signs)
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu:
+        tel = load_reference_telemetry(a.n, a.p)
+        est, sample = cpu_reference_estimate(G, signs, a.p, a.cpu_sample_s,
+                                             cpu_threads(), tel)
+        cpu = {"value": est, "unit": "s", "cores": cpu_threads(), "kind": "port",
+               "sample": sample}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC.format(n=a.n), "value": value, "unit": "s",
+            "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": ms_per_step, "higher_is_better": False,
+            "scaling": "weak" if world > 1 else "strong",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: numpy default_rng(0).standard_normal((n,n)), J=diag(+1 x p, -1 x n-p)",
+            "config": {"workload": f"n={a.n} p={a.p} full HSVD with V^-T (SURVEY.md §8(d) cfg 5)",
+                       "n": a.n, "p": a.p, "mode": a.mode,
+                       "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                       "l2": "inputs larger than L2 (G and V^-T are n*n*8 B each)"},
+            "sweeps": res.sweeps_used, "stop_reason": res.stop_reason,
+            "rotations": res.rotations, "skips": res.skips,
+            "accuracy": acc,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches,
+            "clocks": clocks,
+            "sweep_gpu_ms": [round(x, 3) for x in sweep_ms[-1]],
+        }
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    a = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if a.impl == "reference":
+        run_reference(a, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(a, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,187 @@
+/*
+ * hsvd_b200.h -- C ABI of the B200-native one-sided hyperbolic Jacobi HSVD.
+ *
+ * Plain pointers, sizes and a CUDA stream (passed as void*); no C++ or torch
+ * types cross this boundary.  Every matrix is float64 column-major with an
+ * explicit leading dimension; every pointer argument is a DEVICE pointer
+ * unless its name ends in _host.  Return value: HSVD_OK (0), a positive
+ * algorithmic status mirroring the reference's exceptions, or a negative
+ * CUDA/usage error with a message in hsvd_last_error().
+ *
+ * Each entry point replaces one function of the reference package
+ * (/root/reference/pkg/src/hjsvd/...), cited per declaration.  The Python
+ * host package paper_1008_1371_b200 binds these with ctypes; INTEGRATION.md
+ * shows the binding a maintainer would add to the reference itself.
+ */
+#ifndef HSVD_B200_H
+#define HSVD_B200_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define HSVD_API __attribute__((visibility("default")))
+#else
+#define HSVD_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (errors.py:4-30) ------------------------------------- */
+#define HSVD_OK 0
+#define HSVD_DEFINITENESS_LOST 1 /* DefinitenessLostError(block, i, j)   */
+#define HSVD_RANK_DEFICIENT 2    /* RankDeficiencyError (zero column)     */
+#define HSVD_SHAPE_ERROR 3       /* ShapeError                            */
+#define HSVD_ERR_CUDA (-1)
+#define HSVD_ERR_ARG (-2)
+#define HSVD_ERR_UNSUPPORTED (-3)
+
+/* ---- solver modes ------------------------------------------------------ */
+#define HSVD_MODE_POINTWISE 0 /* bit-exact mirror of the reference          */
+#define HSVD_MODE_BLOCK 1     /* block-column pairs, FP64 DMMA Gram/update  */
+
+/* ---- schedules (solver.py:204-209) ------------------------------------- */
+#define HSVD_SCHEDULE_MODULUS 0
+#define HSVD_SCHEDULE_ROW_CYCLIC 1
+
+/* Solver knobs: SolverConfig (solver.py:46-64) plus the B200 additions. */
+typedef struct hsvd_config {
+    int64_t max_sweeps;   /* 30                                           */
+    double eps;           /* 2^-52                                        */
+    double teps;          /* sqrt(eps)/2                                  */
+    int32_t accumulate_v; /* 1                                            */
+    int32_t use_skip;     /* use_rel_orth_skip, 1                         */
+    int64_t chunk;        /* 32 (DEFAULT_CHUNK, linalg.py:20)             */
+    int32_t schedule;     /* HSVD_SCHEDULE_*                              */
+    int32_t sort;         /* 1                                            */
+    int32_t mode;         /* HSVD_MODE_*                                  */
+    int32_t block_cols;   /* block mode: b, columns per block (32 or 64)  */
+    int32_t inner_full;   /* block mode: 1 = full inner pass every step   */
+    int32_t use_graph;    /* capture each sweep as a CUDA graph           */
+} hsvd_config;
+
+/* Per-run result record: the scalar part of HsvdResult (solver.py:67-77). */
+typedef struct hsvd_result {
+    int64_t sweeps_used;
+    int32_t stop_reason; /* 0 orthogonal, 1 quadratic, 2 max_sweeps   */
+    int32_t status;      /* HSVD_* of the run                          */
+    int64_t rotations;
+    int64_t skips;
+    int64_t err[3];      /* (block, i, j) or (column, -1, -1)          */
+    int64_t launches;    /* kernels this library launched for the run   */
+} hsvd_result;
+
+/* Per-sweep telemetry row (solver.py:247): (sweep, rot, skip, max|t|). */
+typedef struct hsvd_telemetry {
+    int64_t sweep;
+    int64_t rotations;
+    int64_t skips;
+    double max_t;
+    double gpu_ms;     /* device time of the sweep (CUDA events on the
+                          launching stream): steps + reduction + sort    */
+} hsvd_telemetry;
+
+HSVD_API const char *hsvd_last_error(void);
+HSVD_API int hsvd_version(void);
+HSVD_API void hsvd_default_config(hsvd_config *cfg);
+
+/* ---- reference-kernel mirrors ------------------------------------------ */
+
+/* _kernels.dot_chunked (_kernels.py:32-59): *out (device) = x.y with
+ * chunk-sequential FMA partials and the adjacent-pair tree; bit-exact. */
+HSVD_API int hsvd_dot_chunked(const double *x, const double *y, int64_t n,
+                     int64_t chunk, double *out, void *stream);
+
+/* _kernels.fused_pair_update (_kernels.py:62-75), in place. */
+HSVD_API int hsvd_fused_pair_update(double *x, double *y, int64_t n, double t, double c,
+                           double s, void *stream);
+
+/* _kernels.rotation_batch (_kernels.py:176-185): t[k], c[k] per entry;
+ * *first_bad (device int64) = first failing index or -1. */
+HSVD_API int hsvd_rotation_batch(const double *a_ii, const double *a_jj,
+                        const double *a_ij, const int64_t *hyp, int64_t m,
+                        double *t, double *c, int64_t *first_bad,
+                        void *stream);
+
+/* solver.precompute (solver.py:80-94): d[k] = dot_chunked(g_k, g_k);
+ * *first_zero (device int64) = first zero column or -1. */
+HSVD_API int hsvd_precompute(const double *G, int64_t n, int64_t r, int64_t ldg,
+                    int64_t chunk, double *d, int64_t *first_zero,
+                    void *stream);
+
+/* _kernels.step_blocks (_kernels.py:188-235) over slots [k0, k1) of one
+ * step, all slots concurrently (one CTA per slot).  V may be NULL.
+ * rotk/skipk (uint32[k1]) and maxt (double[k1]) are per-slot counters that
+ * are incremented / max-ed; *err_packed (device uint64) is atomically
+ * min-ed with the packed (block, i, j) of a failing slot and, when not ~0
+ * on entry, makes the launch a no-op.  If advance != 0 each slot then
+ * advances its stepper quadruple (ip, jp, iblk, jblk), fusing
+ * _kernels.advance_stepper (_kernels.py:238-251). */
+HSVD_API int hsvd_step_blocks(double *G, int64_t n, int64_t ldg, double *V, int64_t rv,
+                     int64_t ldv, double *d, const int64_t *rho,
+                     const int64_t *jsign, int64_t *ip, int64_t *jp,
+                     int64_t *iblk, int64_t *jblk, int64_t r, uint8_t *C,
+                     int64_t k0, int64_t k1, double eps, double teps,
+                     int32_t use_skip, int64_t chunk, int32_t advance,
+                     uint32_t *rotk, uint32_t *skipk, double *maxt,
+                     uint64_t *err_packed, void *stream);
+
+/* _kernels.advance_stepper (_kernels.py:238-251). */
+HSVD_API int hsvd_advance_stepper(int64_t *ip, int64_t *jp, int64_t *iblk,
+                         int64_t *jblk, int64_t nblk, int64_t r, void *stream);
+
+/* strategies.stepper_init (strategies.py:41-47). */
+HSVD_API int hsvd_stepper_init(int64_t *ip, int64_t *jp, int64_t *iblk, int64_t *jblk,
+                      int64_t r, void *stream);
+
+/* solver.sort_diagonal (solver.py:97-110): stable, [0,p) descending,
+ * [p,r) ascending; rho and jsign travel.  ws: 24*r bytes of device scratch. */
+HSVD_API int hsvd_sort_diagonal(double *d, int64_t *rho, int64_t *jsign, int64_t r,
+                       int64_t p, void *ws, void *stream);
+
+/* solver.check_convergence (solver.py:113-121) fused with the per-sweep
+ * statistics merge of _run_ranges (solver.py:147-156): OR of C[0..m),
+ * sums of rotk/skipk and max of maxt over nslots, written to out (device):
+ * out = {code, rotations, skips, max_t bits}.  reset != 0 zeroes C and the
+ * counters afterwards. */
+HSVD_API int hsvd_reduce_sweep(uint8_t *C, int64_t m, uint32_t *rotk, uint32_t *skipk,
+                      double *maxt, int64_t nslots, int64_t *out,
+                      int32_t reset, void *stream);
+
+/* Result extraction (solver.py:261-267): sigma[rho]=sqrt(d), lam[rho]=d*j,
+ * U[:,c] = G[:,c] / sigma[c] (in place on G, true division). */
+HSVD_API int hsvd_extract(double *G, int64_t n, int64_t ldg, const double *d,
+                 const int64_t *rho, const int64_t *jsign, int64_t r,
+                 double *sigma, double *lam, void *stream);
+
+/* ---- whole solver ------------------------------------------------------- */
+
+/* Device scratch bytes hsvd_drive needs for (n, r, cfg). */
+HSVD_API int64_t hsvd_drive_workspace_size(int64_t n, int64_t r, const hsvd_config *cfg);
+
+/* solver.drive (solver.py:179-269) entirely on the device: G (n x r, ldg)
+ * is overwritten by U; Vinv_t (r x r, ldv) receives V^{-T} if
+ * cfg->accumulate_v; sigma/lam receive the results in original column
+ * order; res_host / tele_host (max_sweeps rows, may be NULL) are host
+ * memory.  signs_host: int8 +-1 with the p +1 entries leading. */
+HSVD_API int hsvd_drive(double *G, int64_t n, int64_t r, int64_t ldg, double *Vinv_t,
+               int64_t ldv, const int8_t *signs_host, int64_t p,
+               const hsvd_config *cfg, double *sigma, double *lam,
+               void *workspace, int64_t workspace_bytes,
+               hsvd_result *res_host, hsvd_telemetry *tele_host,
+               void *stream);
+
+/* Same as hsvd_drive on HOST buffers (G_host is read, not modified):
+ * allocates device memory, copies in, solves, copies U, V^{-T}, sigma, lam
+ * back.  The e2e entry a ctypes/cffi binding of the reference would call. */
+HSVD_API int hsvd_drive_host(const double *G_host, int64_t n, int64_t r,
+                    const int8_t *signs_host, int64_t p,
+                    const hsvd_config *cfg, double *U_host,
+                    double *Vinv_t_host, double *sigma_host, double *lam_host,
+                    hsvd_result *res_host, hsvd_telemetry *tele_host);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HSVD_B200_H */

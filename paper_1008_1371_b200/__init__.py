@@ -1,0 +1,62 @@
+"""paper_1008_1371_b200 -- B200-native one-sided Jacobi hyperbolic SVD.
+
+Drop-in for the hot path of the reference package ``hjsvd``:
+``drive(G, J, cfg) -> HsvdResult`` with the same names, fields, defaults and
+exceptions (/root/reference/pkg/src/hjsvd/__init__.py:9-81, solver part).
+All numerics run in hand-written sm_100a CUDA (lib/libhsvd_b200.so, C ABI
+in include/hsvd_b200.h); there is no CPU fallback.
+"""
+
+from .errors import (
+    DefinitenessLostError,
+    HsvdCudaError,
+    NumericalSingularityError,
+    RankDeficiencyError,
+    ShapeError,
+)
+from .linalg import (
+    DEFAULT_CHUNK,
+    EPS,
+    SignatureVector,
+    as_factor,
+    dot_chunked,
+    fused_pair_update,
+    orthonormality_distance,
+)
+from .rotation import (
+    CODE_BIG,
+    CODE_NONE,
+    CODE_SMALL,
+    TEPS,
+    PivotGram,
+    Rotation,
+    compute_rotation,
+    convergence_code,
+    diagonal_update_predicted,
+    relatively_orthogonal,
+    rotation_params_batch,
+)
+from .solver import (
+    BorderInfo,
+    DiagonalPackageVector,
+    HsvdResult,
+    SolverConfig,
+    border,
+    check_convergence,
+    drive,
+    drive_device,
+    jacobi_step,
+    precompute,
+    recover_V,
+    sort_diagonal,
+    strip_bordered,
+)
+from .strategies import (
+    StepperState,
+    schedule_table,
+    stepper_advance,
+    stepper_advance_all,
+    stepper_init,
+)
+
+__version__ = "0.1.0"

@@ -1,0 +1,74 @@
+// hsvd_internal.cuh -- shared device helpers of the B200 HSVD library.
+//
+// Compiled into the pointwise (bit-exact) translation unit with
+// -fmad=false: every a*b+c that the reference evaluates with two roundings
+// stays two roundings, and fma() appears exactly where the reference calls
+// its llvm.fma intrinsic (/root/reference/pkg/src/hjsvd/_kernels.py:17-29).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/hsvd_b200.h"
+
+namespace hsvd {
+
+// ---- error plumbing (host) ----------------------------------------------
+void set_error(const std::string &msg);
+int cuda_fail(cudaError_t e, const char *what);
+
+#define HSVD_CUDA(call)                                   \
+    do {                                                  \
+        cudaError_t _e = (call);                          \
+        if (_e != cudaSuccess) return hsvd::cuda_fail(_e, #call); \
+    } while (0)
+
+#define HSVD_LAUNCH_CHECK(what)                                   \
+    do {                                                          \
+        cudaError_t _e = cudaGetLastError();                      \
+        if (_e != cudaSuccess) return hsvd::cuda_fail(_e, what);  \
+    } while (0)
+
+constexpr unsigned long long kNoError = ~0ull;
+
+// Packed (block, i, j) error word; min over failing slots = first slot.
+__host__ __device__ inline unsigned long long pack_err(int64_t k, int64_t i,
+                                                       int64_t j)
+{
+    return ((unsigned long long)k << 42) | ((unsigned long long)i << 21) |
+           (unsigned long long)j;
+}
+inline void unpack_err(unsigned long long w, int64_t *out)
+{
+    out[0] = (int64_t)(w >> 42);
+    out[1] = (int64_t)((w >> 21) & ((1ull << 21) - 1));
+    out[2] = (int64_t)(w & ((1ull << 21) - 1));
+}
+
+// Smem column layout: one pad double per 32 so that the chunk-sequential
+// reads of a warp (lane c reads element 32c+q) are bank-conflict free.
+__host__ __device__ inline int padx(int e) { return e + (e >> 5); }
+__host__ __device__ inline int padded_len(int n) { return n + (n >> 5) + 1; }
+
+// ---- host-side launch helpers (defined in hsvd_pointwise.cu) -------------
+int launch_pointwise_step(double *G, int64_t n, int64_t ldg, double *V,
+                          int64_t rv, int64_t ldv, double *d,
+                          const int64_t *rho, const int64_t *jsign,
+                          int64_t *ip, int64_t *jp, int64_t *iblk,
+                          int64_t *jblk, int64_t r, uint8_t *C, int64_t k0,
+                          int64_t k1, double eps, double teps, int use_skip,
+                          int64_t chunk, int advance, uint32_t *rotk,
+                          uint32_t *skipk, double *maxt,
+                          unsigned long long *err, cudaStream_t s);
+int launch_rowcyclic_sweep(double *G, int64_t n, int64_t ldg, double *V,
+                           int64_t rv, int64_t ldv, double *d,
+                           const int64_t *rho, const int64_t *jsign,
+                           int64_t r, uint8_t *C, double eps, double teps,
+                           int use_skip, int64_t chunk, uint32_t *rotk,
+                           uint32_t *skipk, double *maxt,
+                           unsigned long long *err, cudaStream_t s);
+int pointwise_smem_bytes(int64_t n, int64_t chunk, size_t *bytes);
+
+}  // namespace hsvd
