@@ -47,7 +47,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=8192)
     ap.add_argument("--p", type=int, default=None)
-    ap.add_argument("--mode", default="pointwise", choices=["pointwise", "block"])
+    ap.add_argument("--mode", default="block", choices=["pointwise", "block"])
     ap.add_argument("--block-cols", type=int, default=32)
     ap.add_argument("--cpu-sample-s", type=float, default=12.0)
     ap.add_argument("--e2e-steps", type=int, default=1)
@@ -148,12 +148,14 @@ def save_reference_telemetry(n, p, telemetry):
         with open(TELEMETRY_FILE) as f:
             data = json.load(f)
     data[f"n{n}_p{p}"] = {"sweeps": len(telemetry),
-                          "rot": [int(t[1]) for t in telemetry],
-                          "skip": [int(t[2]) for t in telemetry],
+                          "rotations": sum(int(t[1]) for t in telemetry),
+                          "skips": sum(int(t[2]) for t in telemetry),
+                          "per_sweep": [[int(t[1]), int(t[2])] for t in telemetry],
                           "source": "pointwise GPU mode (bit-exact with hjsvd.drive)"}
-    os.makedirs(os.path.dirname(TELEMETRY_FILE), exist_ok=True)
-    with open(TELEMETRY_FILE, "w") as f:
-        json.dump(data, f, indent=1)
+    for path in (TELEMETRY_FILE, os.path.join(ROOT, "gpurun_out", "reference_telemetry.json")):
+        if os.path.isdir(os.path.dirname(path)):
+            with open(path, "w") as f:
+                json.dump(data, f, indent=1)
 
 
 def cpu_reference_estimate(G, signs, p, budget_s, threads, telemetry):
@@ -178,8 +180,8 @@ def cpu_reference_estimate(G, signs, p, budget_s, threads, telemetry):
     skip_a = steps_a * half - rot_a
     c_rot = max((ta - skip_a * c_skip) / max(rot_a, 1), c_skip)
     if telemetry is not None:
-        rot = sum(telemetry["rot"])
-        skip = sum(telemetry["skip"])
+        rot = telemetry["rotations"]
+        skip = telemetry["skips"]
         sweeps = telemetry["sweeps"]
         how = "exact per-sweep rotation/skip counts of this input"
     else:  # no telemetry yet: every visit of 14 sweeps rotates (upper bound)
@@ -262,6 +264,8 @@ def run_ours(a, rank, world, local_rank):
     G, signs = make_input(a.n, a.p, seed=0)
     J = H.SignatureVector(signs, a.p)
     cfg = H.SolverConfig(mode=a.mode, block_cols=a.block_cols)
+    if a.mode == "block" and a.n % (2 * a.block_cols):
+        raise SystemExit("block mode needs n to be a multiple of 2*block_cols")
     G0 = torch.from_numpy(np.ascontiguousarray(G.T)).to(dev)  # (r, n) = col-major G
     Gw = torch.empty_like(G0)
     stream = torch.cuda.current_stream()
@@ -291,6 +295,7 @@ def run_ours(a, rank, world, local_rank):
         res = solve()
         launches += res.gpu_launches
         sweep_ms.append(res.sweep_gpu_ms)
+    res_timed = res
     ev1.record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -304,28 +309,64 @@ def run_ours(a, rank, world, local_rank):
     ms_per_step = ms / a.steps
     value = ms_per_step / 1e3
 
-    # ---- roofline of the dominant kernel class -------------------------
+    # ---- roofline of the dominant kernel ---------------------------------
+    # One extra solve limited to sweep 0 in profile mode: CUDA events around
+    # every launch on the library's launching stream (outside the timed run).
     n = r = a.n
     tele = res.telemetry
+    prof = H.drive_device(Gw.copy_(G0), J, H.SolverConfig(
+        mode=a.mode, block_cols=a.block_cols, max_sweeps=1, profile=True))
+    kp = prof.kernel_profile
+    peaks = {}
+    if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")):
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    traffic = {}
+    if os.path.exists(os.path.join(ROOT, "profiles", "traffic.json")):
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
     if a.mode == "pointwise":
+        t0 = prof.telemetry[0]
         # per rotated pair: read+write 2 G columns + 2 V columns; per skip:
-        # read 2 G columns; sweep time is ~all step kernels
-        alg_bytes = sum(t[1] * (32 * n + 32 * r) + t[2] * 16 * n for t in tele)
-        kern_s = sum(res.sweep_gpu_ms) / 1e3
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) \
-            if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+        # read 2 G columns
+        bytes_per_launch = (t0[1] * (32 * n + 32 * r) + t0[2] * 16 * n) / r
+        avg_s = kp["step"]["ms"] / kp["step"]["launches"] / 1e3
         peak = float(peaks.get("hbm_gbs", 6650.0))
-        achieved = alg_bytes / kern_s / 1e9
+        achieved = bytes_per_launch / avg_s / 1e9
+        tr = traffic.get(f"pointwise_n{n}")
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                    "frac": achieved / peak, "traffic": None,
-                    "kernel": "k_pointwise_step (whole sweep graph, CUDA events)",
-                    "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s",
-                    "algorithmic_bytes_per_solve": alg_bytes,
-                    "kernel_s_per_solve": kern_s}
+                    "frac": achieved / peak, "traffic": tr,
+                    "kernel": "k_pointwise_step", "launch_avg_ms": avg_s * 1e3,
+                    "alg_bytes_per_launch": bytes_per_launch,
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s"}
         if rank == 0 and a.n >= 1024:
             save_reference_telemetry(a.n, a.p, tele)
     else:
-        roofline = getattr(res, "roofline", None)
+        b2 = 2 * a.block_cols
+        nslots = n // b2
+        fl = {"gram": 2.0 * n * b2 * b2 * nslots,          # A_P = G_P^T G_P per slot
+              "update": 2.0 * (n + r) * b2 * b2 * nslots}  # [G_P; V_P] W_P per slot
+        dom = max(("gram", "update"), key=lambda k: kp[k]["ms"])
+        avg_s = kp[dom]["ms"] / kp[dom]["launches"] / 1e3
+        fp64 = {}
+        pk = os.path.join(ROOT, "profiles", "r01_fp64_dgemm_peak.json")
+        if os.path.exists(pk):
+            fp64 = json.load(open(pk))
+        peak = float(fp64.get("fp64_tflops", 37.0))
+        achieved = fl[dom] / avg_s / 1e12
+        tot_ms = sum(v["ms"] for v in kp.values())
+        solve_tflops = res.sweeps_used * 12.0 * n ** 3 / value / 1e12
+        roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                    "frac": achieved / peak, "traffic": traffic.get(f"{dom}_n{n}_b{a.block_cols}"),
+                    "kernel": f"k_{dom}", "launch_avg_ms": avg_s * 1e3,
+                    "alg_flop_per_launch": fl[dom],
+                    "peak_source": ("cuBLAS DGEMM 8192^3 measured on this pool "
+                                    "(profiles/r01_fp64_dgemm_peak.json); DMMA microbench 37.1 "
+                                    "(profiles/r01_fp64_micro.jsonl)") if fp64 else "nominal 37",
+                    "kernel_share_sweep0": {k: round(v["ms"] / tot_ms, 4) for k, v in kp.items()},
+                    "kernel_ms_sweep0": {k: round(v["ms"], 3) for k, v in kp.items()},
+                    "gram_tflops": fl["gram"] / (kp["gram"]["ms"] / kp["gram"]["launches"] / 1e3) / 1e12,
+                    "update_tflops": fl["update"] / (kp["update"]["ms"] / kp["update"]["launches"] / 1e3) / 1e12,
+                    "solve_alg_tflops": solve_tflops,
+                    "solve_frac": solve_tflops / peak}
 
     # ---- end to end through the public numpy API -------------------------
     e2e_ms = []
@@ -381,6 +422,7 @@ def run_ours(a, rank, world, local_rank):
             "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
+            "host_phase_ms": res_timed.host_phase_ms,
             "clocks": clocks,
             "sweep_gpu_ms": [round(x, 3) for x in sweep_ms[-1]],
         }

@@ -59,6 +59,8 @@ typedef struct hsvd_config {
     int32_t block_cols;   /* block mode: b, columns per block (32 or 64)  */
     int32_t inner_full;   /* block mode: 1 = full inner pass every step   */
     int32_t use_graph;    /* capture each sweep as a CUDA graph           */
+    int32_t profile;      /* time every kernel of sweep 0 with CUDA events
+                             (no graph); fills hsvd_result.kernel_ms     */
 } hsvd_config;
 
 /* Per-run result record: the scalar part of HsvdResult (solver.py:67-77). */
@@ -70,6 +72,13 @@ typedef struct hsvd_result {
     int64_t skips;
     int64_t err[3];      /* (block, i, j) or (column, -1, -1)          */
     int64_t launches;    /* kernels this library launched for the run   */
+    double setup_ms;     /* host wall: entry -> first sweep launched     */
+    double sweeps_ms;    /* host wall: all sweeps incl. stop decisions   */
+    double finish_ms;    /* host wall: extraction + teardown             */
+    /* profile mode, sweep 0: device time and launches per kernel class
+       [0] step / gram, [1] inner, [2] update, [3] sweep-end kernels   */
+    double kernel_ms[4];
+    int64_t kernel_launches[4];
 } hsvd_result;
 
 /* Per-sweep telemetry row (solver.py:247): (sweep, rot, skip, max|t|). */

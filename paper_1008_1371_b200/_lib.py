@@ -49,6 +49,7 @@ class HsvdConfigC(ctypes.Structure):
         ("block_cols", ctypes.c_int32),
         ("inner_full", ctypes.c_int32),
         ("use_graph", ctypes.c_int32),
+        ("profile", ctypes.c_int32),
     ]
 
 
@@ -61,6 +62,11 @@ class HsvdResultC(ctypes.Structure):
         ("skips", ctypes.c_int64),
         ("err", ctypes.c_int64 * 3),
         ("launches", ctypes.c_int64),
+        ("setup_ms", ctypes.c_double),
+        ("sweeps_ms", ctypes.c_double),
+        ("finish_ms", ctypes.c_double),
+        ("kernel_ms", ctypes.c_double * 4),
+        ("kernel_launches", ctypes.c_int64 * 4),
     ]
 
 

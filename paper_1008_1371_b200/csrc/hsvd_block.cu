@@ -1,14 +1,789 @@
-// hsvd_block.cu -- block-column mode (placeholder until the DMMA path lands).
+// hsvd_block.cu -- block-column one-sided hyperbolic Jacobi on sm_100a.
+//
+// The pivot unit is a pair of block columns P = [B_I B_J] (b columns each,
+// positions [I*b, I*b+b) and [J*b, J*b+b) of the sorted package order,
+// gathered through rho as the reference addresses columns, solver.py:26-43).
+// One step of the modified-modulus schedule on the r/b block indices
+// (strategies.py:41-72) processes all r/(2b) slots with three kernels:
+//
+//   k_gram    A_P = G_P^T G_P (2b x 2b), FP64 tensor cores (mma.sync
+//             m8n8k4 -> SASS DMMA.8x8x4) fed by cp.async multi-stage smem
+//             pipelines; split-K over CTAs, upper-triangle tiles only,
+//             partials reduced in fixed order by the next kernel.
+//   k_inner   one CTA per slot: sums the split-K partials, runs one pass of
+//             2x2 rotations on (A_P, J_P) in shared memory -- each 2x2
+//             rotation is the reference's double-double rotation_tc
+//             (_kernels.py:128-173), trig or hyperbolic from the signs, with
+//             the relative-orthogonality skip (_kernels.py:211) -- and
+//             accumulates the J-orthogonal W_P; writes convergence codes and
+//             statistics, advances the stepper.
+//   k_update  [G_P; V_P] <- [G_P; V_P] W_P, FP64 tensor cores, in place.
+//
+// The inner pass uses the paper's block-oriented ordering:
+// the full 2b(2b-1)/2 pairs at the first step of a sweep (each diagonal
+// block meets itself once per sweep), only the b^2 cross pairs I x J at the
+// other steps.  Per sweep the algorithm therefore applies the same pair
+// visits as the pointwise method, in blocked order.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <string>
+
 #include "hsvd_internal.cuh"
+#include "hsvd_rotation.cuh"
 
 namespace hsvd {
-int64_t block_workspace_size(int64_t, int64_t, const hsvd_config *) { return 256; }
-int block_drive(double *, int64_t, int64_t, int64_t, double *, int64_t,
-                const int8_t *, int64_t, const hsvd_config *, double *,
-                double *, void *, int64_t, hsvd_result *, hsvd_telemetry *,
-                cudaStream_t)
+
+// ---------------------------------------------------------------------
+// PTX helpers
+// ---------------------------------------------------------------------
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem, int src_bytes)
 {
-    set_error("block mode not built yet");
-    return HSVD_ERR_UNSUPPORTED;
+    unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem),
+                 "r"(src_bytes));
 }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// D(8x8) += A(8x4, row) * B(4x8, col), FP64 tensor core.
+// a = A[lane>>2][lane&3], b = B[lane&3][lane>>2],
+// d = {D[lane>>2][2*(lane&3)], D[lane>>2][2*(lane&3)+1]}.
+__device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b)
+{
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+constexpr int kThreads = 256;
+
+// position of column c (0..2b) of slot P = (I, J), I < J
+__device__ __forceinline__ int64_t slot_pos(int c, int b, int64_t I, int64_t J)
+{
+    return c < b ? I * b + c : J * b + (c - b);
+}
+
+// ---------------------------------------------------------------------
+// k_gram: partial Gram matrices, one CTA per (split, slot)
+// ---------------------------------------------------------------------
+template <int B2, int KT, int STAGES>
+struct GramSmem {
+    static constexpr int LD = KT + 4;  // == 4 mod 16: conflict-free fragments
+    double x[STAGES][B2][LD];
+    const double *col[B2];
+};
+
+template <int B2, int KT, int STAGES>
+__global__ void __launch_bounds__(kThreads, 2) k_gram(
+    const double *__restrict__ G, int64_t ldg, int n, const int64_t *__restrict__ rho,
+    const int64_t *__restrict__ iblk, const int64_t *__restrict__ jblk, int ksplit,
+    int kchunk, double *__restrict__ Apart, const unsigned long long *err)
+{
+    extern __shared__ __align__(16) unsigned char gsm_raw[];
+    auto &S = *reinterpret_cast<GramSmem<B2, KT, STAGES> *>(gsm_raw);
+    if (*(volatile const unsigned long long *)err != kNoError) return;
+    constexpr int b = B2 / 2;
+    const int split = blockIdx.x, slot = blockIdx.y;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    int64_t I = iblk[slot], J = jblk[slot];
+    if (I > J) { int64_t t = I; I = J; J = t; }
+    if (tid < B2) S.col[tid] = G + rho[slot_pos(tid, b, I, J)] * ldg;
+    __syncthreads();
+
+    const int k_lo = split * kchunk;
+    const int k_hi = min(n, k_lo + kchunk);
+    const int ntiles = k_hi > k_lo ? (k_hi - k_lo + KT - 1) / KT : 0;
+
+    // cp.async assignment: B2 columns x KT/2 16-byte chunks per stage
+    constexpr int CHUNKS = B2 * (KT / 2);
+    constexpr int PER_T = (CHUNKS + kThreads - 1) / kThreads;
+    auto load_stage = [&](int st, int tile) {
+        const int k0 = k_lo + tile * KT;
+#pragma unroll
+        for (int u = 0; u < PER_T; ++u) {
+            const int q = tid + u * kThreads;
+            if (q < CHUNKS) {
+                const int c = q / (KT / 2), part = q % (KT / 2);
+                const int k = k0 + 2 * part;
+                const int rem = k_hi - k;
+                const int bytes = rem >= 2 ? 16 : (rem == 1 ? 8 : 0);
+                const double *src = bytes ? S.col[c] + k : S.col[c];
+                cp_async16(&S.x[st][c][2 * part], src, bytes);
+            }
+        }
+    };
+
+    // warp tiling of the B2 x B2 output: 4 warps along M, 2 along N
+    constexpr int WM = B2 / 4, WN = B2 / 2, MI = WM / 8, NI = WN / 8;
+    const int wm = warp >> 1, wn = warp & 1;
+    const int m0 = wm * WM, n0 = wn * WN;
+    double acc[MI][NI][2];
+#pragma unroll
+    for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int j = 0; j < NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    // upper-triangle 8x8 tiles only (A is symmetric)
+    bool live[MI][NI];
+#pragma unroll
+    for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int j = 0; j < NI; ++j) live[i][j] = (m0 + 8 * i) <= (n0 + 8 * j);
+
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+        if (s < ntiles) load_stage(s, s);
+        cp_async_commit();
+    }
+    const int fr = lane >> 2, fk = lane & 3;
+    for (int tile = 0; tile < ntiles; ++tile) {
+        cp_async_wait<STAGES - 2>();
+        __syncthreads();
+        const int nxt = tile + STAGES - 1;
+        if (nxt < ntiles) load_stage(nxt % STAGES, nxt);
+        cp_async_commit();
+        const auto &X = S.x[tile % STAGES];
+#pragma unroll
+        for (int kk = 0; kk < KT; kk += 4) {
+            double a[MI], bb[NI];
+#pragma unroll
+            for (int i = 0; i < MI; ++i) a[i] = X[m0 + 8 * i + fr][kk + fk];
+#pragma unroll
+            for (int j = 0; j < NI; ++j) bb[j] = X[n0 + 8 * j + fr][kk + fk];
+#pragma unroll
+            for (int i = 0; i < MI; ++i)
+#pragma unroll
+                for (int j = 0; j < NI; ++j)
+                    if (live[i][j]) dmma(acc[i][j][0], acc[i][j][1], a[i], bb[j]);
+        }
+    }
+    cp_async_wait<0>();
+    double *out = Apart + ((int64_t)slot * ksplit + split) * (B2 * B2);
+#pragma unroll
+    for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int j = 0; j < NI; ++j)
+            if (live[i][j]) {
+                const int row = m0 + 8 * i + fr, col = n0 + 8 * j + 2 * fk;
+                out[row * B2 + col] = acc[i][j][0];
+                out[row * B2 + col + 1] = acc[i][j][1];
+            }
+}
+
+// ---------------------------------------------------------------------
+// k_inner: one pass of 2x2 rotations on the 2b x 2b pivot Gram
+// ---------------------------------------------------------------------
+struct InnerArgs {
+    const double *Apart;
+    double *Wg;
+    const int64_t *jsign;
+    int64_t *ip, *jp, *iblk, *jblk, *cur;
+    uint8_t *C;
+    uint32_t *rotk, *skipk;
+    double *maxt;
+    unsigned long long *err;
+    int64_t nb;
+    double eps, teps;
+    int ksplit, full, use_skip;
+};
+
+template <int B2>
+struct InnerSmem {
+    static constexpr int LD = B2 + 1;
+    double A[B2][LD];
+    double W[B2][LD];
+    double rt[B2 / 2], rc[B2 / 2], rs[B2 / 2];
+    int pi[B2 / 2], pj[B2 / 2], act[B2 / 2];
+    int js[B2];
+    unsigned int rot, skip, big;
+    unsigned long long maxt_bits;
+    unsigned long long fail;
+};
+
+template <int B2>
+__global__ void __launch_bounds__(kThreads) k_inner(InnerArgs a)
+{
+    extern __shared__ __align__(16) unsigned char ism_raw[];
+    auto &S = *reinterpret_cast<InnerSmem<B2> *>(ism_raw);
+    if (*(volatile unsigned long long *)a.err != kNoError) return;
+    constexpr int b = B2 / 2;
+    const int slot = blockIdx.x, tid = threadIdx.x;
+    int64_t I = a.iblk[slot], J = a.jblk[slot];
+    if (I > J) { int64_t t = I; I = J; J = t; }
+
+    // A = sum of split-K partials (fixed order), upper triangle mirrored
+    const double *P0 = a.Apart + (int64_t)slot * a.ksplit * (B2 * B2);
+    for (int e = tid; e < B2 * B2; e += kThreads) {
+        const int i = e / B2, j = e % B2;
+        const int lo = min(i, j), hi = max(i, j);
+        double v = 0.0;
+        for (int s = 0; s < a.ksplit; ++s) v += P0[(int64_t)s * B2 * B2 + lo * B2 + hi];
+        S.A[i][j] = v;
+        S.W[i][j] = i == j ? 1.0 : 0.0;
+    }
+    if (tid < B2) S.js[tid] = (int)a.jsign[slot_pos(tid, b, I, J)];
+    if (tid == 0) {
+        S.rot = S.skip = S.big = 0;
+        S.maxt_bits = 0;
+        S.fail = kNoError;
+    }
+    __syncthreads();
+
+    const int rounds = a.full ? B2 - 1 : b;
+    unsigned int my_rot = 0, my_skip = 0, my_big = 0;
+    double my_max = 0.0;
+    for (int rd = 0; rd < rounds; ++rd) {
+        // phase 1: the round's b disjoint pairs and their rotations
+        if (tid < b) {
+            int i, j;
+            if (a.full) {  // circle method on B2 players
+                const int m = B2 - 1;
+                if (tid == 0) {
+                    i = m;
+                    j = rd;
+                } else {
+                    i = (rd + tid) % m;
+                    j = (rd - tid + m) % m;
+                }
+            } else {  // block-oriented: round rd pairs i with b + (i + rd) mod b
+                i = tid;
+                j = b + (tid + rd) % b;
+            }
+            if (i > j) { int t = i; i = j; j = t; }
+            S.pi[tid] = i;
+            S.pj[tid] = j;
+            const double a_ii = S.A[i][i], a_jj = S.A[j][j], a_ij = S.A[i][j];
+            int act = 0;
+            if (!(a_ij == 0.0 || (a.use_skip && fabs(a_ij) < a.eps * sqrt(a_ii * a_jj)))) {
+                const int hyp = S.js[i] == S.js[j] ? -1 : 1;
+                double t, c;
+                if (rotation_tc(a_ii, a_jj, a_ij, hyp, t, c) != 0) {
+                    atomicMin(&S.fail, pack_err(slot, slot_pos(i, b, I, J), slot_pos(j, b, I, J)));
+                } else {
+                    act = 1;
+                    S.rt[tid] = t;
+                    S.rc[tid] = c;
+                    S.rs[tid] = hyp < 0 ? -1.0 : 1.0;
+                    ++my_rot;
+                    const double at = fabs(t);
+                    my_big |= at > a.teps;
+                    my_max = fmax(my_max, at);
+                }
+            } else {
+                ++my_skip;
+            }
+            S.act[tid] = act;
+        }
+        __syncthreads();
+        if (S.fail != kNoError) break;
+        // phase 2: columns of A and W (x' = (x + s t y) c, y' = (t x + y) c)
+        for (int e = tid; e < b * B2; e += kThreads) {
+            const int q = e / B2, row = e % B2;
+            if (!S.act[q]) continue;
+            const int i = S.pi[q], j = S.pj[q];
+            const double t = S.rt[q], c = S.rc[q], st = S.rs[q] * t;
+            const double x = S.A[row][i], y = S.A[row][j];
+            S.A[row][i] = fma(st, y, x) * c;
+            S.A[row][j] = fma(t, x, y) * c;
+            const double wx = S.W[row][i], wy = S.W[row][j];
+            S.W[row][i] = fma(st, wy, wx) * c;
+            S.W[row][j] = fma(t, wx, wy) * c;
+        }
+        __syncthreads();
+        // phase 3: rows of A
+        for (int e = tid; e < b * B2; e += kThreads) {
+            const int q = e / B2, col = e % B2;
+            if (!S.act[q]) continue;
+            const int i = S.pi[q], j = S.pj[q];
+            const double t = S.rt[q], c = S.rc[q], st = S.rs[q] * t;
+            const double x = S.A[i][col], y = S.A[j][col];
+            S.A[i][col] = fma(st, y, x) * c;
+            S.A[j][col] = fma(t, x, y) * c;
+        }
+        __syncthreads();
+        if (tid < b && S.act[tid]) {  // annihilated exactly
+            S.A[S.pi[tid]][S.pj[tid]] = 0.0;
+            S.A[S.pj[tid]][S.pi[tid]] = 0.0;
+        }
+        __syncthreads();
+    }
+    if (tid < b) {
+        atomicAdd(&S.rot, my_rot);
+        atomicAdd(&S.skip, my_skip);
+        atomicOr(&S.big, my_big);
+        atomicMax(&S.maxt_bits, (unsigned long long)__double_as_longlong(my_max));
+    }
+    __syncthreads();
+    if (S.fail != kNoError) {
+        if (tid == 0) atomicMin(a.err, S.fail);
+        return;
+    }
+    // W column-major: Wg[slot][c * B2 + k] = W[k][c]
+    double *Wout = a.Wg + (int64_t)slot * B2 * B2;
+    for (int e = tid; e < B2 * B2; e += kThreads) Wout[e] = S.W[e % B2][e / B2];
+    if (tid == 0) {
+        // convergence code (_kernels.py:227-231 semantics per slot)
+        if (S.big) a.C[slot] = 3;
+        else if (S.rot) a.C[slot] |= 1;
+        a.rotk[slot] += S.rot;
+        a.skipk[slot] += S.skip;
+        const double mt = __longlong_as_double((long long)S.maxt_bits);
+        if (mt > a.maxt[slot]) a.maxt[slot] = mt;
+        a.cur[2 * slot] = I;
+        a.cur[2 * slot + 1] = J;
+        // advance_stepper (_kernels.py:238-251) on the block indices
+        const int64_t r = a.nb, half = r / 2;
+        int64_t ip = a.ip[slot], jp = a.jp[slot];
+        if (ip + jp >= r - 1) {
+            ip += 1;
+            if (ip == jp) {
+                ip -= half;
+                jp = ip;
+            }
+            a.ip[slot] = ip;
+            a.jp[slot] = jp;
+            a.iblk[slot] = ip;
+        } else {
+            jp += 1;
+            a.jp[slot] = jp;
+            a.jblk[slot] = jp;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------
+// k_update: [G_P; V_P] <- [G_P; V_P] W_P in place, FP64 tensor cores
+// ---------------------------------------------------------------------
+template <int B2, int MT>
+struct UpdSmem {
+    static constexpr int LDX = MT + 4;  // == 4 mod 16
+    static constexpr int LDW = B2 + 4;
+    double w[B2][LDW];  // w[c][k] = W[k][c]
+    double x[B2][LDX];  // x[k][row]
+    double *col[B2];
+};
+
+template <int B2, int MT>
+__global__ void __launch_bounds__(kThreads, 2) k_update(
+    double *__restrict__ G, int64_t ldg, int n, double *__restrict__ V, int64_t ldv, int rv,
+    const int64_t *__restrict__ rho, const int64_t *__restrict__ cur,
+    const double *__restrict__ Wg, int tiles_g, const unsigned long long *err)
+{
+    extern __shared__ __align__(16) unsigned char usm_raw[];
+    auto &S = *reinterpret_cast<UpdSmem<B2, MT> *>(usm_raw);
+    if (*(volatile const unsigned long long *)err != kNoError) return;
+    constexpr int b = B2 / 2;
+    const int slot = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const bool isV = (int)blockIdx.x >= tiles_g;
+    const int tile = isV ? blockIdx.x - tiles_g : blockIdx.x;
+    const int nrows = isV ? rv : n;
+    const int64_t ld = isV ? ldv : ldg;
+    double *M = isV ? V : G;
+    const int row0 = tile * MT;
+    const int64_t I = cur[2 * slot], J = cur[2 * slot + 1];
+    if (tid < B2) S.col[tid] = M + rho[slot_pos(tid, b, I, J)] * ld;
+    // W (column-major in global) -> w[c][k]
+    const double *Wsrc = Wg + (int64_t)slot * B2 * B2;
+    for (int q = tid; q < B2 * B2 / 2; q += kThreads) {
+        const int c = (2 * q) / B2, k = (2 * q) % B2;
+        cp_async16(&S.w[c][k], Wsrc + 2 * q, 16);
+    }
+    __syncthreads();
+    constexpr int CPC = MT / 2;  // 16-byte chunks per column
+    for (int q = tid; q < B2 * CPC; q += kThreads) {
+        const int k = q / CPC, part = q % CPC;
+        const int row = row0 + 2 * part;
+        const int rem = nrows - row;
+        const int bytes = rem >= 2 ? 16 : (rem == 1 ? 8 : 0);
+        cp_async16(&S.x[k][2 * part], bytes ? S.col[k] + row : S.col[k], bytes);
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+
+    constexpr int WM = MT / 4, WN = B2 / 2, MI = WM / 8, NI = WN / 8;
+    const int wm = warp >> 1, wn = warp & 1;
+    const int m0 = wm * WM, n0 = wn * WN;
+    const int fr = lane >> 2, fk = lane & 3;
+    double acc[MI][NI][2];
+#pragma unroll
+    for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int j = 0; j < NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+#pragma unroll 4
+    for (int kk = 0; kk < B2; kk += 4) {
+        double a[MI], bb[NI];
+#pragma unroll
+        for (int i = 0; i < MI; ++i) a[i] = S.x[kk + fk][m0 + 8 * i + fr];
+#pragma unroll
+        for (int j = 0; j < NI; ++j) bb[j] = S.w[n0 + 8 * j + fr][kk + fk];
+#pragma unroll
+        for (int i = 0; i < MI; ++i)
+#pragma unroll
+            for (int j = 0; j < NI; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], bb[j]);
+    }
+    __syncthreads();  // everyone done reading x
+#pragma unroll
+    for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int j = 0; j < NI; ++j) {
+            const int row = m0 + 8 * i + fr, col = n0 + 8 * j + 2 * fk;
+            S.x[col][row] = acc[i][j][0];
+            S.x[col + 1][row] = acc[i][j][1];
+        }
+    __syncthreads();
+    for (int q = tid; q < B2 * MT; q += kThreads) {
+        const int c = q / MT, rr = q % MT;
+        if (row0 + rr < nrows) S.col[c][row0 + rr] = S.x[c][rr];
+    }
+}
+
+// ---------------------------------------------------------------------
+// column norms by position: d[k] = ||G[:, rho[k]]||^2 (one warp per column)
+// ---------------------------------------------------------------------
+__global__ void k_block_norms(const double *__restrict__ G, int64_t ldg, int n,
+                              const int64_t *__restrict__ rho, int64_t r, double *d,
+                              unsigned long long *first_zero)
+{
+    const int64_t k = blockIdx.x * (int64_t)(blockDim.x / 32) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (k >= r) return;
+    const double *g = G + rho[k] * ldg;
+    double s0 = 0.0, s1 = 0.0;
+    int e = lane;
+    for (; e + 32 < n; e += 64) {
+        const double x = g[e], y = g[e + 32];
+        s0 = fma(x, x, s0);
+        s1 = fma(y, y, s1);
+    }
+    for (; e < n; e += 32) s0 = fma(g[e], g[e], s0);
+    double s = s0 + s1;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) {
+        d[k] = s;
+        if (s == 0.0 && first_zero) atomicMin(first_zero, (unsigned long long)rho[k]);
+    }
+}
+
+// ---------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------
+struct BlockWs {
+    double *d, *Apart, *Wg;
+    int64_t *rho, *js, *ip, *jp, *iblk, *jblk, *cur;
+    uint8_t *C;
+    uint32_t *rotk, *skipk;
+    double *maxt;
+    unsigned long long *err, *first_zero;
+    void *sortws;
+    int64_t *out;
+    int8_t *signs;
+};
+
+struct Carve2 {
+    char *base;
+    int64_t off;
+    template <typename T>
+    T *take(int64_t count)
+    {
+        off = (off + 255) & ~(int64_t)255;
+        T *p = (T *)(base + off);
+        off += count * (int64_t)sizeof(T);
+        return p;
+    }
+};
+
+static int choose_ksplit(int64_t n, int64_t nslots, int KT)
+{
+    if (nslots < 1) nslots = 1;
+    // enough CTAs for >= 2 waves of 148 SMs, each CTA >= 4 k-tiles
+    int64_t want = (2 * 148 + nslots - 1) / nslots;
+    int64_t maxs = (n + 4 * KT - 1) / (4 * KT);
+    if (want > maxs) want = maxs;
+    if (want < 1) want = 1;
+    return (int)want;
+}
+
+static int64_t carve_block(Carve2 &c, int64_t n, int64_t r, int b, BlockWs *w)
+{
+    const int64_t B2 = 2 * b, nb = r / b, nslots = nb / 2 > 0 ? nb / 2 : 1;
+    const int ks = choose_ksplit(n, nslots, 32);
+    BlockWs t;
+    t.d = c.take<double>(r);
+    t.rho = c.take<int64_t>(r);
+    t.js = c.take<int64_t>(r);
+    t.ip = c.take<int64_t>(nslots);
+    t.jp = c.take<int64_t>(nslots);
+    t.iblk = c.take<int64_t>(nslots);
+    t.jblk = c.take<int64_t>(nslots);
+    t.cur = c.take<int64_t>(2 * nslots);
+    t.C = c.take<uint8_t>(nslots);
+    t.rotk = c.take<uint32_t>(nslots);
+    t.skipk = c.take<uint32_t>(nslots);
+    t.maxt = c.take<double>(nslots);
+    t.err = c.take<unsigned long long>(1);
+    t.first_zero = c.take<unsigned long long>(1);
+    t.sortws = c.take<char>(24 * r);
+    t.out = c.take<int64_t>(8);
+    t.signs = c.take<int8_t>(r);
+    t.Apart = c.take<double>(nslots * ks * B2 * B2);
+    t.Wg = c.take<double>(nslots * B2 * B2);
+    if (w) *w = t;
+    return c.off + 256;
+}
+
+int64_t block_workspace_size(int64_t n, int64_t r, const hsvd_config *cfg)
+{
+    Carve2 c{nullptr, 0};
+    return carve_block(c, n, r, cfg->block_cols, nullptr);
+}
+
+int launch_reduce_sweep(uint8_t *C, int64_t m, uint32_t *rotk, uint32_t *skipk,
+                        double *maxt, int64_t nslots, int64_t *out,
+                        const unsigned long long *err, int reset, cudaStream_t s);
+int launch_init_packages(const int8_t *signs, int64_t r, int64_t *rho,
+                         int64_t *jsign, cudaStream_t s);
+int launch_identity(double *V, int64_t r, int64_t ldv, cudaStream_t s);
+
+template <int B2>
+struct BlockKernels {
+    static constexpr int KT = 32, STAGES = 3, MT = 128;
+    static size_t gram_smem() { return sizeof(GramSmem<B2, KT, STAGES>); }
+    static size_t inner_smem() { return sizeof(InnerSmem<B2>); }
+    static size_t upd_smem() { return sizeof(UpdSmem<B2, MT>); }
+    static int setup()
+    {
+        HSVD_CUDA(cudaFuncSetAttribute(k_gram<B2, KT, STAGES>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)gram_smem()));
+        HSVD_CUDA(cudaFuncSetAttribute(k_inner<B2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)inner_smem()));
+        HSVD_CUDA(cudaFuncSetAttribute(k_update<B2, MT>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)upd_smem()));
+        return HSVD_OK;
+    }
+    // one step: Gram -> inner pass -> update
+    static int step(double *G, int64_t ldg, int n, double *V, int64_t ldv, int rv,
+                    const BlockWs &w, int64_t nb, int ksplit, int full,
+                    const hsvd_config *cfg, cudaStream_t s, KernelTimer &T)
+    {
+        const int64_t nslots = nb / 2;
+        const int kchunk = (int)((((int64_t)n + ksplit - 1) / ksplit + KT - 1) / KT * KT);
+        T.begin(0, s);
+        k_gram<B2, KT, STAGES><<<dim3(ksplit, (unsigned)nslots), kThreads, gram_smem(), s>>>(
+            G, ldg, n, w.rho, w.iblk, w.jblk, ksplit, kchunk, w.Apart, w.err);
+        T.end(s);
+        HSVD_LAUNCH_CHECK("k_gram");
+        InnerArgs ia;
+        ia.Apart = w.Apart; ia.Wg = w.Wg; ia.jsign = w.js;
+        ia.ip = w.ip; ia.jp = w.jp; ia.iblk = w.iblk; ia.jblk = w.jblk; ia.cur = w.cur;
+        ia.C = w.C; ia.rotk = w.rotk; ia.skipk = w.skipk; ia.maxt = w.maxt; ia.err = w.err;
+        ia.nb = nb; ia.eps = cfg->eps; ia.teps = cfg->teps; ia.ksplit = ksplit;
+        ia.full = full; ia.use_skip = cfg->use_skip;
+        T.begin(1, s);
+        k_inner<B2><<<(unsigned)nslots, kThreads, inner_smem(), s>>>(ia);
+        T.end(s);
+        HSVD_LAUNCH_CHECK("k_inner");
+        const int tiles_g = (n + MT - 1) / MT;
+        const int tiles_v = V ? (rv + MT - 1) / MT : 0;
+        T.begin(2, s);
+        k_update<B2, MT><<<dim3(tiles_g + tiles_v, (unsigned)nslots), kThreads, upd_smem(), s>>>(
+            G, ldg, n, V, ldv, rv, w.rho, w.cur, w.Wg, tiles_g, w.err);
+        T.end(s);
+        HSVD_LAUNCH_CHECK("k_update");
+        return HSVD_OK;
+    }
+};
+
+static int block_norms(double *G, int64_t ldg, int64_t n, const BlockWs &w, int64_t r,
+                       unsigned long long *first_zero, cudaStream_t s)
+{
+    k_block_norms<<<(unsigned)((r + 7) / 8), 256, 0, s>>>(G, ldg, (int)n, w.rho, r, w.d,
+                                                          first_zero);
+    HSVD_LAUNCH_CHECK("k_block_norms");
+    return HSVD_OK;
+}
+
+template <int B2>
+static int block_drive_t(double *G, int64_t n, int64_t r, int64_t ldg, double *V, int64_t ldv,
+                         const int8_t *signs_host, int64_t p, const hsvd_config *cfg,
+                         double *sigma, double *lam, void *ws, int64_t ws_bytes,
+                         hsvd_result *res, hsvd_telemetry *tele, cudaStream_t s)
+{
+    using K = BlockKernels<B2>;
+    constexpr int b = B2 / 2;
+    const int64_t nb = r / b, nslots = nb / 2;
+    Carve2 c{(char *)ws, 0};
+    BlockWs w;
+    if (carve_block(c, n, r, b, &w) > ws_bytes) {
+        set_error("workspace too small");
+        return HSVD_ERR_ARG;
+    }
+    const int ksplit = choose_ksplit(n, nslots, K::KT);
+    int st = K::setup();
+    if (st) return st;
+
+    int64_t *host = nullptr;
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    struct Cleanup {
+        int64_t *&h; cudaEvent_t &a, &b; cudaGraph_t &g; cudaGraphExec_t &e;
+        ~Cleanup()
+        {
+            if (e) cudaGraphExecDestroy(e);
+            if (g) cudaGraphDestroy(g);
+            if (a) cudaEventDestroy(a);
+            if (b) cudaEventDestroy(b);
+            if (h) cudaFreeHost(h);
+        }
+    } cleanup{host, t0, t1, graph, exec};
+    HSVD_CUDA(cudaHostAlloc((void **)&host, 16 * sizeof(int64_t), cudaHostAllocDefault));
+    HSVD_CUDA(cudaEventCreate(&t0));
+    HSVD_CUDA(cudaEventCreate(&t1));
+
+    if (V) {
+        st = launch_identity(V, r, ldv, s);
+        if (st) return st;
+    }
+    HSVD_CUDA(cudaMemcpyAsync(w.signs, signs_host, (size_t)r, cudaMemcpyHostToDevice, s));
+    st = launch_init_packages(w.signs, r, w.rho, w.js, s);
+    if (st) return st;
+    HSVD_CUDA(cudaMemsetAsync(w.first_zero, 0xff, sizeof(unsigned long long), s));
+    st = block_norms(G, ldg, n, w, r, w.first_zero, s);
+    if (st) return st;
+    HSVD_CUDA(cudaMemcpyAsync(host, w.first_zero, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    HSVD_CUDA(cudaStreamSynchronize(s));
+    if ((unsigned long long)host[0] != kNoError) {
+        res->err[0] = host[0];
+        res->err[1] = res->err[2] = -1;
+        set_error("column " + std::to_string(host[0]) + " has zero norm");
+        return HSVD_RANK_DEFICIENT;
+    }
+    if (cfg->sort) {
+        st = hsvd_sort_diagonal(w.d, w.rho, w.js, r, p, w.sortws, s);
+        if (st) return st;
+    }
+    st = hsvd_stepper_init(w.ip, w.jp, w.iblk, w.jblk, nb, s);
+    if (st) return st;
+    HSVD_CUDA(cudaMemsetAsync(w.C, 0, (size_t)nslots, s));
+    HSVD_CUDA(cudaMemsetAsync(w.rotk, 0, sizeof(uint32_t) * nslots, s));
+    HSVD_CUDA(cudaMemsetAsync(w.skipk, 0, sizeof(uint32_t) * nslots, s));
+    HSVD_CUDA(cudaMemsetAsync(w.maxt, 0, sizeof(double) * nslots, s));
+    HSVD_CUDA(cudaMemsetAsync(w.err, 0xff, sizeof(unsigned long long), s));
+
+    KernelTimer T;
+    auto enqueue_sweep = [&]() -> int {
+        for (int64_t step = 0; step < nb; ++step) {
+            const int full = cfg->inner_full || step == 0;
+            int e = K::step(G, ldg, (int)n, V, ldv, (int)r, w, nb, ksplit, full, cfg, s, T);
+            if (e) return e;
+        }
+        T.begin(3, s);
+        int e = block_norms(G, ldg, n, w, r, nullptr, s);
+        if (e) return e;
+        e = launch_reduce_sweep(w.C, nslots, w.rotk, w.skipk, w.maxt, nslots, w.out, w.err, 1, s);
+        if (e) return e;
+        if (cfg->sort) {
+            e = hsvd_sort_diagonal(w.d, w.rho, w.js, r, p, w.sortws, s);
+            if (e) return e;
+        }
+        T.end(s);
+        HSVD_CUDA(cudaMemcpyAsync(host, w.out, 5 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        return HSVD_OK;
+    };
+    if (cfg->use_graph && !cfg->profile) {
+        HSVD_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        st = enqueue_sweep();
+        cudaError_t ce = cudaStreamEndCapture(s, &graph);
+        if (st) return st;
+        if (ce != cudaSuccess) return cuda_fail(ce, "cudaStreamEndCapture");
+        HSVD_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+    }
+    const int64_t per_sweep = 3 * nb + 1 + 1 + (cfg->sort ? 2 : 0);
+    int64_t launches = (V ? 1 : 0) + 1 + 1 + (cfg->sort ? 2 : 0) + 1 + 2;
+    int64_t sweeps_used = 0, total_rot = 0, total_skip = 0;
+    int stop = 2;
+    const double t_loop0 = wall_ms();
+    res->setup_ms = t_loop0;  // absolute for now; hsvd_drive makes it relative
+    for (int64_t sweep = 0; sweep < cfg->max_sweeps; ++sweep) {
+        HSVD_CUDA(cudaEventRecord(t0, s));
+        launches += per_sweep;
+        if (exec) {
+            HSVD_CUDA(cudaGraphLaunch(exec, s));
+        } else {
+            T.on = cfg->profile && sweep == 0;
+            st = enqueue_sweep();
+            if (st) return st;
+        }
+        HSVD_CUDA(cudaEventRecord(t1, s));
+        HSVD_CUDA(cudaStreamSynchronize(s));
+        if (T.on) T.collect(res);
+        float ms = 0.f;
+        HSVD_CUDA(cudaEventElapsedTime(&ms, t0, t1));
+        if ((unsigned long long)host[4] != kNoError) {
+            unpack_err((unsigned long long)host[4], res->err);
+            set_error("definiteness lost at block " + std::to_string(res->err[0]) +
+                      ", pivot pair (" + std::to_string(res->err[1]) + ", " +
+                      std::to_string(res->err[2]) + ")");
+            return HSVD_DEFINITENESS_LOST;
+        }
+        const int code = (int)host[0];
+        double max_t;
+        memcpy(&max_t, &host[3], sizeof(double));
+        sweeps_used = sweep + 1;
+        total_rot += host[1];
+        total_skip += host[2];
+        if (tele) {
+            tele[sweep].sweep = sweep;
+            tele[sweep].rotations = host[1];
+            tele[sweep].skips = host[2];
+            tele[sweep].max_t = max_t;
+            tele[sweep].gpu_ms = ms;
+        }
+        if (code == 0) { stop = 0; break; }
+        if (code == 1) { stop = 1; break; }
+    }
+    res->sweeps_ms = wall_ms() - t_loop0;
+    // d was refreshed from G at the end of the last sweep (then sorted)
+    st = hsvd_extract(G, n, ldg, w.d, w.rho, w.js, r, sigma, lam, s);
+    if (st) return st;
+    res->sweeps_used = sweeps_used;
+    res->stop_reason = stop;
+    res->rotations = total_rot;
+    res->skips = total_skip;
+    res->launches = launches;
+    return HSVD_OK;
+}
+
+int block_drive(double *G, int64_t n, int64_t r, int64_t ldg, double *V, int64_t ldv,
+                const int8_t *signs_host, int64_t p, const hsvd_config *cfg, double *sigma,
+                double *lam, void *ws, int64_t ws_bytes, hsvd_result *res,
+                hsvd_telemetry *tele, cudaStream_t s)
+{
+    const int b = cfg->block_cols;
+    if (b != 16 && b != 32) {
+        set_error("block mode supports block_cols 16 or 32");
+        return HSVD_ERR_UNSUPPORTED;
+    }
+    if (r % (2 * b) != 0) {
+        set_error("block mode needs r to be a multiple of 2*block_cols (use border())");
+        return HSVD_ERR_UNSUPPORTED;
+    }
+    if (ldg % 2 || (V && ldv % 2) || ((uintptr_t)G & 15) || (V && ((uintptr_t)V & 15))) {
+        set_error("block mode needs 16-byte aligned columns (even leading dimensions)");
+        return HSVD_ERR_UNSUPPORTED;
+    }
+    if (b == 16)
+        return block_drive_t<32>(G, n, r, ldg, V, ldv, signs_host, p, cfg, sigma, lam, ws,
+                                 ws_bytes, res, tele, s);
+    return block_drive_t<64>(G, n, r, ldg, V, ldv, signs_host, p, cfg, sigma, lam, ws,
+                             ws_bytes, res, tele, s);
+}
+
 }  // namespace hsvd

@@ -124,24 +124,29 @@ struct DriveRes {
 static int enqueue_sweep(double *G, int64_t n, int64_t r, int64_t ldg,
                          double *V, int64_t ldv, int64_t p,
                          const hsvd_config *cfg, const PointwiseWs &w,
-                         int64_t *host_out, cudaStream_t s)
+                         int64_t *host_out, cudaStream_t s, KernelTimer &T)
 {
     int st;
     if (cfg->schedule == HSVD_SCHEDULE_ROW_CYCLIC) {
+        T.begin(0, s);
         st = launch_rowcyclic_sweep(G, n, ldg, V, r, ldv, w.d, w.rho, w.js, r,
                                     w.C, cfg->eps, cfg->teps, cfg->use_skip,
                                     cfg->chunk, w.rotk, w.skipk, w.maxt, w.err, s);
+        T.end(s);
         if (st) return st;
     } else {
         for (int64_t step = 0; step < r; ++step) {
+            T.begin(0, s);
             st = launch_pointwise_step(G, n, ldg, V, r, ldv, w.d, w.rho, w.js,
                                        w.ip, w.jp, w.iblk, w.jblk, r, w.C, 0,
                                        r / 2, cfg->eps, cfg->teps,
                                        cfg->use_skip, cfg->chunk, 1, w.rotk,
                                        w.skipk, w.maxt, w.err, s);
+            T.end(s);
             if (st) return st;
         }
     }
+    T.begin(3, s);
     st = launch_reduce_sweep(w.C, w.ncodes, w.rotk, w.skipk, w.maxt, w.nslots,
                              w.out, w.err, 1, s);
     if (st) return st;
@@ -149,6 +154,7 @@ static int enqueue_sweep(double *G, int64_t n, int64_t r, int64_t ldg,
         st = hsvd_sort_diagonal(w.d, w.rho, w.js, r, p, w.sortws, s);
         if (st) return st;
     }
+    T.end(s);
     HSVD_CUDA(cudaMemcpyAsync(host_out, w.out, 5 * sizeof(int64_t),
                               cudaMemcpyDeviceToHost, s));
     return HSVD_OK;
@@ -206,9 +212,10 @@ static int pointwise_drive(double *G, int64_t n, int64_t r, int64_t ldg,
     HSVD_CUDA(cudaMemsetAsync(w.maxt, 0, sizeof(double) * w.nslots, s));
     HSVD_CUDA(cudaMemsetAsync(w.err, 0xff, sizeof(unsigned long long), s));
 
-    if (cfg->use_graph) {
+    KernelTimer T;
+    if (cfg->use_graph && !cfg->profile) {
         HSVD_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-        st = enqueue_sweep(G, n, r, ldg, V, ldv, p, cfg, w, host, s);
+        st = enqueue_sweep(G, n, r, ldg, V, ldv, p, cfg, w, host, s, T);
         cudaGraph_t g = nullptr;
         cudaError_t ce = cudaStreamEndCapture(s, &g);
         if (st) {
@@ -227,17 +234,21 @@ static int pointwise_drive(double *G, int64_t n, int64_t r, int64_t ldg,
     HSVD_CUDA(cudaEventCreate(&R.t1));
     int64_t sweeps_used = 0, total_rot = 0, total_skip = 0;
     int stop = 2;
+    const double t_loop0 = wall_ms();
+    res->setup_ms = t_loop0;  // absolute for now; hsvd_drive makes it relative
     for (int64_t sweep = 0; sweep < cfg->max_sweeps; ++sweep) {
         HSVD_CUDA(cudaEventRecord(R.t0, s));
         launches += per_sweep;
         if (R.exec) {
             HSVD_CUDA(cudaGraphLaunch(R.exec, s));
         } else {
-            st = enqueue_sweep(G, n, r, ldg, V, ldv, p, cfg, w, host, s);
+            T.on = cfg->profile && sweep == 0;
+            st = enqueue_sweep(G, n, r, ldg, V, ldv, p, cfg, w, host, s, T);
             if (st) return st;
         }
         HSVD_CUDA(cudaEventRecord(R.t1, s));
         HSVD_CUDA(cudaStreamSynchronize(s));
+        if (T.on) T.collect(res);
         float sweep_ms = 0.f;
         HSVD_CUDA(cudaEventElapsedTime(&sweep_ms, R.t0, R.t1));
         if ((unsigned long long)host[4] != kNoError) {
@@ -264,6 +275,7 @@ static int pointwise_drive(double *G, int64_t n, int64_t r, int64_t ldg,
         if (code == 0) { stop = 0; break; }
         if (code == 1) { stop = 1; break; }
     }
+    res->sweeps_ms = wall_ms() - t_loop0;
     st = hsvd_extract(G, n, ldg, w.d, w.rho, w.js, r, sigma, lam, s);
     if (st) return st;
     res->sweeps_used = sweeps_used;
@@ -315,6 +327,7 @@ int hsvd_drive(double *G, int64_t n, int64_t r, int64_t ldg, double *Vinv_t,
                void *workspace, int64_t workspace_bytes,
                hsvd_result *res_host, hsvd_telemetry *tele_host, void *stream)
 {
+    const double t_entry = wall_ms();
     memset(res_host, 0, sizeof(*res_host));
     res_host->err[0] = res_host->err[1] = res_host->err[2] = -1;
     if (r % 2 != 0 || r < 2) {
@@ -356,6 +369,11 @@ int hsvd_drive(double *G, int64_t n, int64_t r, int64_t ldg, double *Vinv_t,
     if (st == HSVD_OK && (e1 != cudaSuccess || e2 != cudaSuccess))
         return cuda_fail(e1 != cudaSuccess ? e1 : e2, "stream join");
     cudaStreamSynchronize(R.s);
+    if (st == HSVD_OK) {
+        const double t_loop0 = res_host->setup_ms;
+        res_host->setup_ms = t_loop0 - t_entry;
+        res_host->finish_ms = wall_ms() - t_loop0 - res_host->sweeps_ms;
+    }
     return st;
 }
 

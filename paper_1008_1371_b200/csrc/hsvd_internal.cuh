@@ -9,7 +9,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <chrono>
 #include <string>
+#include <vector>
 
 #include "../../include/hsvd_b200.h"
 
@@ -32,6 +34,57 @@ int cuda_fail(cudaError_t e, const char *what);
     } while (0)
 
 constexpr unsigned long long kNoError = ~0ull;
+
+inline double wall_ms()
+{
+    return std::chrono::duration<double, std::milli>(
+               std::chrono::steady_clock::now().time_since_epoch())
+        .count();
+}
+
+// Profile-mode kernel timer: CUDA events around each launch of sweep 0,
+// summed per kernel class after the sweep's synchronisation.
+struct KernelTimer {
+    bool on = false;
+    std::vector<cudaEvent_t> ev;
+    std::vector<int> cls;
+    size_t used = 0;
+    ~KernelTimer()
+    {
+        for (auto e : ev) cudaEventDestroy(e);
+    }
+    void begin(int c, cudaStream_t s)
+    {
+        if (!on) return;
+        if (used + 2 > ev.size()) {
+            for (int i = 0; i < 2; ++i) {
+                cudaEvent_t e;
+                cudaEventCreate(&e);
+                ev.push_back(e);
+            }
+        }
+        cls.push_back(c);
+        cudaEventRecord(ev[used++], s);
+    }
+    void end(cudaStream_t s)
+    {
+        if (!on) return;
+        cudaEventRecord(ev[used++], s);
+    }
+    // call after synchronising the stream
+    void collect(hsvd_result *res)
+    {
+        for (size_t k = 0; k < cls.size(); ++k) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, ev[2 * k], ev[2 * k + 1]);
+            res->kernel_ms[cls[k]] += ms;
+            res->kernel_launches[cls[k]] += 1;
+        }
+        cls.clear();
+        used = 0;
+        on = false;
+    }
+};
 
 // Packed (block, i, j) error word; min over failing slots = first slot.
 __host__ __device__ inline unsigned long long pack_err(int64_t k, int64_t i,

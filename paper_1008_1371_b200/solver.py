@@ -59,6 +59,7 @@ class SolverConfig:
     block_cols: int = 32
     inner_ordering: str = "oriented"
     use_graph: bool = True
+    profile: bool = False
 
     def __post_init__(self):
         if self.teps is None:
@@ -87,6 +88,7 @@ class SolverConfig:
         c.block_cols = int(self.block_cols)
         c.inner_full = int(self.inner_ordering == "full")
         c.use_graph = int(bool(self.use_graph))
+        c.profile = int(bool(self.profile))
         return c
 
 
@@ -107,6 +109,8 @@ class HsvdResult:
     #: B200 extras: device time of each sweep (ms) and kernel launches
     sweep_gpu_ms: list = field(default_factory=list)
     gpu_launches: int = 0
+    host_phase_ms: dict = field(default_factory=dict)
+    kernel_profile: dict = field(default_factory=dict)
 
 
 def precompute(G, J, chunk=DEFAULT_CHUNK):
@@ -192,11 +196,19 @@ def drive_device(Gt, J, cfg=None, n=None):
     telemetry = [(int(tele[s].sweep), int(tele[s].rotations),
                   int(tele[s].skips), float(tele[s].max_t))
                  for s in range(res.sweeps_used)]
+    names = (("step", "inner", "update", "sweep_end") if cfg.mode == "pointwise"
+             else ("gram", "inner", "update", "sweep_end"))
+    prof = ({names[k]: {"ms": float(res.kernel_ms[k]),
+                        "launches": int(res.kernel_launches[k])}
+             for k in range(4) if res.kernel_launches[k]} if cfg.profile else {})
     return HsvdResult(sigma, Gt, lam, Vt, int(res.sweeps_used),
                       _STOP[int(res.stop_reason)], int(res.rotations),
                       int(res.skips), telemetry,
                       [float(tele[s].gpu_ms) for s in range(res.sweeps_used)],
-                      int(res.launches))
+                      int(res.launches),
+                      {"setup": float(res.setup_ms), "sweeps": float(res.sweeps_ms),
+                       "finish": float(res.finish_ms)},
+                      prof)
 
 
 def drive(G, J, cfg=None):

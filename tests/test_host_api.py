@@ -56,8 +56,8 @@ def test_solverconfig_defaults_mirror_reference():
 
 
 def test_struct_sizes():
-    assert ctypes.sizeof(_lib.HsvdConfigC) == 64
-    assert ctypes.sizeof(_lib.HsvdResultC) == 64
+    assert ctypes.sizeof(_lib.HsvdConfigC) == 72
+    assert ctypes.sizeof(_lib.HsvdResultC) == 152
     assert ctypes.sizeof(_lib.HsvdTelemetryC) == 40
 
 
