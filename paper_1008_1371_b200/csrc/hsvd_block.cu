@@ -68,115 +68,213 @@ __device__ __forceinline__ int64_t slot_pos(int c, int b, int64_t I, int64_t J)
 }
 
 // ---------------------------------------------------------------------
-// k_gram: partial Gram matrices, one CTA per (split, slot)
+// k_gram: partial Gram matrices over a static "stream-K" partition
 // ---------------------------------------------------------------------
-template <int B2, int KT, int STAGES>
-struct GramSmem {
-    static constexpr int LD = KT + 4;  // == 4 mod 16: conflict-free fragments
-    double x[STAGES][B2][LD];
-    const double *col[B2];
+// The work of one step is W = nslots * T k-tiles (T = ceil(n / KT)).  The
+// grid has P = (#SMs x resident CTAs) CTAs and CTA c owns the contiguous
+// item range [c*W/P, (c+1)*W/P): every SM gets the same number of DMMAs,
+// with no wave tail.  A CTA flushes one partial Gram per slot segment it
+// covers; k_inner sums a slot's partials in segment order, so the result
+// is deterministic for a given P.
+struct GramPart {
+    int64_t W, P, T;
+    __host__ __device__ int64_t begin(int64_t c) const { return c * W / P; }
+    // CTA owning item x
+    __host__ __device__ int64_t owner(int64_t x) const
+    {
+        int64_t c = (x * P) / W;
+        while (c + 1 < P && begin(c + 1) <= x) ++c;
+        while (c > 0 && begin(c) > x) --c;
+        return c;
+    }
+    __host__ __device__ int64_t first_cta(int64_t slot) const { return owner(slot * T); }
+    __host__ __device__ int64_t nseg(int64_t slot) const
+    {
+        return owner(slot * T + T - 1) - first_cta(slot) + 1;
+    }
 };
 
 template <int B2, int KT, int STAGES>
-__global__ void __launch_bounds__(kThreads, 2) k_gram(
+struct GramSmem {
+    static constexpr int LD = KT + 4;  // == 4 mod 16: conflict-free fragments
+    static constexpr int MAXSLOTS = 4;  // slots one CTA may touch
+    double x[STAGES][B2][LD];
+    const double *col[MAXSLOTS][B2];
+};
+
+// Per-warp DMMA roles over the upper-triangle 8x8 tiles of the B2 x B2
+// output (A is symmetric).  Roles are resolved by warp-uniform branches, so
+// no DMMA is ever issued predicated-off (a predicated-off DMMA still
+// occupies the tensor pipe).  B2 = 64: 16x16 super-tiles; warps 0-5 own one
+// off-diagonal super-tile (4 DMMA per k-step), warps 6-7 two diagonal
+// super-tiles (3 DMMA each): 8/8/10/10 DMMA per SM sub-partition.
+// B2 = 32: ten 8x8 tiles, warps 0-1 own two, warps 2-7 one.
+template <int B2>
+struct GramRoles;
+
+template <>
+struct GramRoles<64> {
+    static constexpr int NACC = 6;  // accumulator tiles per warp (max)
+    __device__ static void mma(int warp, const double (*X)[GramSmem<64, 32, 4>::LD], int kk,
+                               int fr, int fk, double (&acc)[NACC][2])
+    {
+        if (warp < 6) {
+            const int R = warp < 3 ? 0 : (warp < 5 ? 1 : 2);
+            const int C = warp < 3 ? warp + 1 : (warp < 5 ? warp - 1 : 3);
+            const double a0 = X[16 * R + fr][kk + fk], a1 = X[16 * R + 8 + fr][kk + fk];
+            const double b0 = X[16 * C + fr][kk + fk], b1 = X[16 * C + 8 + fr][kk + fk];
+            dmma(acc[0][0], acc[0][1], a0, b0);
+            dmma(acc[1][0], acc[1][1], a0, b1);
+            dmma(acc[2][0], acc[2][1], a1, b0);
+            dmma(acc[3][0], acc[3][1], a1, b1);
+        } else {
+            const int D0 = 2 * (warp - 6), D1 = D0 + 1;
+            const double f0 = X[16 * D0 + fr][kk + fk], f1 = X[16 * D0 + 8 + fr][kk + fk];
+            const double g0 = X[16 * D1 + fr][kk + fk], g1 = X[16 * D1 + 8 + fr][kk + fk];
+            dmma(acc[0][0], acc[0][1], f0, f0);
+            dmma(acc[1][0], acc[1][1], f0, f1);
+            dmma(acc[2][0], acc[2][1], f1, f1);
+            dmma(acc[3][0], acc[3][1], g0, g0);
+            dmma(acc[4][0], acc[4][1], g0, g1);
+            dmma(acc[5][0], acc[5][1], g1, g1);
+        }
+    }
+    // (row-tile, col-tile) of accumulator q of this warp; -1 if unused
+    __device__ static void tile(int warp, int q, int &rt, int &ct)
+    {
+        rt = ct = -1;
+        if (warp < 6) {
+            const int R = warp < 3 ? 0 : (warp < 5 ? 1 : 2);
+            const int C = warp < 3 ? warp + 1 : (warp < 5 ? warp - 1 : 3);
+            if (q < 4) { rt = 2 * R + (q >> 1); ct = 2 * C + (q & 1); }
+        } else {
+            const int D = 2 * (warp - 6) + (q >= 3 ? 1 : 0);
+            const int qq = q % 3;
+            rt = 2 * D + (qq == 2 ? 1 : 0);
+            ct = 2 * D + (qq == 0 ? 0 : 1);
+        }
+    }
+};
+
+template <>
+struct GramRoles<32> {
+    static constexpr int NACC = 2;
+    // upper 8x8 tiles of a 4x4 tile grid, in order
+    __device__ static void tile(int warp, int q, int &rt, int &ct)
+    {
+        const int t = q == 0 ? warp : (warp < 2 ? 8 + warp : -1);
+        rt = ct = -1;
+        if (t < 0) return;
+        // nibble t of the packed tables: R = 0,0,0,0,1,1,1,2,2,3  C = 0,1,2,3,1,2,3,2,3,3
+        rt = (int)((0x3221110000ull >> (4 * t)) & 0xF);
+        ct = (int)((0x3323213210ull >> (4 * t)) & 0xF);
+    }
+    __device__ static void mma(int warp, const double (*X)[GramSmem<32, 32, 4>::LD], int kk,
+                               int fr, int fk, double (&acc)[NACC][2])
+    {
+        int rt, ct;
+        tile(warp, 0, rt, ct);
+        dmma(acc[0][0], acc[0][1], X[8 * rt + fr][kk + fk], X[8 * ct + fr][kk + fk]);
+        if (warp < 2) {
+            tile(warp, 1, rt, ct);
+            dmma(acc[1][0], acc[1][1], X[8 * rt + fr][kk + fk], X[8 * ct + fr][kk + fk]);
+        }
+    }
+};
+
+template <int B2, int KT, int STAGES>
+__global__ void __launch_bounds__(kThreads, 3) k_gram(
     const double *__restrict__ G, int64_t ldg, int n, const int64_t *__restrict__ rho,
-    const int64_t *__restrict__ iblk, const int64_t *__restrict__ jblk, int ksplit,
-    int kchunk, double *__restrict__ Apart, const unsigned long long *err)
+    const int64_t *__restrict__ iblk, const int64_t *__restrict__ jblk, GramPart part,
+    int maxseg, double *__restrict__ Apart, const unsigned long long *err)
 {
+    using Sm = GramSmem<B2, KT, STAGES>;
+    using Roles = GramRoles<B2>;
     extern __shared__ __align__(16) unsigned char gsm_raw[];
-    auto &S = *reinterpret_cast<GramSmem<B2, KT, STAGES> *>(gsm_raw);
+    auto &S = *reinterpret_cast<Sm *>(gsm_raw);
     if (*(volatile const unsigned long long *)err != kNoError) return;
     constexpr int b = B2 / 2;
-    const int split = blockIdx.x, slot = blockIdx.y;
+    const int64_t cta = blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    int64_t I = iblk[slot], J = jblk[slot];
-    if (I > J) { int64_t t = I; I = J; J = t; }
-    if (tid < B2) S.col[tid] = G + rho[slot_pos(tid, b, I, J)] * ldg;
+    const int64_t it0 = part.begin(cta), it1 = part.begin(cta + 1);
+    if (it1 <= it0) return;
+    const int64_t slot0 = it0 / part.T;
+    const int nsl = (int)((it1 - 1) / part.T - slot0 + 1);  // <= MAXSLOTS (host-checked)
+    for (int q = tid; q < nsl * B2; q += kThreads) {
+        const int si = q / B2, c = q % B2;
+        const int64_t slot = slot0 + si;
+        int64_t I = iblk[slot], J = jblk[slot];
+        if (I > J) { int64_t t = I; I = J; J = t; }
+        S.col[si][c] = G + rho[slot_pos(c, b, I, J)] * ldg;
+    }
     __syncthreads();
 
-    const int k_lo = split * kchunk;
-    const int k_hi = min(n, k_lo + kchunk);
-    const int ntiles = k_hi > k_lo ? (k_hi - k_lo + KT - 1) / KT : 0;
-
-    // cp.async assignment: B2 columns x KT/2 16-byte chunks per stage
     constexpr int CHUNKS = B2 * (KT / 2);
     constexpr int PER_T = (CHUNKS + kThreads - 1) / kThreads;
-    auto load_stage = [&](int st, int tile) {
-        const int k0 = k_lo + tile * KT;
+    auto load_stage = [&](int st, int64_t item) {
+        const int si = (int)(item / part.T - slot0);
+        const int k0 = (int)(item % part.T) * KT;
 #pragma unroll
         for (int u = 0; u < PER_T; ++u) {
             const int q = tid + u * kThreads;
             if (q < CHUNKS) {
-                const int c = q / (KT / 2), part = q % (KT / 2);
-                const int k = k0 + 2 * part;
-                const int rem = k_hi - k;
+                const int c = q / (KT / 2), pp = q % (KT / 2);
+                const int k = k0 + 2 * pp;
+                const int rem = n - k;
                 const int bytes = rem >= 2 ? 16 : (rem == 1 ? 8 : 0);
-                const double *src = bytes ? S.col[c] + k : S.col[c];
-                cp_async16(&S.x[st][c][2 * part], src, bytes);
+                const double *src = bytes ? S.col[si][c] + k : S.col[si][c];
+                cp_async16(&S.x[st][c][2 * pp], src, bytes);
             }
         }
     };
 
-    // warp tiling of the B2 x B2 output: 4 warps along M, 2 along N
-    constexpr int WM = B2 / 4, WN = B2 / 2, MI = WM / 8, NI = WN / 8;
-    const int wm = warp >> 1, wn = warp & 1;
-    const int m0 = wm * WM, n0 = wn * WN;
-    double acc[MI][NI][2];
+    double acc[Roles::NACC][2];
 #pragma unroll
-    for (int i = 0; i < MI; ++i)
-#pragma unroll
-        for (int j = 0; j < NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-    // upper-triangle 8x8 tiles only (A is symmetric)
-    bool live[MI][NI];
-#pragma unroll
-    for (int i = 0; i < MI; ++i)
-#pragma unroll
-        for (int j = 0; j < NI; ++j) live[i][j] = (m0 + 8 * i) <= (n0 + 8 * j);
-
+    for (int q = 0; q < Roles::NACC; ++q) acc[q][0] = acc[q][1] = 0.0;
+    const int64_t nitems = it1 - it0;
 #pragma unroll
     for (int s = 0; s < STAGES - 1; ++s) {
-        if (s < ntiles) load_stage(s, s);
+        if (s < nitems) load_stage(s, it0 + s);
         cp_async_commit();
     }
     const int fr = lane >> 2, fk = lane & 3;
-    for (int tile = 0; tile < ntiles; ++tile) {
+    for (int64_t i = 0; i < nitems; ++i) {
         cp_async_wait<STAGES - 2>();
         __syncthreads();
-        const int nxt = tile + STAGES - 1;
-        if (nxt < ntiles) load_stage(nxt % STAGES, nxt);
+        const int64_t nxt = i + STAGES - 1;
+        if (nxt < nitems) load_stage((int)(nxt % STAGES), it0 + nxt);
         cp_async_commit();
-        const auto &X = S.x[tile % STAGES];
+        const auto X = S.x[i % STAGES];
 #pragma unroll
-        for (int kk = 0; kk < KT; kk += 4) {
-            double a[MI], bb[NI];
+        for (int kk = 0; kk < KT; kk += 4) Roles::mma(warp, X, kk, fr, fk, acc);
+        const int64_t item = it0 + i;
+        if (i + 1 == nitems || (item + 1) % part.T == 0) {
+            // flush this slot segment's partial (upper tiles only)
+            const int64_t slot = item / part.T;
+            const int64_t seg = cta - part.first_cta(slot);
+            double *out = Apart + (slot * maxseg + seg) * (B2 * B2);
 #pragma unroll
-            for (int i = 0; i < MI; ++i) a[i] = X[m0 + 8 * i + fr][kk + fk];
-#pragma unroll
-            for (int j = 0; j < NI; ++j) bb[j] = X[n0 + 8 * j + fr][kk + fk];
-#pragma unroll
-            for (int i = 0; i < MI; ++i)
-#pragma unroll
-                for (int j = 0; j < NI; ++j)
-                    if (live[i][j]) dmma(acc[i][j][0], acc[i][j][1], a[i], bb[j]);
+            for (int q = 0; q < Roles::NACC; ++q) {
+                int rt, ct;
+                Roles::tile(warp, q, rt, ct);
+                if (rt >= 0) {
+                    const int row = 8 * rt + fr, col = 8 * ct + 2 * fk;
+                    out[row * B2 + col] = acc[q][0];
+                    out[row * B2 + col + 1] = acc[q][1];
+                }
+                acc[q][0] = acc[q][1] = 0.0;
+            }
         }
     }
     cp_async_wait<0>();
-    double *out = Apart + ((int64_t)slot * ksplit + split) * (B2 * B2);
-#pragma unroll
-    for (int i = 0; i < MI; ++i)
-#pragma unroll
-        for (int j = 0; j < NI; ++j)
-            if (live[i][j]) {
-                const int row = m0 + 8 * i + fr, col = n0 + 8 * j + 2 * fk;
-                out[row * B2 + col] = acc[i][j][0];
-                out[row * B2 + col + 1] = acc[i][j][1];
-            }
 }
 
 // ---------------------------------------------------------------------
 // k_inner: one pass of 2x2 rotations on the 2b x 2b pivot Gram
 // ---------------------------------------------------------------------
 struct InnerArgs {
+    GramPart part;
+    int maxseg;
     const double *Apart;
     double *Wg;
     const int64_t *jsign;
@@ -187,7 +285,7 @@ struct InnerArgs {
     unsigned long long *err;
     int64_t nb;
     double eps, teps;
-    int ksplit, full, use_skip;
+    int full, use_skip;
 };
 
 template <int B2>
@@ -195,8 +293,10 @@ struct InnerSmem {
     static constexpr int LD = B2 + 1;
     double A[B2][LD];
     double W[B2][LD];
-    double rt[B2 / 2], rc[B2 / 2], rs[B2 / 2];
-    int pi[B2 / 2], pj[B2 / 2], act[B2 / 2];
+    // rotation parameters, double-buffered by round parity: the W update of
+    // round r-1 runs on warps 1.. while warp 0 forms round r's rotations
+    double rt[2][B2 / 2], rc[2][B2 / 2], rs[2][B2 / 2];
+    int pi[2][B2 / 2], pj[2][B2 / 2], act[2][B2 / 2];
     int js[B2];
     unsigned int rot, skip, big;
     unsigned long long maxt_bits;
@@ -214,13 +314,14 @@ __global__ void __launch_bounds__(kThreads) k_inner(InnerArgs a)
     int64_t I = a.iblk[slot], J = a.jblk[slot];
     if (I > J) { int64_t t = I; I = J; J = t; }
 
-    // A = sum of split-K partials (fixed order), upper triangle mirrored
-    const double *P0 = a.Apart + (int64_t)slot * a.ksplit * (B2 * B2);
+    // A = sum of the slot's partial segments (fixed order), upper mirrored
+    const double *P0 = a.Apart + (int64_t)slot * a.maxseg * (B2 * B2);
+    const int nseg = (int)a.part.nseg(slot);
     for (int e = tid; e < B2 * B2; e += kThreads) {
         const int i = e / B2, j = e % B2;
         const int lo = min(i, j), hi = max(i, j);
         double v = 0.0;
-        for (int s = 0; s < a.ksplit; ++s) v += P0[(int64_t)s * B2 * B2 + lo * B2 + hi];
+        for (int s = 0; s < nseg; ++s) v += P0[(int64_t)s * B2 * B2 + lo * B2 + hi];
         S.A[i][j] = v;
         S.W[i][j] = i == j ? 1.0 : 0.0;
     }
@@ -235,79 +336,107 @@ __global__ void __launch_bounds__(kThreads) k_inner(InnerArgs a)
     const int rounds = a.full ? B2 - 1 : b;
     unsigned int my_rot = 0, my_skip = 0, my_big = 0;
     double my_max = 0.0;
+    // Thread-to-work map of the update phases: pair q = e / RPT, rows
+    // (e % RPT) + RPT * k; the pair's parameters are read once per thread.
+    // W <- W R for the rotations of buffer pb, by threads [t0, kThreads)
+    auto apply_w = [&](int pb, int t0) {
+        const int nt = kThreads - t0;
+        for (int e = tid - t0; e < b * 8; e += nt) {
+            const int q = e >> 3;
+            if (!S.act[pb][q]) continue;
+            const int i = S.pi[pb][q], j = S.pj[pb][q];
+            const double t = S.rt[pb][q], c = S.rc[pb][q], st = S.rs[pb][q] * t;
+            for (int row = e & 7; row < B2; row += 8) {
+                const double wx = S.W[row][i], wy = S.W[row][j];
+                S.W[row][i] = fma(st, wy, wx) * c;
+                S.W[row][j] = fma(t, wx, wy) * c;
+            }
+        }
+    };
     for (int rd = 0; rd < rounds; ++rd) {
-        // phase 1: the round's b disjoint pairs and their rotations
-        if (tid < b) {
-            int i, j;
-            if (a.full) {  // circle method on B2 players
-                const int m = B2 - 1;
-                if (tid == 0) {
-                    i = m;
-                    j = rd;
-                } else {
-                    i = (rd + tid) % m;
-                    j = (rd - tid + m) % m;
+        const int pb = rd & 1;
+        int w_any = 0;
+        if (tid < 32) {
+            // phase 1 (warp 0): the round's b disjoint pairs and rotations
+            int my_any = 0;
+            for (int q = tid; q < b; q += 32) {
+                int i, j;
+                if (a.full) {  // circle method on B2 players
+                    const int m = B2 - 1;
+                    if (q == 0) {
+                        i = m;
+                        j = rd;
+                    } else {
+                        i = (rd + q) % m;
+                        j = (rd - q + m) % m;
+                    }
+                } else {  // block-oriented: round rd pairs i with b + (i + rd) mod b
+                    i = q;
+                    j = b + (q + rd) % b;
                 }
-            } else {  // block-oriented: round rd pairs i with b + (i + rd) mod b
-                i = tid;
-                j = b + (tid + rd) % b;
-            }
-            if (i > j) { int t = i; i = j; j = t; }
-            S.pi[tid] = i;
-            S.pj[tid] = j;
-            const double a_ii = S.A[i][i], a_jj = S.A[j][j], a_ij = S.A[i][j];
-            int act = 0;
-            if (!(a_ij == 0.0 || (a.use_skip && fabs(a_ij) < a.eps * sqrt(a_ii * a_jj)))) {
-                const int hyp = S.js[i] == S.js[j] ? -1 : 1;
-                double t, c;
-                if (rotation_tc(a_ii, a_jj, a_ij, hyp, t, c) != 0) {
-                    atomicMin(&S.fail, pack_err(slot, slot_pos(i, b, I, J), slot_pos(j, b, I, J)));
+                if (i > j) { int t = i; i = j; j = t; }
+                S.pi[pb][q] = i;
+                S.pj[pb][q] = j;
+                const double a_ii = S.A[i][i], a_jj = S.A[j][j], a_ij = S.A[i][j];
+                int act = 0;
+                if (!(a_ij == 0.0 || (a.use_skip && fabs(a_ij) < a.eps * sqrt(a_ii * a_jj)))) {
+                    const int hyp = S.js[i] == S.js[j] ? -1 : 1;
+                    double t, c;
+                    if (rotation_tc(a_ii, a_jj, a_ij, hyp, t, c) != 0) {
+                        atomicMin(&S.fail, pack_err(slot, slot_pos(i, b, I, J), slot_pos(j, b, I, J)));
+                    } else {
+                        act = 1;
+                        S.rt[pb][q] = t;
+                        S.rc[pb][q] = c;
+                        S.rs[pb][q] = hyp < 0 ? -1.0 : 1.0;
+                        ++my_rot;
+                        const double at = fabs(t);
+                        my_big |= at > a.teps;
+                        my_max = fmax(my_max, at);
+                    }
                 } else {
-                    act = 1;
-                    S.rt[tid] = t;
-                    S.rc[tid] = c;
-                    S.rs[tid] = hyp < 0 ? -1.0 : 1.0;
-                    ++my_rot;
-                    const double at = fabs(t);
-                    my_big |= at > a.teps;
-                    my_max = fmax(my_max, at);
+                    ++my_skip;
                 }
-            } else {
-                ++my_skip;
+                S.act[pb][q] = act;
+                my_any |= act;
             }
-            S.act[tid] = act;
+            w_any = __any_sync(0xffffffffu, my_any);
+        } else if (rd > 0) {
+            apply_w(pb ^ 1, 32);  // previous round's W update, overlapped
         }
-        __syncthreads();
+        // any pair of this round rotating?  (skipped rounds cost one barrier)
+        const int any = __syncthreads_or(w_any);
         if (S.fail != kNoError) break;
-        // phase 2: columns of A and W (x' = (x + s t y) c, y' = (t x + y) c)
-        for (int e = tid; e < b * B2; e += kThreads) {
-            const int q = e / B2, row = e % B2;
-            if (!S.act[q]) continue;
-            const int i = S.pi[q], j = S.pj[q];
-            const double t = S.rt[q], c = S.rc[q], st = S.rs[q] * t;
-            const double x = S.A[row][i], y = S.A[row][j];
-            S.A[row][i] = fma(st, y, x) * c;
-            S.A[row][j] = fma(t, x, y) * c;
-            const double wx = S.W[row][i], wy = S.W[row][j];
-            S.W[row][i] = fma(st, wy, wx) * c;
-            S.W[row][j] = fma(t, wx, wy) * c;
+        if (!any) continue;
+        // phase 2: columns of A (x' = (x + s t y) c, y' = (t x + y) c)
+        for (int e = tid; e < b * 8; e += kThreads) {
+            const int q = e >> 3;
+            if (!S.act[pb][q]) continue;
+            const int i = S.pi[pb][q], j = S.pj[pb][q];
+            const double t = S.rt[pb][q], c = S.rc[pb][q], st = S.rs[pb][q] * t;
+            for (int row = e & 7; row < B2; row += 8) {
+                const double x = S.A[row][i], y = S.A[row][j];
+                S.A[row][i] = fma(st, y, x) * c;
+                S.A[row][j] = fma(t, x, y) * c;
+            }
         }
         __syncthreads();
-        // phase 3: rows of A
-        for (int e = tid; e < b * B2; e += kThreads) {
-            const int q = e / B2, col = e % B2;
-            if (!S.act[q]) continue;
-            const int i = S.pi[q], j = S.pj[q];
-            const double t = S.rt[q], c = S.rc[q], st = S.rs[q] * t;
-            const double x = S.A[i][col], y = S.A[j][col];
-            S.A[i][col] = fma(st, y, x) * c;
-            S.A[j][col] = fma(t, x, y) * c;
+        // phase 3: rows of A; the annihilated pair entries are set to 0
+        for (int e = tid; e < b * 8; e += kThreads) {
+            const int q = e >> 3;
+            if (!S.act[pb][q]) continue;
+            const int i = S.pi[pb][q], j = S.pj[pb][q];
+            const double t = S.rt[pb][q], c = S.rc[pb][q], st = S.rs[pb][q] * t;
+            for (int col = e & 7; col < B2; col += 8) {
+                const double x = S.A[i][col], y = S.A[j][col];
+                S.A[i][col] = col == j ? 0.0 : fma(st, y, x) * c;
+                S.A[j][col] = col == i ? 0.0 : fma(t, x, y) * c;
+            }
         }
         __syncthreads();
-        if (tid < b && S.act[tid]) {  // annihilated exactly
-            S.A[S.pi[tid]][S.pj[tid]] = 0.0;
-            S.A[S.pj[tid]][S.pi[tid]] = 0.0;
-        }
+    }
+    if (S.fail == kNoError && rounds > 0) {
+        apply_w((rounds - 1) & 1, 0);
         __syncthreads();
     }
     if (tid < b) {
@@ -392,17 +521,20 @@ __global__ void __launch_bounds__(kThreads, 2) k_update(
         cp_async16(&S.w[c][k], Wsrc + 2 * q, 16);
     }
     __syncthreads();
+    // X tile in two commit groups (K halves) so the first half's DMMAs
+    // overlap the second half's loads
     constexpr int CPC = MT / 2;  // 16-byte chunks per column
-    for (int q = tid; q < B2 * CPC; q += kThreads) {
-        const int k = q / CPC, part = q % CPC;
-        const int row = row0 + 2 * part;
-        const int rem = nrows - row;
-        const int bytes = rem >= 2 ? 16 : (rem == 1 ? 8 : 0);
-        cp_async16(&S.x[k][2 * part], bytes ? S.col[k] + row : S.col[k], bytes);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        for (int q = tid; q < (B2 / 2) * CPC; q += kThreads) {
+            const int k = h * (B2 / 2) + q / CPC, part = q % CPC;
+            const int row = row0 + 2 * part;
+            const int rem = nrows - row;
+            const int bytes = rem >= 2 ? 16 : (rem == 1 ? 8 : 0);
+            cp_async16(&S.x[k][2 * part], bytes ? S.col[k] + row : S.col[k], bytes);
+        }
+        cp_async_commit();
     }
-    cp_async_commit();
-    cp_async_wait<0>();
-    __syncthreads();
 
     constexpr int WM = MT / 4, WN = B2 / 2, MI = WM / 8, NI = WN / 8;
     const int wm = warp >> 1, wn = warp & 1;
@@ -413,17 +545,23 @@ __global__ void __launch_bounds__(kThreads, 2) k_update(
     for (int i = 0; i < MI; ++i)
 #pragma unroll
         for (int j = 0; j < NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        if (h == 0) cp_async_wait<1>();
+        else cp_async_wait<0>();
+        __syncthreads();
 #pragma unroll 4
-    for (int kk = 0; kk < B2; kk += 4) {
-        double a[MI], bb[NI];
+        for (int kk = h * (B2 / 2); kk < (h + 1) * (B2 / 2); kk += 4) {
+            double a[MI], bb[NI];
 #pragma unroll
-        for (int i = 0; i < MI; ++i) a[i] = S.x[kk + fk][m0 + 8 * i + fr];
+            for (int i = 0; i < MI; ++i) a[i] = S.x[kk + fk][m0 + 8 * i + fr];
 #pragma unroll
-        for (int j = 0; j < NI; ++j) bb[j] = S.w[n0 + 8 * j + fr][kk + fk];
+            for (int j = 0; j < NI; ++j) bb[j] = S.w[n0 + 8 * j + fr][kk + fk];
 #pragma unroll
-        for (int i = 0; i < MI; ++i)
+            for (int i = 0; i < MI; ++i)
 #pragma unroll
-            for (int j = 0; j < NI; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], bb[j]);
+                for (int j = 0; j < NI; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], bb[j]);
+        }
     }
     __syncthreads();  // everyone done reading x
 #pragma unroll
@@ -497,21 +635,50 @@ struct Carve2 {
     }
 };
 
-static int choose_ksplit(int64_t n, int64_t nslots, int KT)
+static int num_sms()
 {
-    if (nslots < 1) nslots = 1;
-    // enough CTAs for >= 2 waves of 148 SMs, each CTA >= 4 k-tiles
-    int64_t want = (2 * 148 + nslots - 1) / nslots;
-    int64_t maxs = (n + 4 * KT - 1) / (4 * KT);
-    if (want > maxs) want = maxs;
-    if (want < 1) want = 1;
-    return (int)want;
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+            sms = 148;
+    }
+    return sms;
+}
+
+constexpr int kGramKT = 32, kGramStages = 4, kGramOcc = 3;
+
+// Static Gram partition: P = #SMs x resident CTAs, capped so that a CTA
+// spans at most GramSmem::MAXSLOTS slots and owns >= 1 k-tile.
+static GramPart gram_partition(int64_t n, int64_t nslots)
+{
+    GramPart g;
+    g.T = (n + kGramKT - 1) / kGramKT;
+    g.W = nslots * g.T;
+    g.P = (int64_t)num_sms() * kGramOcc;
+    if (g.P > g.W) g.P = g.W;
+    // items per CTA >= T / 2 keeps a CTA within 4 slots: W/P <= 2T always
+    // holds for P >= nslots/2; raise P if the slots outnumber the CTAs
+    while (g.W / g.P + 2 > 4 * g.T && g.P < g.W) g.P *= 2;
+    if (g.P > g.W) g.P = g.W;
+    return g;
+}
+
+static int gram_maxseg(const GramPart &g, int64_t nslots)
+{
+    int m = 1;
+    for (int64_t s = 0; s < nslots; ++s) {
+        const int k = (int)g.nseg(s);
+        if (k > m) m = k;
+    }
+    return m;
 }
 
 static int64_t carve_block(Carve2 &c, int64_t n, int64_t r, int b, BlockWs *w)
 {
     const int64_t B2 = 2 * b, nb = r / b, nslots = nb / 2 > 0 ? nb / 2 : 1;
-    const int ks = choose_ksplit(n, nslots, 32);
+    const int ks = gram_maxseg(gram_partition(n, nslots), nslots);
     BlockWs t;
     t.d = c.take<double>(r);
     t.rho = c.take<int64_t>(r);
@@ -551,7 +718,7 @@ int launch_identity(double *V, int64_t r, int64_t ldv, cudaStream_t s);
 
 template <int B2>
 struct BlockKernels {
-    static constexpr int KT = 32, STAGES = 3, MT = 128;
+    static constexpr int KT = kGramKT, STAGES = kGramStages, MT = 128;
     static size_t gram_smem() { return sizeof(GramSmem<B2, KT, STAGES>); }
     static size_t inner_smem() { return sizeof(InnerSmem<B2>); }
     static size_t upd_smem() { return sizeof(UpdSmem<B2, MT>); }
@@ -569,21 +736,21 @@ struct BlockKernels {
     }
     // one step: Gram -> inner pass -> update
     static int step(double *G, int64_t ldg, int n, double *V, int64_t ldv, int rv,
-                    const BlockWs &w, int64_t nb, int ksplit, int full,
+                    const BlockWs &w, int64_t nb, const GramPart &gp, int maxseg, int full,
                     const hsvd_config *cfg, cudaStream_t s, KernelTimer &T)
     {
         const int64_t nslots = nb / 2;
-        const int kchunk = (int)((((int64_t)n + ksplit - 1) / ksplit + KT - 1) / KT * KT);
         T.begin(0, s);
-        k_gram<B2, KT, STAGES><<<dim3(ksplit, (unsigned)nslots), kThreads, gram_smem(), s>>>(
-            G, ldg, n, w.rho, w.iblk, w.jblk, ksplit, kchunk, w.Apart, w.err);
+        k_gram<B2, KT, STAGES><<<(unsigned)gp.P, kThreads, gram_smem(), s>>>(
+            G, ldg, n, w.rho, w.iblk, w.jblk, gp, maxseg, w.Apart, w.err);
         T.end(s);
         HSVD_LAUNCH_CHECK("k_gram");
         InnerArgs ia;
+        ia.part = gp; ia.maxseg = maxseg;
         ia.Apart = w.Apart; ia.Wg = w.Wg; ia.jsign = w.js;
         ia.ip = w.ip; ia.jp = w.jp; ia.iblk = w.iblk; ia.jblk = w.jblk; ia.cur = w.cur;
         ia.C = w.C; ia.rotk = w.rotk; ia.skipk = w.skipk; ia.maxt = w.maxt; ia.err = w.err;
-        ia.nb = nb; ia.eps = cfg->eps; ia.teps = cfg->teps; ia.ksplit = ksplit;
+        ia.nb = nb; ia.eps = cfg->eps; ia.teps = cfg->teps;
         ia.full = full; ia.use_skip = cfg->use_skip;
         T.begin(1, s);
         k_inner<B2><<<(unsigned)nslots, kThreads, inner_smem(), s>>>(ia);
@@ -624,7 +791,8 @@ static int block_drive_t(double *G, int64_t n, int64_t r, int64_t ldg, double *V
         set_error("workspace too small");
         return HSVD_ERR_ARG;
     }
-    const int ksplit = choose_ksplit(n, nslots, K::KT);
+    const GramPart gp = gram_partition(n, nslots);
+    const int maxseg = gram_maxseg(gp, nslots);
     int st = K::setup();
     if (st) return st;
 
@@ -681,7 +849,7 @@ static int block_drive_t(double *G, int64_t n, int64_t r, int64_t ldg, double *V
     auto enqueue_sweep = [&]() -> int {
         for (int64_t step = 0; step < nb; ++step) {
             const int full = cfg->inner_full || step == 0;
-            int e = K::step(G, ldg, (int)n, V, ldv, (int)r, w, nb, ksplit, full, cfg, s, T);
+            int e = K::step(G, ldg, (int)n, V, ldv, (int)r, w, nb, gp, maxseg, full, cfg, s, T);
             if (e) return e;
         }
         T.begin(3, s);
