@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--p", type=int, default=None)
     ap.add_argument("--mode", default="block", choices=["pointwise", "block"])
     ap.add_argument("--block-cols", type=int, default=32)
+    ap.add_argument("--block-rotation", default="fast", choices=["fast", "dd"])
     ap.add_argument("--cpu-sample-s", type=float, default=12.0)
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--no-cpu", action="store_true")
@@ -263,7 +264,8 @@ def run_ours(a, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     G, signs = make_input(a.n, a.p, seed=0)
     J = H.SignatureVector(signs, a.p)
-    cfg = H.SolverConfig(mode=a.mode, block_cols=a.block_cols)
+    cfg = H.SolverConfig(mode=a.mode, block_cols=a.block_cols,
+                         block_rotation=a.block_rotation)
     if a.mode == "block" and a.n % (2 * a.block_cols):
         raise SystemExit("block mode needs n to be a multiple of 2*block_cols")
     G0 = torch.from_numpy(np.ascontiguousarray(G.T)).to(dev)  # (r, n) = col-major G
@@ -315,7 +317,8 @@ def run_ours(a, rank, world, local_rank):
     n = r = a.n
     tele = res.telemetry
     prof = H.drive_device(Gw.copy_(G0), J, H.SolverConfig(
-        mode=a.mode, block_cols=a.block_cols, max_sweeps=1, profile=True))
+        mode=a.mode, block_cols=a.block_cols, block_rotation=a.block_rotation,
+        max_sweeps=1, profile=True))
     kp = prof.kernel_profile
     peaks = {}
     if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")):
@@ -412,6 +415,8 @@ def run_ours(a, rank, world, local_rank):
             "data": "synthetic: numpy default_rng(0).standard_normal((n,n)), J=diag(+1 x p, -1 x n-p)",
             "config": {"workload": f"n={a.n} p={a.p} full HSVD with V^-T (SURVEY.md §8(d) cfg 5)",
                        "n": a.n, "p": a.p, "mode": a.mode,
+                       **({"block_cols": a.block_cols, "block_rotation": a.block_rotation}
+                          if a.mode == "block" else {}),
                        "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
                        "l2": "inputs larger than L2 (G and V^-T are n*n*8 B each)"},
             "sweeps": res.sweeps_used, "stop_reason": res.stop_reason,

@@ -41,6 +41,10 @@ extern "C" {
 #define HSVD_MODE_POINTWISE 0 /* bit-exact mirror of the reference          */
 #define HSVD_MODE_BLOCK 1     /* block-column pairs, FP64 DMMA Gram/update  */
 
+/* ---- block-mode 2x2 rotation formula ----------------------------------- */
+#define HSVD_ROTATION_DD 0   /* the reference's double-double rotation_tc  */
+#define HSVD_ROTATION_FAST 1 /* plain fp64, same branches and tests         */
+
 /* ---- schedules (solver.py:204-209) ------------------------------------- */
 #define HSVD_SCHEDULE_MODULUS 0
 #define HSVD_SCHEDULE_ROW_CYCLIC 1
@@ -61,6 +65,7 @@ typedef struct hsvd_config {
     int32_t use_graph;    /* capture each sweep as a CUDA graph           */
     int32_t profile;      /* time every kernel of sweep 0 with CUDA events
                              (no graph); fills hsvd_result.kernel_ms     */
+    int32_t block_rotation; /* block mode: HSVD_ROTATION_*               */
 } hsvd_config;
 
 /* Per-run result record: the scalar part of HsvdResult (solver.py:67-77). */

@@ -50,6 +50,7 @@ class HsvdConfigC(ctypes.Structure):
         ("inner_full", ctypes.c_int32),
         ("use_graph", ctypes.c_int32),
         ("profile", ctypes.c_int32),
+        ("block_rotation", ctypes.c_int32),
     ]
 
 

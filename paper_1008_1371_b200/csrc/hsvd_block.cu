@@ -281,9 +281,10 @@ struct InnerArgs {
     int64_t *ip, *jp, *iblk, *jblk, *cur;
     uint8_t *C;
     uint32_t *rotk, *skipk;
+    uint8_t *wact;
     double *maxt;
     unsigned long long *err;
-    int64_t nb;
+    int64_t nb, slot_base;
     double eps, teps;
     int full, use_skip;
 };
@@ -293,37 +294,111 @@ struct InnerSmem {
     static constexpr int LD = B2 + 1;
     double A[B2][LD];
     double W[B2][LD];
-    // rotation parameters, double-buffered by round parity: the W update of
-    // round r-1 runs on warps 1.. while warp 0 forms round r's rotations
-    double rt[2][B2 / 2], rc[2][B2 / 2], rs[2][B2 / 2];
-    int pi[2][B2 / 2], pj[2][B2 / 2], act[2][B2 / 2];
+    // the round's rotations (written by warp 0, read after the barrier)
+    double pt[B2 / 2], pc[B2 / 2], ps[B2 / 2];
+    int pi[B2 / 2], pj[B2 / 2];
     int js[B2];
     unsigned int rot, skip, big;
     unsigned long long maxt_bits;
     unsigned long long fail;
 };
 
-template <int B2>
+// Plain-double annihilating rotation for block mode (the pointwise mode keeps
+// the reference's double-double rotation_tc, hsvd_rotation.cuh).  Same
+// branches, same sign convention and same definiteness test as rotation_tc
+// (_kernels.py:128-173): trig t = sgn(zeta)/(|zeta| + sqrt(1 + zeta^2)),
+// hyperbolic t = theta/(1 + sqrt(1 - theta^2)); 1 - x^2 by one fma.
+__device__ __forceinline__ int rotation_fast(double a_ii, double a_jj, double a_ij, int hyp,
+                                             double &t_out, double &c_out)
+{
+    t_out = 0.0;
+    c_out = 1.0;
+    if (a_ij == 0.0) return 0;
+    if (hyp < 0) {
+        const double zeta = (a_jj - a_ii) / (2.0 * a_ij);
+        if (fabs(zeta) > 6.7e7) {
+            t_out = 0.5 / zeta;
+            return 0;
+        }
+        const double az = fabs(zeta);
+        double t = 1.0 / (az + sqrt(fma(az, az, 1.0)));
+        if (!(zeta >= 0.0)) t = -t;
+        t_out = t;
+        c_out = rsqrt(fma(t, t, 1.0));
+        return 0;
+    }
+    const double th = (-2.0 * a_ij) / (a_ii + a_jj);
+    const double d = fma(-th, th, 1.0);
+    if (!(d > 0.0)) return 1;
+    const double t = th / (1.0 + sqrt(d));
+    const double u = fma(-t, t, 1.0);
+    if (!(u > 0.0)) return 1;
+    t_out = t;
+    c_out = rsqrt(u);
+    return 0;
+}
+
+// One pass of disjoint 2x2 rotations on the 2b x 2b pivot Gram A_P in shared
+// memory, accumulating W_P (A_P <- W^T A_P W, W J-orthogonal).
+//
+// A round's b pairs are disjoint, so the round is the congruence
+// A <- R^T A R with R block-diagonal in 2x2 blocks: every 2x2 block (p, q) of
+// A (rows {i_p, j_p}, columns {i_q, j_q}) becomes R_p^T A_pq R_q on its own.
+// Every warp computes all b rotations of the round redundantly (lane q owns
+// pair q; a warp-uniform decision skips inactive rounds without a barrier),
+// then updates its share of the blocks and of W from registers and shuffles:
+// two barriers per active round, none per inactive round.
+template <int B2, bool FAST>
 __global__ void __launch_bounds__(kThreads) k_inner(InnerArgs a)
 {
     extern __shared__ __align__(16) unsigned char ism_raw[];
     auto &S = *reinterpret_cast<InnerSmem<B2> *>(ism_raw);
     if (*(volatile unsigned long long *)a.err != kNoError) return;
-    constexpr int b = B2 / 2;
-    const int slot = blockIdx.x, tid = threadIdx.x;
+    constexpr int b = B2 / 2;    // pairs per round
+    const int slot = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     int64_t I = a.iblk[slot], J = a.jblk[slot];
     if (I > J) { int64_t t = I; I = J; J = t; }
 
-    // A = sum of the slot's partial segments (fixed order), upper mirrored
+    // A = sum of the slot's partial segments in segment order (the upper
+    // triangle is read coalesced and mirrored); all loads of a batch of
+    // segments are issued before the sums
     const double *P0 = a.Apart + (int64_t)slot * a.maxseg * (B2 * B2);
     const int nseg = (int)a.part.nseg(slot);
-    for (int e = tid; e < B2 * B2; e += kThreads) {
-        const int i = e / B2, j = e % B2;
-        const int lo = min(i, j), hi = max(i, j);
-        double v = 0.0;
-        for (int s = 0; s < nseg; ++s) v += P0[(int64_t)s * B2 * B2 + lo * B2 + hi];
-        S.A[i][j] = v;
+    constexpr int PER = B2 * B2 / kThreads;
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+        const int e = tid + k * kThreads, i = e / B2, j = e % B2;
         S.W[i][j] = i == j ? 1.0 : 0.0;
+    }
+    {
+        double v[PER];
+#pragma unroll
+        for (int k = 0; k < PER; ++k) v[k] = 0.0;
+        constexpr int BATCH = 2;
+        for (int s0 = 0; s0 < nseg; s0 += BATCH) {
+            double x[BATCH][PER];
+#pragma unroll
+            for (int u = 0; u < BATCH; ++u)
+#pragma unroll
+                for (int k = 0; k < PER; ++k) {
+                    const int e = tid + k * kThreads;
+                    x[u][k] = (s0 + u < nseg && e / B2 <= e % B2)
+                                  ? P0[(int64_t)(s0 + u) * B2 * B2 + e] : 0.0;
+                }
+#pragma unroll
+            for (int u = 0; u < BATCH; ++u)
+#pragma unroll
+                for (int k = 0; k < PER; ++k)
+                    if (s0 + u < nseg) v[k] += x[u][k];
+        }
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int e = tid + k * kThreads, i = e / B2, j = e % B2;
+            if (i <= j) {
+                S.A[i][j] = v[k];
+                S.A[j][i] = v[k];
+            }
+        }
     }
     if (tid < B2) S.js[tid] = (int)a.jsign[slot_pos(tid, b, I, J)];
     if (tid == 0) {
@@ -336,110 +411,114 @@ __global__ void __launch_bounds__(kThreads) k_inner(InnerArgs a)
     const int rounds = a.full ? B2 - 1 : b;
     unsigned int my_rot = 0, my_skip = 0, my_big = 0;
     double my_max = 0.0;
-    // Thread-to-work map of the update phases: pair q = e / RPT, rows
-    // (e % RPT) + RPT * k; the pair's parameters are read once per thread.
-    // W <- W R for the rotations of buffer pb, by threads [t0, kThreads)
-    auto apply_w = [&](int pb, int t0) {
-        const int nt = kThreads - t0;
-        for (int e = tid - t0; e < b * 8; e += nt) {
-            const int q = e >> 3;
-            if (!S.act[pb][q]) continue;
-            const int i = S.pi[pb][q], j = S.pj[pb][q];
-            const double t = S.rt[pb][q], c = S.rc[pb][q], st = S.rs[pb][q] * t;
-            for (int row = e & 7; row < B2; row += 8) {
-                const double wx = S.W[row][i], wy = S.W[row][j];
-                S.W[row][i] = fma(st, wy, wx) * c;
-                S.W[row][j] = fma(t, wx, wy) * c;
-            }
-        }
-    };
+    static_assert(b == 16 || b == 32, "k_inner: b must be 16 or 32");
+    constexpr int PSTRIDE = kThreads / b;   // row-pair stride of phase U
+    constexpr int NBK = b * b / kThreads;   // A blocks per thread per round
+    constexpr int NWR = B2 * b / kThreads;  // W rows per thread per round
+    const int q = lane % b;                 // pair owned by this thread
+    const int prow = tid / b;
     for (int rd = 0; rd < rounds; ++rd) {
-        const int pb = rd & 1;
-        int w_any = 0;
-        if (tid < 32) {
-            // phase 1 (warp 0): the round's b disjoint pairs and rotations
-            int my_any = 0;
-            for (int q = tid; q < b; q += 32) {
-                int i, j;
-                if (a.full) {  // circle method on B2 players
-                    const int m = B2 - 1;
-                    if (q == 0) {
-                        i = m;
-                        j = rd;
-                    } else {
-                        i = (rd + q) % m;
-                        j = (rd - q + m) % m;
-                    }
-                } else {  // block-oriented: round rd pairs i with b + (i + rd) mod b
-                    i = q;
-                    j = b + (q + rd) % b;
-                }
-                if (i > j) { int t = i; i = j; j = t; }
-                S.pi[pb][q] = i;
-                S.pj[pb][q] = j;
-                const double a_ii = S.A[i][i], a_jj = S.A[j][j], a_ij = S.A[i][j];
-                int act = 0;
-                if (!(a_ij == 0.0 || (a.use_skip && fabs(a_ij) < a.eps * sqrt(a_ii * a_jj)))) {
-                    const int hyp = S.js[i] == S.js[j] ? -1 : 1;
-                    double t, c;
-                    if (rotation_tc(a_ii, a_jj, a_ij, hyp, t, c) != 0) {
-                        atomicMin(&S.fail, pack_err(slot, slot_pos(i, b, I, J), slot_pos(j, b, I, J)));
-                    } else {
-                        act = 1;
-                        S.rt[pb][q] = t;
-                        S.rc[pb][q] = c;
-                        S.rs[pb][q] = hyp < 0 ? -1.0 : 1.0;
-                        ++my_rot;
-                        const double at = fabs(t);
-                        my_big |= at > a.teps;
-                        my_max = fmax(my_max, at);
-                    }
+        // ---- phase R: every warp forms all b rotations of the round
+        int i, j;
+        if (a.full) {  // circle method on B2 players
+            const int m = B2 - 1;
+            if (q == 0) { i = m; j = rd; }
+            else { i = (rd + q) % m; j = (rd - q + m) % m; }
+        } else {  // block-oriented: round rd pairs i with b + (i + rd) mod b
+            i = q;
+            j = b + (q + rd) % b;
+        }
+        if (i > j) { const int t = i; i = j; j = t; }
+        const double a_ii = S.A[i][i], a_jj = S.A[j][j], a_ij = S.A[i][j];
+        double t = 0.0, c = 1.0, st = 0.0;
+        int act = 0, bad = 0;
+        if (!(a_ij == 0.0 || (a.use_skip && fabs(a_ij) < a.eps * sqrt(a_ii * a_jj)))) {
+            const int hyp = S.js[i] == S.js[j] ? -1 : 1;
+            const int status = FAST ? rotation_fast(a_ii, a_jj, a_ij, hyp, t, c)
+                                    : rotation_tc(a_ii, a_jj, a_ij, hyp, t, c);
+            if (status != 0) {
+                bad = 1;
+                t = 0.0;
+                c = 1.0;
+            } else {
+                act = 1;
+                st = hyp < 0 ? -t : t;
+            }
+        }
+        if (warp == 0 && lane < b) {
+            S.pt[q] = t;
+            S.pc[q] = c;
+            S.ps[q] = st;
+            S.pi[q] = i;
+            S.pj[q] = j;
+            if (bad) atomicMin(&S.fail, pack_err(a.slot_base + slot, slot_pos(i, b, I, J),
+                                                 slot_pos(j, b, I, J)));
+            else if (act) {
+                ++my_rot;
+                const double at = fabs(t);
+                my_big |= at > a.teps;
+                my_max = fmax(my_max, at);
+            } else {
+                ++my_skip;
+            }
+        }
+        if (__any_sync(0xffffffffu, bad)) break;  // identical in every warp
+        if (!__any_sync(0xffffffffu, act)) continue;
+        __syncthreads();  // the round's inputs are read, its rotations published
+        // ---- phase U.  This thread owns pair q (its own registers) as the
+        // column pair of blocks (p, q), p = prow + k * PSTRIDE, and of the
+        // W rows prow + k * PSTRIDE.
+        {
+            double x[NBK][4], tp[NBK], cp[NBK], sp[NBK];
+            int ip[NBK], jp[NBK];
+#pragma unroll
+            for (int k = 0; k < NBK; ++k) {
+                const int p = prow + k * PSTRIDE;
+                tp[k] = S.pt[p];
+                cp[k] = S.pc[p];
+                sp[k] = S.ps[p];
+                ip[k] = S.pi[p];
+                jp[k] = S.pj[p];
+                x[k][0] = S.A[ip[k]][i];
+                x[k][1] = S.A[ip[k]][j];
+                x[k][2] = S.A[jp[k]][i];
+                x[k][3] = S.A[jp[k]][j];
+            }
+#pragma unroll
+            for (int k = 0; k < NBK; ++k) {
+                if (t == 0.0 && tp[k] == 0.0) continue;
+                // Y = X R_q (columns), X' = R_p^T Y (rows)
+                const double y00 = fma(st, x[k][1], x[k][0]) * c;
+                const double y01 = fma(t, x[k][0], x[k][1]) * c;
+                const double y10 = fma(st, x[k][3], x[k][2]) * c;
+                const double y11 = fma(t, x[k][2], x[k][3]) * c;
+                S.A[ip[k]][i] = fma(sp[k], y10, y00) * cp[k];
+                S.A[jp[k]][j] = fma(tp[k], y01, y11) * cp[k];
+                if (prow + k * PSTRIDE == q) {  // the pair itself: annihilated
+                    S.A[ip[k]][j] = 0.0;
+                    S.A[jp[k]][i] = 0.0;
                 } else {
-                    ++my_skip;
+                    S.A[ip[k]][j] = fma(sp[k], y11, y01) * cp[k];
+                    S.A[jp[k]][i] = fma(tp[k], y00, y10) * cp[k];
                 }
-                S.act[pb][q] = act;
-                my_any |= act;
             }
-            w_any = __any_sync(0xffffffffu, my_any);
-        } else if (rd > 0) {
-            apply_w(pb ^ 1, 32);  // previous round's W update, overlapped
-        }
-        // any pair of this round rotating?  (skipped rounds cost one barrier)
-        const int any = __syncthreads_or(w_any);
-        if (S.fail != kNoError) break;
-        if (!any) continue;
-        // phase 2: columns of A (x' = (x + s t y) c, y' = (t x + y) c)
-        for (int e = tid; e < b * 8; e += kThreads) {
-            const int q = e >> 3;
-            if (!S.act[pb][q]) continue;
-            const int i = S.pi[pb][q], j = S.pj[pb][q];
-            const double t = S.rt[pb][q], c = S.rc[pb][q], st = S.rs[pb][q] * t;
-            for (int row = e & 7; row < B2; row += 8) {
-                const double x = S.A[row][i], y = S.A[row][j];
-                S.A[row][i] = fma(st, y, x) * c;
-                S.A[row][j] = fma(t, x, y) * c;
+            if (t != 0.0) {  // W <- W R_q on this thread's rows
+                double wx[NWR], wy[NWR];
+#pragma unroll
+                for (int k = 0; k < NWR; ++k) {
+                    wx[k] = S.W[prow + k * PSTRIDE][i];
+                    wy[k] = S.W[prow + k * PSTRIDE][j];
+                }
+#pragma unroll
+                for (int k = 0; k < NWR; ++k) {
+                    S.W[prow + k * PSTRIDE][i] = fma(st, wy[k], wx[k]) * c;
+                    S.W[prow + k * PSTRIDE][j] = fma(t, wx[k], wy[k]) * c;
+                }
             }
         }
-        __syncthreads();
-        // phase 3: rows of A; the annihilated pair entries are set to 0
-        for (int e = tid; e < b * 8; e += kThreads) {
-            const int q = e >> 3;
-            if (!S.act[pb][q]) continue;
-            const int i = S.pi[pb][q], j = S.pj[pb][q];
-            const double t = S.rt[pb][q], c = S.rc[pb][q], st = S.rs[pb][q] * t;
-            for (int col = e & 7; col < B2; col += 8) {
-                const double x = S.A[i][col], y = S.A[j][col];
-                S.A[i][col] = col == j ? 0.0 : fma(st, y, x) * c;
-                S.A[j][col] = col == i ? 0.0 : fma(t, x, y) * c;
-            }
-        }
-        __syncthreads();
+        __syncthreads();  // the round's updates are visible
     }
-    if (S.fail == kNoError && rounds > 0) {
-        apply_w((rounds - 1) & 1, 0);
-        __syncthreads();
-    }
-    if (tid < b) {
+    if (warp == 0) {
         atomicAdd(&S.rot, my_rot);
         atomicAdd(&S.skip, my_skip);
         atomicOr(&S.big, my_big);
@@ -454,6 +533,8 @@ __global__ void __launch_bounds__(kThreads) k_inner(InnerArgs a)
     double *Wout = a.Wg + (int64_t)slot * B2 * B2;
     for (int e = tid; e < B2 * B2; e += kThreads) Wout[e] = S.W[e % B2][e / B2];
     if (tid == 0) {
+        // W == I exactly when nothing rotated: k_update skips the slot
+        a.wact[slot] = S.rot != 0;
         // convergence code (_kernels.py:227-231 semantics per slot)
         if (S.big) a.C[slot] = 3;
         else if (S.rot) a.C[slot] |= 1;
@@ -499,13 +580,15 @@ template <int B2, int MT>
 __global__ void __launch_bounds__(kThreads, 2) k_update(
     double *__restrict__ G, int64_t ldg, int n, double *__restrict__ V, int64_t ldv, int rv,
     const int64_t *__restrict__ rho, const int64_t *__restrict__ cur,
-    const double *__restrict__ Wg, int tiles_g, const unsigned long long *err)
+    const double *__restrict__ Wg, const uint8_t *__restrict__ wact, int tiles_g,
+    const unsigned long long *err)
 {
     extern __shared__ __align__(16) unsigned char usm_raw[];
     auto &S = *reinterpret_cast<UpdSmem<B2, MT> *>(usm_raw);
     if (*(volatile const unsigned long long *)err != kNoError) return;
     constexpr int b = B2 / 2;
     const int slot = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (!wact[slot]) return;  // no rotation in this slot: W == I
     const bool isV = (int)blockIdx.x >= tiles_g;
     const int tile = isV ? blockIdx.x - tiles_g : blockIdx.x;
     const int nrows = isV ? rv : n;
@@ -613,7 +696,7 @@ __global__ void k_block_norms(const double *__restrict__ G, int64_t ldg, int n,
 struct BlockWs {
     double *d, *Apart, *Wg;
     int64_t *rho, *js, *ip, *jp, *iblk, *jblk, *cur;
-    uint8_t *C;
+    uint8_t *C, *wact;
     uint32_t *rotk, *skipk;
     double *maxt;
     unsigned long long *err, *first_zero;
@@ -689,6 +772,7 @@ static int64_t carve_block(Carve2 &c, int64_t n, int64_t r, int b, BlockWs *w)
     t.jblk = c.take<int64_t>(nslots);
     t.cur = c.take<int64_t>(2 * nslots);
     t.C = c.take<uint8_t>(nslots);
+    t.wact = c.take<uint8_t>(nslots);
     t.rotk = c.take<uint32_t>(nslots);
     t.skipk = c.take<uint32_t>(nslots);
     t.maxt = c.take<double>(nslots);
@@ -727,7 +811,11 @@ struct BlockKernels {
         HSVD_CUDA(cudaFuncSetAttribute(k_gram<B2, KT, STAGES>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)gram_smem()));
-        HSVD_CUDA(cudaFuncSetAttribute(k_inner<B2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        HSVD_CUDA(cudaFuncSetAttribute(k_inner<B2, true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)inner_smem()));
+        HSVD_CUDA(cudaFuncSetAttribute(k_inner<B2, false>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)inner_smem()));
         HSVD_CUDA(cudaFuncSetAttribute(k_update<B2, MT>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -749,18 +837,21 @@ struct BlockKernels {
         ia.part = gp; ia.maxseg = maxseg;
         ia.Apart = w.Apart; ia.Wg = w.Wg; ia.jsign = w.js;
         ia.ip = w.ip; ia.jp = w.jp; ia.iblk = w.iblk; ia.jblk = w.jblk; ia.cur = w.cur;
-        ia.C = w.C; ia.rotk = w.rotk; ia.skipk = w.skipk; ia.maxt = w.maxt; ia.err = w.err;
-        ia.nb = nb; ia.eps = cfg->eps; ia.teps = cfg->teps;
+        ia.C = w.C; ia.wact = w.wact; ia.rotk = w.rotk; ia.skipk = w.skipk; ia.maxt = w.maxt; ia.err = w.err;
+        ia.nb = nb; ia.slot_base = 0; ia.eps = cfg->eps; ia.teps = cfg->teps;
         ia.full = full; ia.use_skip = cfg->use_skip;
         T.begin(1, s);
-        k_inner<B2><<<(unsigned)nslots, kThreads, inner_smem(), s>>>(ia);
+        if (cfg->block_rotation == HSVD_ROTATION_FAST)
+            k_inner<B2, true><<<(unsigned)nslots, kThreads, inner_smem(), s>>>(ia);
+        else
+            k_inner<B2, false><<<(unsigned)nslots, kThreads, inner_smem(), s>>>(ia);
         T.end(s);
         HSVD_LAUNCH_CHECK("k_inner");
         const int tiles_g = (n + MT - 1) / MT;
         const int tiles_v = V ? (rv + MT - 1) / MT : 0;
         T.begin(2, s);
         k_update<B2, MT><<<dim3(tiles_g + tiles_v, (unsigned)nslots), kThreads, upd_smem(), s>>>(
-            G, ldg, n, V, ldv, rv, w.rho, w.cur, w.Wg, tiles_g, w.err);
+            G, ldg, n, V, ldv, rv, w.rho, w.cur, w.Wg, w.wact, tiles_g, w.err);
         T.end(s);
         HSVD_LAUNCH_CHECK("k_update");
         return HSVD_OK;

@@ -312,6 +312,7 @@ void hsvd_default_config(hsvd_config *cfg)
     cfg->block_cols = 32;
     cfg->inner_full = 0;
     cfg->use_graph = 1;
+    cfg->block_rotation = HSVD_ROTATION_FAST;
 }
 
 int64_t hsvd_drive_workspace_size(int64_t n, int64_t r, const hsvd_config *cfg)

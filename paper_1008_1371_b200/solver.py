@@ -60,6 +60,9 @@ class SolverConfig:
     inner_ordering: str = "oriented"
     use_graph: bool = True
     profile: bool = False
+    #: block mode 2x2 rotation: "fast" (plain fp64) or "dd" (the reference's
+    #: double-double rotation_tc, _kernels.py:128-173)
+    block_rotation: str = "fast"
 
     def __post_init__(self):
         if self.teps is None:
@@ -72,6 +75,8 @@ class SolverConfig:
             raise ValueError(f"unknown mode {self.mode!r}")
         if self.inner_ordering not in ("oriented", "full"):
             raise ValueError(f"unknown inner_ordering {self.inner_ordering!r}")
+        if self.block_rotation not in ("fast", "dd"):
+            raise ValueError(f"unknown block_rotation {self.block_rotation!r}")
 
     def to_c(self):
         c = _lib.HsvdConfigC()
@@ -89,6 +94,7 @@ class SolverConfig:
         c.inner_full = int(self.inner_ordering == "full")
         c.use_graph = int(bool(self.use_graph))
         c.profile = int(bool(self.profile))
+        c.block_rotation = int(self.block_rotation == "fast")
         return c
 
 

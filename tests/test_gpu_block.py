@@ -31,13 +31,15 @@ CASES = [
 ]
 
 
+@pytest.mark.parametrize("rot", ["fast", "dd"])
 @pytest.mark.parametrize("case", CASES, ids=lambda c: f"n{c[0]}r{c[1]}p{c[2]}{c[4]}b{c[5]}")
-def test_block_matches_reference(case):
+def test_block_matches_reference(case, rot):
     n, r, p, seed, kind, b = case
     G = make_case_input(n, r, seed, kind)
     signs = np.array([1] * p + [-1] * (r - p), np.int8)
     ref = O.drive(G, signs, p)
-    res = H.drive(G, H.SignatureVector(signs, p), H.SolverConfig(mode="block", block_cols=b))
+    res = H.drive(G, H.SignatureVector(signs, p),
+                  H.SolverConfig(mode="block", block_cols=b, block_rotation=rot))
     assert res.stop_reason in ("orthogonal", "quadratic")
     d = sigma_class_reldiff(res.sigma, res.lam, ref.sigma, ref.lam)
     assert d <= SIGMA_RTOL, d
