@@ -195,6 +195,68 @@ HSVD_API int hsvd_drive_host(const double *G_host, int64_t n, int64_t r,
                     double *Vinv_t_host, double *sigma_host, double *lam_host,
                     hsvd_result *res_host, hsvd_telemetry *tele_host);
 
+/* ---- multi-GPU: block mode sharded over N GPUs --------
+ *
+ * The reference splits the slots of a step into contiguous ranges and runs
+ * them on worker threads (_run_ranges, solver.py:124-156); here the ranges
+ * are GPUs.  Shard g owns slots [g*S/N, (g+1)*S/N) of the S = r/(2b) block
+ * slots and keeps their block columns resident; after every step one block
+ * column moves to a ring neighbour (NCCL send/recv), after every sweep the
+ * norms are all-gathered, every shard runs the same stable sort, and the
+ * columns are redistributed (grouped all-to-all).  Block mode only. */
+
+/* NCCL communicator (NCCL is dlopen-ed; HSVD_ERR_UNSUPPORTED if absent).
+ * Rank 0 creates the 128-byte id, the caller broadcasts it (e.g. with
+ * torch.distributed), every rank calls hsvd_comm_init with its CUDA device
+ * current. */
+HSVD_API int hsvd_comm_unique_id(uint8_t *id_out);
+HSVD_API int hsvd_comm_init(const uint8_t *id, int nranks, int rank, void **comm_out);
+HSVD_API int hsvd_comm_destroy(void *comm);
+
+/* Columns shard `shard` returns (2 * its slots * b), -1 if r, b, nshards
+ * do not shard (need r/(2b) >= nshards). */
+HSVD_API int64_t hsvd_shard_columns(int64_t r, int32_t block_cols, int32_t nshards,
+                                    int32_t shard);
+/* Device scratch bytes of one shard. */
+HSVD_API int64_t hsvd_sharded_workspace_size(int64_t n, int64_t r, int32_t nshards,
+                                             int32_t shard, const hsvd_config *cfg);
+
+/* Sharded solve.  comm != NULL: one process per GPU, nlocal == 1 and
+ * shard_ids[0] == rank.  comm == NULL: this process drives all nshards
+ * shards (nlocal == nshards; devices[i] may repeat -- the local transport
+ * copies with cudaMemcpyPeerAsync).  Per local shard i: G[i] is the FULL
+ * n x r factor (ldg) on devices[i] (read only); the outputs hold the
+ * shard's hsvd_shard_columns() columns after the final sweep:
+ * U_out[i] (n x cols, ld n), V_out[i] (r x cols of V^{-T}, ld r, may be
+ * NULL without accumulate_v), sigma_out[i] / lam_out[i] (device) and
+ * cols_host[i] (host int64: the ORIGINAL column index of each returned
+ * column).  ws[i] / ws_bytes[i]: hsvd_sharded_workspace_size bytes on
+ * devices[i].  Statuses as hsvd_drive; every rank returns the same one. */
+HSVD_API int hsvd_drive_sharded(void *comm, int32_t nshards, int32_t nlocal,
+                                const int32_t *shard_ids, const int32_t *devices,
+                                const double *const *G, int64_t n, int64_t r, int64_t ldg,
+                                const int8_t *signs_host, int64_t p, const hsvd_config *cfg,
+                                double *const *U_out, double *const *V_out,
+                                int64_t *const *cols_host, double *const *sigma_out,
+                                double *const *lam_out, void *const *ws,
+                                const int64_t *ws_bytes, hsvd_result *res_host,
+                                hsvd_telemetry *tele_host);
+
+/* The shard plan alone (host only, no GPU): the stepper of all slots, the
+ * block placement and the per-step block moves, for tests of the exchange
+ * protocol.  hsvd_plan_advance writes (block, from, from_area, to, to_area)
+ * per move and returns the count (-1 on error). */
+HSVD_API void *hsvd_plan_create(int64_t nblocks, int32_t nshards);
+HSVD_API void hsvd_plan_destroy(void *plan);
+HSVD_API int64_t hsvd_plan_advance(void *plan, int64_t *moves, int64_t max_moves);
+HSVD_API int hsvd_plan_state(void *plan, int64_t *iblk, int64_t *jblk, int32_t *owner,
+                             int32_t *area, int64_t *slot_begin);
+HSVD_API int hsvd_plan_redistribute(void *plan, int32_t b, const int64_t *rho_old,
+                                    const int64_t *rho_new, int64_t r, int32_t shard,
+                                    int64_t *send, int64_t *send_count, int64_t *recv,
+                                    int64_t *recv_count);
+HSVD_API void hsvd_plan_place(void *plan);
+
 #ifdef __cplusplus
 }
 #endif

@@ -51,6 +51,13 @@ from .solver import (
     sort_diagonal,
     strip_bordered,
 )
+from .sharded import (
+    ShardComm,
+    ShardedResult,
+    drive_local_shards,
+    drive_sharded,
+    gather_result,
+)
 from .strategies import (
     StepperState,
     schedule_table,

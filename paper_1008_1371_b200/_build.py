@@ -14,12 +14,28 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
           "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr"]
 
+def _nccl_include():
+    """nccl.h of the NCCL torch loads (types only: the library is dlopen-ed)."""
+    try:
+        import nvidia.nccl
+        for base in nvidia.nccl.__path__:
+            inc = os.path.join(base, "include")
+            if os.path.exists(os.path.join(inc, "nccl.h")):
+                return inc
+    except ImportError:
+        pass
+    return "/usr/include"
+
+
+NCCL_INC = _nccl_include()
+
 # translation unit -> extra flags.  The pointwise TU is the bit-exact mirror
 # of the reference and must not contract a*b+c into FMA.
 UNITS = {
     "hsvd_pointwise.cu": ["-fmad=false"],
     "hsvd_driver.cu": ["-fmad=false"],
     "hsvd_block.cu": [],
+    "hsvd_sharded.cu": ["-I" + NCCL_INC],
 }
 
 
@@ -55,7 +71,7 @@ def build(force=False, verbose=False):
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
         objs.append(obj)
-    cmd = [nvcc(), *ARCH, "-shared", "-o", LIB, *objs, "-lcudart"]
+    cmd = [nvcc(), *ARCH, "-shared", "-o", LIB, *objs, "-lcudart", "-ldl"]
     subprocess.run(cmd, check=True)
     for o in objs:
         os.remove(o)

@@ -32,6 +32,10 @@ EXPORTED = (
     "hsvd_stepper_init", "hsvd_sort_diagonal", "hsvd_reduce_sweep",
     "hsvd_extract", "hsvd_drive_workspace_size", "hsvd_drive",
     "hsvd_drive_host",
+    "hsvd_comm_unique_id", "hsvd_comm_init", "hsvd_comm_destroy",
+    "hsvd_shard_columns", "hsvd_sharded_workspace_size", "hsvd_drive_sharded",
+    "hsvd_plan_create", "hsvd_plan_destroy", "hsvd_plan_advance", "hsvd_plan_state",
+    "hsvd_plan_redistribute", "hsvd_plan_place",
 )
 
 
@@ -112,6 +116,22 @@ _SIGS = {
                                        ctypes.POINTER(HsvdConfigC), _P, _P, _P,
                                        _P, ctypes.POINTER(HsvdResultC),
                                        ctypes.POINTER(HsvdTelemetryC)]),
+    "hsvd_comm_unique_id": (ctypes.c_int, [_P]),
+    "hsvd_comm_init": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_P)]),
+    "hsvd_comm_destroy": (ctypes.c_int, [_P]),
+    "hsvd_shard_columns": (ctypes.c_int64, [_I64, _I32, _I32, _I32]),
+    "hsvd_sharded_workspace_size": (ctypes.c_int64, [_I64, _I64, _I32, _I32,
+                                                     ctypes.POINTER(HsvdConfigC)]),
+    "hsvd_drive_sharded": (ctypes.c_int, [_P, _I32, _I32, _P, _P, _P, _I64, _I64, _I64, _P,
+                                          _I64, ctypes.POINTER(HsvdConfigC), _P, _P, _P, _P,
+                                          _P, _P, _P, ctypes.POINTER(HsvdResultC),
+                                          ctypes.POINTER(HsvdTelemetryC)]),
+    "hsvd_plan_create": (_P, [_I64, _I32]),
+    "hsvd_plan_destroy": (None, [_P]),
+    "hsvd_plan_advance": (ctypes.c_int64, [_P, _P, _I64]),
+    "hsvd_plan_state": (ctypes.c_int, [_P, _P, _P, _P, _P, _P]),
+    "hsvd_plan_redistribute": (ctypes.c_int, [_P, _I32, _P, _P, _I64, _I32, _P, _P, _P, _P]),
+    "hsvd_plan_place": (None, [_P]),
 }
 
 _lib = None

@@ -1,0 +1,808 @@
+// hsvd_block_kernels.cuh -- the block-column kernels of one step (Gram,
+// inner rotations, update) and their launch wrapper, shared by the one-GPU
+// driver (hsvd_block.cu) and the sharded multi-GPU driver (hsvd_sharded.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "hsvd_internal.cuh"
+#include "hsvd_rotation.cuh"
+
+namespace hsvd {
+
+// ---------------------------------------------------------------------
+// PTX helpers
+// ---------------------------------------------------------------------
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem, int src_bytes)
+{
+    unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem),
+                 "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// D(8x8) += A(8x4, row) * B(4x8, col), FP64 tensor core.
+// a = A[lane>>2][lane&3], b = B[lane&3][lane>>2],
+// d = {D[lane>>2][2*(lane&3)], D[lane>>2][2*(lane&3)+1]}.
+__device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b)
+{
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+constexpr int kThreads = 256;
+
+// position of column c (0..2b) of slot P = (I, J), I < J
+__device__ __forceinline__ int64_t slot_pos(int c, int b, int64_t I, int64_t J)
+{
+    return c < b ? I * b + c : J * b + (c - b);
+}
+
+// ---------------------------------------------------------------------
+// k_gram: partial Gram matrices over a static "stream-K" partition
+// ---------------------------------------------------------------------
+// The work of one step is W = nslots * T k-tiles (T = ceil(n / KT)).  The
+// grid has P = (#SMs x resident CTAs) CTAs and CTA c owns the contiguous
+// item range [c*W/P, (c+1)*W/P): every SM gets the same number of DMMAs,
+// with no wave tail.  A CTA flushes one partial Gram per slot segment it
+// covers; k_inner sums a slot's partials in segment order, so the result
+// is deterministic for a given P.
+struct GramPart {
+    int64_t W, P, T;
+    __host__ __device__ int64_t begin(int64_t c) const { return c * W / P; }
+    // CTA owning item x
+    __host__ __device__ int64_t owner(int64_t x) const
+    {
+        int64_t c = (x * P) / W;
+        while (c + 1 < P && begin(c + 1) <= x) ++c;
+        while (c > 0 && begin(c) > x) --c;
+        return c;
+    }
+    __host__ __device__ int64_t first_cta(int64_t slot) const { return owner(slot * T); }
+    __host__ __device__ int64_t nseg(int64_t slot) const
+    {
+        return owner(slot * T + T - 1) - first_cta(slot) + 1;
+    }
+};
+
+template <int B2, int KT, int STAGES>
+struct GramSmem {
+    static constexpr int LD = KT + 4;  // == 4 mod 16: conflict-free fragments
+    static constexpr int MAXSLOTS = 4;  // slots one CTA may touch
+    double x[STAGES][B2][LD];
+    const double *col[MAXSLOTS][B2];
+};
+
+// Per-warp DMMA roles over the upper-triangle 8x8 tiles of the B2 x B2
+// output (A is symmetric).  Roles are resolved by warp-uniform branches, so
+// no DMMA is ever issued predicated-off (a predicated-off DMMA still
+// occupies the tensor pipe).  B2 = 64: 16x16 super-tiles; warps 0-5 own one
+// off-diagonal super-tile (4 DMMA per k-step), warps 6-7 two diagonal
+// super-tiles (3 DMMA each): 8/8/10/10 DMMA per SM sub-partition.
+// B2 = 32: ten 8x8 tiles, warps 0-1 own two, warps 2-7 one.
+template <int B2>
+struct GramRoles;
+
+template <>
+struct GramRoles<64> {
+    static constexpr int NACC = 6;  // accumulator tiles per warp (max)
+    __device__ static void mma(int warp, const double (*X)[GramSmem<64, 32, 4>::LD], int kk,
+                               int fr, int fk, double (&acc)[NACC][2])
+    {
+        if (warp < 6) {
+            const int R = warp < 3 ? 0 : (warp < 5 ? 1 : 2);
+            const int C = warp < 3 ? warp + 1 : (warp < 5 ? warp - 1 : 3);
+            const double a0 = X[16 * R + fr][kk + fk], a1 = X[16 * R + 8 + fr][kk + fk];
+            const double b0 = X[16 * C + fr][kk + fk], b1 = X[16 * C + 8 + fr][kk + fk];
+            dmma(acc[0][0], acc[0][1], a0, b0);
+            dmma(acc[1][0], acc[1][1], a0, b1);
+            dmma(acc[2][0], acc[2][1], a1, b0);
+            dmma(acc[3][0], acc[3][1], a1, b1);
+        } else {
+            const int D0 = 2 * (warp - 6), D1 = D0 + 1;
+            const double f0 = X[16 * D0 + fr][kk + fk], f1 = X[16 * D0 + 8 + fr][kk + fk];
+            const double g0 = X[16 * D1 + fr][kk + fk], g1 = X[16 * D1 + 8 + fr][kk + fk];
+            dmma(acc[0][0], acc[0][1], f0, f0);
+            dmma(acc[1][0], acc[1][1], f0, f1);
+            dmma(acc[2][0], acc[2][1], f1, f1);
+            dmma(acc[3][0], acc[3][1], g0, g0);
+            dmma(acc[4][0], acc[4][1], g0, g1);
+            dmma(acc[5][0], acc[5][1], g1, g1);
+        }
+    }
+    // (row-tile, col-tile) of accumulator q of this warp; -1 if unused
+    __device__ static void tile(int warp, int q, int &rt, int &ct)
+    {
+        rt = ct = -1;
+        if (warp < 6) {
+            const int R = warp < 3 ? 0 : (warp < 5 ? 1 : 2);
+            const int C = warp < 3 ? warp + 1 : (warp < 5 ? warp - 1 : 3);
+            if (q < 4) { rt = 2 * R + (q >> 1); ct = 2 * C + (q & 1); }
+        } else {
+            const int D = 2 * (warp - 6) + (q >= 3 ? 1 : 0);
+            const int qq = q % 3;
+            rt = 2 * D + (qq == 2 ? 1 : 0);
+            ct = 2 * D + (qq == 0 ? 0 : 1);
+        }
+    }
+};
+
+template <>
+struct GramRoles<32> {
+    static constexpr int NACC = 2;
+    // upper 8x8 tiles of a 4x4 tile grid, in order
+    __device__ static void tile(int warp, int q, int &rt, int &ct)
+    {
+        const int t = q == 0 ? warp : (warp < 2 ? 8 + warp : -1);
+        rt = ct = -1;
+        if (t < 0) return;
+        // nibble t of the packed tables: R = 0,0,0,0,1,1,1,2,2,3  C = 0,1,2,3,1,2,3,2,3,3
+        rt = (int)((0x3221110000ull >> (4 * t)) & 0xF);
+        ct = (int)((0x3323213210ull >> (4 * t)) & 0xF);
+    }
+    __device__ static void mma(int warp, const double (*X)[GramSmem<32, 32, 4>::LD], int kk,
+                               int fr, int fk, double (&acc)[NACC][2])
+    {
+        int rt, ct;
+        tile(warp, 0, rt, ct);
+        dmma(acc[0][0], acc[0][1], X[8 * rt + fr][kk + fk], X[8 * ct + fr][kk + fk]);
+        if (warp < 2) {
+            tile(warp, 1, rt, ct);
+            dmma(acc[1][0], acc[1][1], X[8 * rt + fr][kk + fk], X[8 * ct + fr][kk + fk]);
+        }
+    }
+};
+
+template <int B2, int KT, int STAGES>
+__global__ void __launch_bounds__(kThreads, 3) k_gram(
+    const double *__restrict__ G, int64_t ldg, int n, const int64_t *__restrict__ rho,
+    const int64_t *__restrict__ iblk, const int64_t *__restrict__ jblk, GramPart part,
+    int maxseg, double *__restrict__ Apart, const unsigned long long *err)
+{
+    using Sm = GramSmem<B2, KT, STAGES>;
+    using Roles = GramRoles<B2>;
+    extern __shared__ __align__(16) unsigned char gsm_raw[];
+    auto &S = *reinterpret_cast<Sm *>(gsm_raw);
+    if (*(volatile const unsigned long long *)err != kNoError) return;
+    constexpr int b = B2 / 2;
+    const int64_t cta = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t it0 = part.begin(cta), it1 = part.begin(cta + 1);
+    if (it1 <= it0) return;
+    const int64_t slot0 = it0 / part.T;
+    const int nsl = (int)((it1 - 1) / part.T - slot0 + 1);  // <= MAXSLOTS (host-checked)
+    for (int q = tid; q < nsl * B2; q += kThreads) {
+        const int si = q / B2, c = q % B2;
+        const int64_t slot = slot0 + si;
+        int64_t I = iblk[slot], J = jblk[slot];
+        if (I > J) { int64_t t = I; I = J; J = t; }
+        S.col[si][c] = G + rho[slot_pos(c, b, I, J)] * ldg;
+    }
+    __syncthreads();
+
+    constexpr int CHUNKS = B2 * (KT / 2);
+    constexpr int PER_T = (CHUNKS + kThreads - 1) / kThreads;
+    auto load_stage = [&](int st, int64_t item) {
+        const int si = (int)(item / part.T - slot0);
+        const int k0 = (int)(item % part.T) * KT;
+#pragma unroll
+        for (int u = 0; u < PER_T; ++u) {
+            const int q = tid + u * kThreads;
+            if (q < CHUNKS) {
+                const int c = q / (KT / 2), pp = q % (KT / 2);
+                const int k = k0 + 2 * pp;
+                const int rem = n - k;
+                const int bytes = rem >= 2 ? 16 : (rem == 1 ? 8 : 0);
+                const double *src = bytes ? S.col[si][c] + k : S.col[si][c];
+                cp_async16(&S.x[st][c][2 * pp], src, bytes);
+            }
+        }
+    };
+
+    double acc[Roles::NACC][2];
+#pragma unroll
+    for (int q = 0; q < Roles::NACC; ++q) acc[q][0] = acc[q][1] = 0.0;
+    const int64_t nitems = it1 - it0;
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+        if (s < nitems) load_stage(s, it0 + s);
+        cp_async_commit();
+    }
+    const int fr = lane >> 2, fk = lane & 3;
+    for (int64_t i = 0; i < nitems; ++i) {
+        cp_async_wait<STAGES - 2>();
+        __syncthreads();
+        const int64_t nxt = i + STAGES - 1;
+        if (nxt < nitems) load_stage((int)(nxt % STAGES), it0 + nxt);
+        cp_async_commit();
+        const auto X = S.x[i % STAGES];
+#pragma unroll
+        for (int kk = 0; kk < KT; kk += 4) Roles::mma(warp, X, kk, fr, fk, acc);
+        const int64_t item = it0 + i;
+        if (i + 1 == nitems || (item + 1) % part.T == 0) {
+            // flush this slot segment's partial (upper tiles only)
+            const int64_t slot = item / part.T;
+            const int64_t seg = cta - part.first_cta(slot);
+            double *out = Apart + (slot * maxseg + seg) * (B2 * B2);
+#pragma unroll
+            for (int q = 0; q < Roles::NACC; ++q) {
+                int rt, ct;
+                Roles::tile(warp, q, rt, ct);
+                if (rt >= 0) {
+                    const int row = 8 * rt + fr, col = 8 * ct + 2 * fk;
+                    out[row * B2 + col] = acc[q][0];
+                    out[row * B2 + col + 1] = acc[q][1];
+                }
+                acc[q][0] = acc[q][1] = 0.0;
+            }
+        }
+    }
+    cp_async_wait<0>();
+}
+
+// ---------------------------------------------------------------------
+// k_inner: one pass of 2x2 rotations on the 2b x 2b pivot Gram
+// ---------------------------------------------------------------------
+struct InnerArgs {
+    GramPart part;
+    int maxseg;
+    const double *Apart;
+    double *Wg;
+    const int64_t *jsign;
+    int64_t *ip, *jp, *iblk, *jblk, *cur;
+    uint8_t *C;
+    uint32_t *rotk, *skipk;
+    uint8_t *wact;
+    double *maxt;
+    unsigned long long *err;
+    int64_t nb, slot_base;
+    double eps, teps;
+    int full, use_skip;
+};
+
+template <int B2>
+struct InnerSmem {
+    static constexpr int LD = B2 + 1;
+    double A[B2][LD];
+    double W[B2][LD];
+    // the round's rotations (written by warp 0, read after the barrier)
+    double pt[B2 / 2], pc[B2 / 2], ps[B2 / 2];
+    int pi[B2 / 2], pj[B2 / 2];
+    int js[B2];
+    unsigned int rot, skip, big;
+    unsigned long long maxt_bits;
+    unsigned long long fail;
+};
+
+// Plain-double annihilating rotation for block mode (the pointwise mode keeps
+// the reference's double-double rotation_tc, hsvd_rotation.cuh).  Same
+// branches, same sign convention and same definiteness test as rotation_tc
+// (_kernels.py:128-173): trig t = sgn(zeta)/(|zeta| + sqrt(1 + zeta^2)),
+// hyperbolic t = theta/(1 + sqrt(1 - theta^2)); 1 - x^2 by one fma.
+__device__ __forceinline__ int rotation_fast(double a_ii, double a_jj, double a_ij, int hyp,
+                                             double &t_out, double &c_out)
+{
+    t_out = 0.0;
+    c_out = 1.0;
+    if (a_ij == 0.0) return 0;
+    if (hyp < 0) {
+        const double zeta = (a_jj - a_ii) / (2.0 * a_ij);
+        if (fabs(zeta) > 6.7e7) {
+            t_out = 0.5 / zeta;
+            return 0;
+        }
+        const double az = fabs(zeta);
+        double t = 1.0 / (az + sqrt(fma(az, az, 1.0)));
+        if (!(zeta >= 0.0)) t = -t;
+        t_out = t;
+        c_out = rsqrt(fma(t, t, 1.0));
+        return 0;
+    }
+    const double th = (-2.0 * a_ij) / (a_ii + a_jj);
+    const double d = fma(-th, th, 1.0);
+    if (!(d > 0.0)) return 1;
+    const double t = th / (1.0 + sqrt(d));
+    const double u = fma(-t, t, 1.0);
+    if (!(u > 0.0)) return 1;
+    t_out = t;
+    c_out = rsqrt(u);
+    return 0;
+}
+
+// One pass of disjoint 2x2 rotations on the 2b x 2b pivot Gram A_P in shared
+// memory, accumulating W_P (A_P <- W^T A_P W, W J-orthogonal).
+//
+// A round's b pairs are disjoint, so the round is the congruence
+// A <- R^T A R with R block-diagonal in 2x2 blocks: every 2x2 block (p, q) of
+// A (rows {i_p, j_p}, columns {i_q, j_q}) becomes R_p^T A_pq R_q on its own.
+// Every warp computes all b rotations of the round redundantly (lane q owns
+// pair q; a warp-uniform decision skips inactive rounds without a barrier),
+// then updates its share of the blocks and of W from registers and shuffles:
+// two barriers per active round, none per inactive round.
+template <int B2, bool FAST>
+__global__ void __launch_bounds__(kThreads) k_inner(InnerArgs a)
+{
+    extern __shared__ __align__(16) unsigned char ism_raw[];
+    auto &S = *reinterpret_cast<InnerSmem<B2> *>(ism_raw);
+    if (*(volatile unsigned long long *)a.err != kNoError) return;
+    constexpr int b = B2 / 2;    // pairs per round
+    const int slot = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    int64_t I = a.iblk[slot], J = a.jblk[slot];
+    if (I > J) { int64_t t = I; I = J; J = t; }
+
+    // A = sum of the slot's partial segments in segment order (the upper
+    // triangle is read coalesced and mirrored); all loads of a batch of
+    // segments are issued before the sums
+    const double *P0 = a.Apart + (int64_t)slot * a.maxseg * (B2 * B2);
+    const int nseg = (int)a.part.nseg(slot);
+    constexpr int PER = B2 * B2 / kThreads;
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+        const int e = tid + k * kThreads, i = e / B2, j = e % B2;
+        S.W[i][j] = i == j ? 1.0 : 0.0;
+    }
+    {
+        double v[PER];
+#pragma unroll
+        for (int k = 0; k < PER; ++k) v[k] = 0.0;
+        constexpr int BATCH = 2;
+        for (int s0 = 0; s0 < nseg; s0 += BATCH) {
+            double x[BATCH][PER];
+#pragma unroll
+            for (int u = 0; u < BATCH; ++u)
+#pragma unroll
+                for (int k = 0; k < PER; ++k) {
+                    const int e = tid + k * kThreads;
+                    x[u][k] = (s0 + u < nseg && e / B2 <= e % B2)
+                                  ? P0[(int64_t)(s0 + u) * B2 * B2 + e] : 0.0;
+                }
+#pragma unroll
+            for (int u = 0; u < BATCH; ++u)
+#pragma unroll
+                for (int k = 0; k < PER; ++k)
+                    if (s0 + u < nseg) v[k] += x[u][k];
+        }
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int e = tid + k * kThreads, i = e / B2, j = e % B2;
+            if (i <= j) {
+                S.A[i][j] = v[k];
+                S.A[j][i] = v[k];
+            }
+        }
+    }
+    if (tid < B2) S.js[tid] = (int)a.jsign[slot_pos(tid, b, I, J)];
+    if (tid == 0) {
+        S.rot = S.skip = S.big = 0;
+        S.maxt_bits = 0;
+        S.fail = kNoError;
+    }
+    __syncthreads();
+
+    const int rounds = a.full ? B2 - 1 : b;
+    unsigned int my_rot = 0, my_skip = 0, my_big = 0;
+    double my_max = 0.0;
+    static_assert(b == 16 || b == 32, "k_inner: b must be 16 or 32");
+    constexpr int PSTRIDE = kThreads / b;   // row-pair stride of phase U
+    constexpr int NBK = b * b / kThreads;   // A blocks per thread per round
+    constexpr int NWR = B2 * b / kThreads;  // W rows per thread per round
+    const int q = lane % b;                 // pair owned by this thread
+    const int prow = tid / b;
+    for (int rd = 0; rd < rounds; ++rd) {
+        // ---- phase R: every warp forms all b rotations of the round
+        int i, j;
+        if (a.full) {  // circle method on B2 players
+            const int m = B2 - 1;
+            if (q == 0) { i = m; j = rd; }
+            else { i = (rd + q) % m; j = (rd - q + m) % m; }
+        } else {  // block-oriented: round rd pairs i with b + (i + rd) mod b
+            i = q;
+            j = b + (q + rd) % b;
+        }
+        if (i > j) { const int t = i; i = j; j = t; }
+        const double a_ii = S.A[i][i], a_jj = S.A[j][j], a_ij = S.A[i][j];
+        double t = 0.0, c = 1.0, st = 0.0;
+        int act = 0, bad = 0;
+        if (!(a_ij == 0.0 || (a.use_skip && fabs(a_ij) < a.eps * sqrt(a_ii * a_jj)))) {
+            const int hyp = S.js[i] == S.js[j] ? -1 : 1;
+            const int status = FAST ? rotation_fast(a_ii, a_jj, a_ij, hyp, t, c)
+                                    : rotation_tc(a_ii, a_jj, a_ij, hyp, t, c);
+            if (status != 0) {
+                bad = 1;
+                t = 0.0;
+                c = 1.0;
+            } else {
+                act = 1;
+                st = hyp < 0 ? -t : t;
+            }
+        }
+        if (warp == 0 && lane < b) {
+            S.pt[q] = t;
+            S.pc[q] = c;
+            S.ps[q] = st;
+            S.pi[q] = i;
+            S.pj[q] = j;
+            if (bad) atomicMin(&S.fail, pack_err(a.slot_base + slot, slot_pos(i, b, I, J),
+                                                 slot_pos(j, b, I, J)));
+            else if (act) {
+                ++my_rot;
+                const double at = fabs(t);
+                my_big |= at > a.teps;
+                my_max = fmax(my_max, at);
+            } else {
+                ++my_skip;
+            }
+        }
+        if (__any_sync(0xffffffffu, bad)) break;  // identical in every warp
+        if (!__any_sync(0xffffffffu, act)) continue;
+        __syncthreads();  // the round's inputs are read, its rotations published
+        // ---- phase U.  This thread owns pair q (its own registers) as the
+        // column pair of blocks (p, q), p = prow + k * PSTRIDE, and of the
+        // W rows prow + k * PSTRIDE.
+        {
+            double x[NBK][4], tp[NBK], cp[NBK], sp[NBK];
+            int ip[NBK], jp[NBK];
+#pragma unroll
+            for (int k = 0; k < NBK; ++k) {
+                const int p = prow + k * PSTRIDE;
+                tp[k] = S.pt[p];
+                cp[k] = S.pc[p];
+                sp[k] = S.ps[p];
+                ip[k] = S.pi[p];
+                jp[k] = S.pj[p];
+                x[k][0] = S.A[ip[k]][i];
+                x[k][1] = S.A[ip[k]][j];
+                x[k][2] = S.A[jp[k]][i];
+                x[k][3] = S.A[jp[k]][j];
+            }
+#pragma unroll
+            for (int k = 0; k < NBK; ++k) {
+                if (t == 0.0 && tp[k] == 0.0) continue;
+                // Y = X R_q (columns), X' = R_p^T Y (rows)
+                const double y00 = fma(st, x[k][1], x[k][0]) * c;
+                const double y01 = fma(t, x[k][0], x[k][1]) * c;
+                const double y10 = fma(st, x[k][3], x[k][2]) * c;
+                const double y11 = fma(t, x[k][2], x[k][3]) * c;
+                S.A[ip[k]][i] = fma(sp[k], y10, y00) * cp[k];
+                S.A[jp[k]][j] = fma(tp[k], y01, y11) * cp[k];
+                if (prow + k * PSTRIDE == q) {  // the pair itself: annihilated
+                    S.A[ip[k]][j] = 0.0;
+                    S.A[jp[k]][i] = 0.0;
+                } else {
+                    S.A[ip[k]][j] = fma(sp[k], y11, y01) * cp[k];
+                    S.A[jp[k]][i] = fma(tp[k], y00, y10) * cp[k];
+                }
+            }
+            if (t != 0.0) {  // W <- W R_q on this thread's rows
+                double wx[NWR], wy[NWR];
+#pragma unroll
+                for (int k = 0; k < NWR; ++k) {
+                    wx[k] = S.W[prow + k * PSTRIDE][i];
+                    wy[k] = S.W[prow + k * PSTRIDE][j];
+                }
+#pragma unroll
+                for (int k = 0; k < NWR; ++k) {
+                    S.W[prow + k * PSTRIDE][i] = fma(st, wy[k], wx[k]) * c;
+                    S.W[prow + k * PSTRIDE][j] = fma(t, wx[k], wy[k]) * c;
+                }
+            }
+        }
+        __syncthreads();  // the round's updates are visible
+    }
+    if (warp == 0) {
+        atomicAdd(&S.rot, my_rot);
+        atomicAdd(&S.skip, my_skip);
+        atomicOr(&S.big, my_big);
+        atomicMax(&S.maxt_bits, (unsigned long long)__double_as_longlong(my_max));
+    }
+    __syncthreads();
+    if (S.fail != kNoError) {
+        if (tid == 0) atomicMin(a.err, S.fail);
+        return;
+    }
+    // W column-major: Wg[slot][c * B2 + k] = W[k][c]
+    double *Wout = a.Wg + (int64_t)slot * B2 * B2;
+    for (int e = tid; e < B2 * B2; e += kThreads) Wout[e] = S.W[e % B2][e / B2];
+    if (tid == 0) {
+        // W == I exactly when nothing rotated: k_update skips the slot
+        a.wact[slot] = S.rot != 0;
+        // convergence code (_kernels.py:227-231 semantics per slot)
+        if (S.big) a.C[slot] = 3;
+        else if (S.rot) a.C[slot] |= 1;
+        a.rotk[slot] += S.rot;
+        a.skipk[slot] += S.skip;
+        const double mt = __longlong_as_double((long long)S.maxt_bits);
+        if (mt > a.maxt[slot]) a.maxt[slot] = mt;
+        a.cur[2 * slot] = I;
+        a.cur[2 * slot + 1] = J;
+        // advance_stepper (_kernels.py:238-251) on the block indices
+        const int64_t r = a.nb, half = r / 2;
+        int64_t ip = a.ip[slot], jp = a.jp[slot];
+        if (ip + jp >= r - 1) {
+            ip += 1;
+            if (ip == jp) {
+                ip -= half;
+                jp = ip;
+            }
+            a.ip[slot] = ip;
+            a.jp[slot] = jp;
+            a.iblk[slot] = ip;
+        } else {
+            jp += 1;
+            a.jp[slot] = jp;
+            a.jblk[slot] = jp;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------
+// k_update: [G_P; V_P] <- [G_P; V_P] W_P in place, FP64 tensor cores
+// ---------------------------------------------------------------------
+template <int B2, int MT>
+struct UpdSmem {
+    static constexpr int LDX = MT + 4;  // == 4 mod 16
+    static constexpr int LDW = B2 + 4;
+    double w[B2][LDW];  // w[c][k] = W[k][c]
+    double x[B2][LDX];  // x[k][row]
+    double *col[B2];
+};
+
+template <int B2, int MT>
+__global__ void __launch_bounds__(kThreads, 2) k_update(
+    double *__restrict__ G, int64_t ldg, int n, double *__restrict__ V, int64_t ldv, int rv,
+    const int64_t *__restrict__ rho, const int64_t *__restrict__ cur,
+    const double *__restrict__ Wg, const uint8_t *__restrict__ wact, int tiles_g,
+    const unsigned long long *err)
+{
+    extern __shared__ __align__(16) unsigned char usm_raw[];
+    auto &S = *reinterpret_cast<UpdSmem<B2, MT> *>(usm_raw);
+    if (*(volatile const unsigned long long *)err != kNoError) return;
+    constexpr int b = B2 / 2;
+    const int slot = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (!wact[slot]) return;  // no rotation in this slot: W == I
+    const bool isV = (int)blockIdx.x >= tiles_g;
+    const int tile = isV ? blockIdx.x - tiles_g : blockIdx.x;
+    const int nrows = isV ? rv : n;
+    const int64_t ld = isV ? ldv : ldg;
+    double *M = isV ? V : G;
+    const int row0 = tile * MT;
+    const int64_t I = cur[2 * slot], J = cur[2 * slot + 1];
+    if (tid < B2) S.col[tid] = M + rho[slot_pos(tid, b, I, J)] * ld;
+    // W (column-major in global) -> w[c][k]
+    const double *Wsrc = Wg + (int64_t)slot * B2 * B2;
+    for (int q = tid; q < B2 * B2 / 2; q += kThreads) {
+        const int c = (2 * q) / B2, k = (2 * q) % B2;
+        cp_async16(&S.w[c][k], Wsrc + 2 * q, 16);
+    }
+    __syncthreads();
+    // X tile in two commit groups (K halves) so the first half's DMMAs
+    // overlap the second half's loads
+    constexpr int CPC = MT / 2;  // 16-byte chunks per column
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        for (int q = tid; q < (B2 / 2) * CPC; q += kThreads) {
+            const int k = h * (B2 / 2) + q / CPC, part = q % CPC;
+            const int row = row0 + 2 * part;
+            const int rem = nrows - row;
+            const int bytes = rem >= 2 ? 16 : (rem == 1 ? 8 : 0);
+            cp_async16(&S.x[k][2 * part], bytes ? S.col[k] + row : S.col[k], bytes);
+        }
+        cp_async_commit();
+    }
+
+    constexpr int WM = MT / 4, WN = B2 / 2, MI = WM / 8, NI = WN / 8;
+    const int wm = warp >> 1, wn = warp & 1;
+    const int m0 = wm * WM, n0 = wn * WN;
+    const int fr = lane >> 2, fk = lane & 3;
+    double acc[MI][NI][2];
+#pragma unroll
+    for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int j = 0; j < NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        if (h == 0) cp_async_wait<1>();
+        else cp_async_wait<0>();
+        __syncthreads();
+#pragma unroll 4
+        for (int kk = h * (B2 / 2); kk < (h + 1) * (B2 / 2); kk += 4) {
+            double a[MI], bb[NI];
+#pragma unroll
+            for (int i = 0; i < MI; ++i) a[i] = S.x[kk + fk][m0 + 8 * i + fr];
+#pragma unroll
+            for (int j = 0; j < NI; ++j) bb[j] = S.w[n0 + 8 * j + fr][kk + fk];
+#pragma unroll
+            for (int i = 0; i < MI; ++i)
+#pragma unroll
+                for (int j = 0; j < NI; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], bb[j]);
+        }
+    }
+    __syncthreads();  // everyone done reading x
+#pragma unroll
+    for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int j = 0; j < NI; ++j) {
+            const int row = m0 + 8 * i + fr, col = n0 + 8 * j + 2 * fk;
+            S.x[col][row] = acc[i][j][0];
+            S.x[col + 1][row] = acc[i][j][1];
+        }
+    __syncthreads();
+    for (int q = tid; q < B2 * MT; q += kThreads) {
+        const int c = q / MT, rr = q % MT;
+        if (row0 + rr < nrows) S.col[c][row0 + rr] = S.x[c][rr];
+    }
+}
+
+// d[k] = ||G[:, rho[k]]||^2 for k < r; first_zero (may be NULL) = min rho of
+// a zero column (defined in hsvd_block.cu)
+int launch_block_norms(const double *G, int64_t ldg, int64_t n, const int64_t *rho, int64_t r,
+                       double *d, unsigned long long *first_zero, cudaStream_t s);
+
+// ---------------------------------------------------------------------
+// host-side helpers
+// ---------------------------------------------------------------------
+struct Carve2 {
+    char *base;
+    int64_t off;
+    template <typename T>
+    T *take(int64_t count)
+    {
+        off = (off + 255) & ~(int64_t)255;
+        T *p = (T *)(base + off);
+        off += count * (int64_t)sizeof(T);
+        return p;
+    }
+};
+
+inline int num_sms()
+{
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+            sms = 148;
+    }
+    return sms;
+}
+
+constexpr int kGramKT = 32, kGramStages = 4, kGramOcc = 3;
+
+// Static Gram partition: P = #SMs x resident CTAs, capped so that a CTA
+// spans at most GramSmem::MAXSLOTS slots and owns >= 1 k-tile.
+inline GramPart gram_partition(int64_t n, int64_t nslots)
+{
+    GramPart g;
+    g.T = (n + kGramKT - 1) / kGramKT;
+    g.W = nslots * g.T;
+    g.P = (int64_t)num_sms() * kGramOcc;
+    if (g.P > g.W) g.P = g.W;
+    // items per CTA >= T / 2 keeps a CTA within 4 slots: W/P <= 2T always
+    // holds for P >= nslots/2; raise P if the slots outnumber the CTAs
+    while (g.W / g.P + 2 > 4 * g.T && g.P < g.W) g.P *= 2;
+    if (g.P > g.W) g.P = g.W;
+    return g;
+}
+
+inline int gram_maxseg(const GramPart &g, int64_t nslots)
+{
+    int m = 1;
+    for (int64_t s = 0; s < nslots; ++s) {
+        const int k = (int)g.nseg(s);
+        if (k > m) m = k;
+    }
+    return m;
+}
+
+// Per-slot state of one step's kernels: the whole problem on one GPU, or
+// one shard's slots when sharded.  colmap maps a column POSITION to its
+// column in the G/V storage (rho on one GPU; the shard's area map when
+// sharded); js maps a position to its J sign.
+struct SlotWs {
+    const int64_t *colmap, *js;
+    int64_t *ip, *jp, *iblk, *jblk, *cur;
+    uint8_t *C, *wact;
+    uint32_t *rotk, *skipk;
+    double *maxt;
+    unsigned long long *err;
+    double *Apart, *Wg;
+    int64_t nslots, nb, slot_base;
+    GramPart gp;
+    int maxseg;
+};
+
+// Carve the per-slot arrays for nslots slots of a problem with nb blocks.
+inline void carve_slots(Carve2 &c, int64_t n, int64_t nslots, int64_t nb, int b, SlotWs *w)
+{
+    const int64_t B2 = 2 * b;
+    const GramPart gp = gram_partition(n, nslots);
+    const int ks = gram_maxseg(gp, nslots);
+    SlotWs t;
+    t.colmap = t.js = nullptr;
+    t.ip = c.take<int64_t>(nslots);
+    t.jp = c.take<int64_t>(nslots);
+    t.iblk = c.take<int64_t>(nslots);
+    t.jblk = c.take<int64_t>(nslots);
+    t.cur = c.take<int64_t>(2 * nslots);
+    t.C = c.take<uint8_t>(nslots);
+    t.wact = c.take<uint8_t>(nslots);
+    t.rotk = c.take<uint32_t>(nslots);
+    t.skipk = c.take<uint32_t>(nslots);
+    t.maxt = c.take<double>(nslots);
+    t.err = c.take<unsigned long long>(1);
+    t.Apart = c.take<double>(nslots * ks * B2 * B2);
+    t.Wg = c.take<double>(nslots * B2 * B2);
+    t.nslots = nslots;
+    t.nb = nb;
+    t.slot_base = 0;
+    t.gp = gp;
+    t.maxseg = ks;
+    if (w) *w = t;
+}
+
+template <int B2>
+struct BlockKernels {
+    static constexpr int KT = kGramKT, STAGES = kGramStages, MT = 128;
+    static size_t gram_smem() { return sizeof(GramSmem<B2, KT, STAGES>); }
+    static size_t inner_smem() { return sizeof(InnerSmem<B2>); }
+    static size_t upd_smem() { return sizeof(UpdSmem<B2, MT>); }
+    static int setup()
+    {
+        HSVD_CUDA(cudaFuncSetAttribute(k_gram<B2, KT, STAGES>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)gram_smem()));
+        HSVD_CUDA(cudaFuncSetAttribute(k_inner<B2, true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)inner_smem()));
+        HSVD_CUDA(cudaFuncSetAttribute(k_inner<B2, false>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)inner_smem()));
+        HSVD_CUDA(cudaFuncSetAttribute(k_update<B2, MT>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)upd_smem()));
+        return HSVD_OK;
+    }
+    // one step: Gram -> inner pass -> update
+    static int step(double *G, int64_t ldg, int n, double *V, int64_t ldv, int rv,
+                    const SlotWs &w, int full, const hsvd_config *cfg, cudaStream_t s,
+                    KernelTimer &T)
+    {
+        const int64_t nslots = w.nslots;
+        const GramPart &gp = w.gp;
+        T.begin(0, s);
+        k_gram<B2, KT, STAGES><<<(unsigned)gp.P, kThreads, gram_smem(), s>>>(
+            G, ldg, n, w.colmap, w.iblk, w.jblk, gp, w.maxseg, w.Apart, w.err);
+        T.end(s);
+        HSVD_LAUNCH_CHECK("k_gram");
+        InnerArgs ia;
+        ia.part = gp; ia.maxseg = w.maxseg;
+        ia.Apart = w.Apart; ia.Wg = w.Wg; ia.jsign = w.js;
+        ia.ip = w.ip; ia.jp = w.jp; ia.iblk = w.iblk; ia.jblk = w.jblk; ia.cur = w.cur;
+        ia.C = w.C; ia.wact = w.wact; ia.rotk = w.rotk; ia.skipk = w.skipk; ia.maxt = w.maxt; ia.err = w.err;
+        ia.nb = w.nb; ia.slot_base = w.slot_base; ia.eps = cfg->eps; ia.teps = cfg->teps;
+        ia.full = full; ia.use_skip = cfg->use_skip;
+        T.begin(1, s);
+        if (cfg->block_rotation == HSVD_ROTATION_FAST)
+            k_inner<B2, true><<<(unsigned)nslots, kThreads, inner_smem(), s>>>(ia);
+        else
+            k_inner<B2, false><<<(unsigned)nslots, kThreads, inner_smem(), s>>>(ia);
+        T.end(s);
+        HSVD_LAUNCH_CHECK("k_inner");
+        const int tiles_g = (n + MT - 1) / MT;
+        const int tiles_v = V ? (rv + MT - 1) / MT : 0;
+        T.begin(2, s);
+        k_update<B2, MT><<<dim3(tiles_g + tiles_v, (unsigned)nslots), kThreads, upd_smem(), s>>>(
+            G, ldg, n, V, ldv, rv, w.colmap, w.cur, w.Wg, w.wact, tiles_g, w.err);
+        T.end(s);
+        HSVD_LAUNCH_CHECK("k_update");
+        return HSVD_OK;
+    }
+};
+
+
+}  // namespace hsvd
