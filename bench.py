@@ -17,8 +17,10 @@ restatement in oracle/ (bit-exact with hjsvd, see tests/golden) with every
 host thread, on a bounded sample of the same workload, extrapolated to a
 full solve with the exact per-sweep rotation/skip counts (oracle/README).
 
-One process per GPU (torchrun); N>1 currently runs independent replicas
-(each rank solves its own copy) and reports the max over ranks.
+One process per GPU (torchrun).  N>1 shards the block-column slots of one
+solve over the N GPUs (paper_1008_1371_b200.sharded, NCCL ring exchange of
+one block column per step); the time is the max over ranks and the scaling
+is strong (the n=8192 problem is fixed).
 """
 
 import argparse
@@ -54,6 +56,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-accuracy", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the sharded (NCCL) solver even on 1 GPU (checks that path)")
     a = ap.parse_args()
     if a.p is None:
         a.p = a.n // 2
@@ -268,17 +272,30 @@ def run_ours(a, rank, world, local_rank):
                          block_rotation=a.block_rotation)
     if a.mode == "block" and a.n % (2 * a.block_cols):
         raise SystemExit("block mode needs n to be a multiple of 2*block_cols")
+    sharded = world > 1 or a.sharded
+    if sharded and a.mode != "block":
+        raise SystemExit("--gpus N > 1 shards block mode only")
     G0 = torch.from_numpy(np.ascontiguousarray(G.T)).to(dev)  # (r, n) = col-major G
     Gw = torch.empty_like(G0)
     stream = torch.cuda.current_stream()
+    comm = H.ShardComm() if sharded else None
 
-    def solve():
+    def solve(c=cfg):
+        if sharded:  # every rank holds the full factor, solves its shard
+            return H.drive_sharded_device(G0, J, c, comm)
         Gw.copy_(G0)
-        return H.drive_device(Gw, J, cfg)
+        return H.drive_device(Gw, J, c)
 
     def barrier():
         if world > 1:
             dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
 
     res = None
     for _ in range(a.warmup):
@@ -303,11 +320,7 @@ def run_ours(a, rank, world, local_rank):
     barrier()
     torch.cuda.synchronize()
     clocks = clk.stop()
-    ms = ev0.elapsed_time(ev1)
-    if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(ev0.elapsed_time(ev1))
     ms_per_step = ms / a.steps
     value = ms_per_step / 1e3
 
@@ -316,9 +329,9 @@ def run_ours(a, rank, world, local_rank):
     # every launch on the library's launching stream (outside the timed run).
     n = r = a.n
     tele = res.telemetry
-    prof = H.drive_device(Gw.copy_(G0), J, H.SolverConfig(
-        mode=a.mode, block_cols=a.block_cols, block_rotation=a.block_rotation,
-        max_sweeps=1, profile=True))
+    pcfg = H.SolverConfig(mode=a.mode, block_cols=a.block_cols,
+                          block_rotation=a.block_rotation, max_sweeps=1, profile=True)
+    prof = solve(pcfg)
     kp = prof.kernel_profile
     peaks = {}
     if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")):
@@ -344,7 +357,7 @@ def run_ours(a, rank, world, local_rank):
             save_reference_telemetry(a.n, a.p, tele)
     else:
         b2 = 2 * a.block_cols
-        nslots = n // b2
+        nslots = n // b2 // world  # slots per launch on this rank
         fl = {"gram": 2.0 * n * b2 * b2 * nslots,          # A_P = G_P^T G_P per slot
               "update": 2.0 * (n + r) * b2 * b2 * nslots}  # [G_P; V_P] W_P per slot
         dom = max(("gram", "update"), key=lambda k: kp[k]["ms"])
@@ -357,8 +370,11 @@ def run_ours(a, rank, world, local_rank):
         achieved = fl[dom] / avg_s / 1e12
         tot_ms = sum(v["ms"] for v in kp.values())
         solve_tflops = res.sweeps_used * 12.0 * n ** 3 / value / 1e12
+        tr = traffic.get(f"{dom}_n{n}_b{a.block_cols}_N{world}",
+                         traffic.get(f"{dom}_n{n}_b{a.block_cols}") if world == 1 else None)
         roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                    "frac": achieved / peak, "traffic": traffic.get(f"{dom}_n{n}_b{a.block_cols}"),
+                    "frac": achieved / peak,
+                    "traffic": tr["bytes_per_launch"] if isinstance(tr, dict) else tr,
                     "kernel": f"k_{dom}", "launch_avg_ms": avg_s * 1e3,
                     "alg_flop_per_launch": fl[dom],
                     "peak_source": ("cuBLAS DGEMM 8192^3 measured on this pool "
@@ -369,33 +385,54 @@ def run_ours(a, rank, world, local_rank):
                     "gram_tflops": fl["gram"] / (kp["gram"]["ms"] / kp["gram"]["launches"] / 1e3) / 1e12,
                     "update_tflops": fl["update"] / (kp["update"]["ms"] / kp["update"]["launches"] / 1e3) / 1e12,
                     "solve_alg_tflops": solve_tflops,
-                    "solve_frac": solve_tflops / peak}
+                    "solve_frac": solve_tflops / (peak * world),
+                    "solve_frac_note": "12 n^3 flop per sweep x sweeps / time / (N x peak)"}
+        if isinstance(tr, dict):
+            roofline["traffic_source"] = tr.get("source")
 
-    # ---- end to end through the public numpy API -------------------------
+    # ---- end to end through the public API, host buffers -------------------
+    # 1 GPU: drive(G_numpy, J) (H2D of G, D2H of U, V^-T, sigma, lam inside).
+    # N GPUs: every rank copies the factor in from pinned host memory, solves
+    # its shard, and copies its own columns of U, V^-T, sigma, lam out.
+    Gpin = torch.from_numpy(np.ascontiguousarray(G.T)).pin_memory() if sharded else None
     e2e_ms = []
+    d2h = 0
     for _ in range(max(a.e2e_steps, 1)):
         torch.cuda.synchronize()
+        barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         t0 = time.perf_counter()
         e0.record(stream)
-        out = H.drive(G, J, cfg)
+        if sharded:
+            Gd = Gpin.to(dev, non_blocking=True)
+            part = H.drive_sharded_device(Gd, J, cfg, comm)
+            outs = [part.U_t.cpu(), part.Vinv_t_t.cpu(), part.sigma.cpu(), part.lam.cpu()]
+            d2h = sum(t.numel() * 8 for t in outs)  # this rank's columns
+        else:
+            H.drive(G, J, cfg)
+            d2h = (n * r + r * r + 2 * r) * 8
         e1.record(stream)
         torch.cuda.synchronize()
         wall = (time.perf_counter() - t0) * 1e3
         e2e_ms.append(max(e0.elapsed_time(e1), wall))
-    e2e_s = float(np.mean(e2e_ms)) / 1e3
-    if world > 1:
-        t = torch.tensor([e2e_s], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
-    h2d = n * r * 8 + r
-    d2h = (n * r + r * r + 2 * r) * 8
+    e2e_s = max_over_ranks(float(np.mean(e2e_ms)) / 1e3)
+    h2d = world * (n * r * 8 + r)  # every rank copies the whole factor in
+    if world > 1:  # all ranks' outputs together
+        t = torch.tensor([float(d2h)], device=dev)
+        dist.all_reduce(t)
+        d2h = int(t.item())
 
     acc = None
     if not a.no_accuracy:
-        res = solve()
-        acc = residuals(G0, res, signs)
+        if sharded:
+            full = H.gather_result(solve(), n, r, to_numpy=False)
+            full.U = full.U.t()  # back to the (r, n) convention of residuals()
+            full.Vinv_t = full.Vinv_t.t()
+            acc = residuals(G0, full, signs)
+        else:
+            res = solve()
+            acc = residuals(G0, res, signs)
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:
@@ -404,23 +441,26 @@ def run_ours(a, rank, world, local_rank):
                                              cpu_threads(), tel)
         cpu = {"value": est, "unit": "s", "cores": cpu_threads(), "kind": "port",
                "sample": sample}
+    if comm is not None:
+        comm.close()
 
     if rank == 0:
         line = {
             "metric": METRIC.format(n=a.n), "value": value, "unit": "s",
             "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
             "ms_per_step": ms_per_step, "higher_is_better": False,
-            "scaling": "weak" if world > 1 else "strong",
+            "scaling": "strong",
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic: numpy default_rng(0).standard_normal((n,n)), J=diag(+1 x p, -1 x n-p)",
             "config": {"workload": f"n={a.n} p={a.p} full HSVD with V^-T (SURVEY.md §8(d) cfg 5)",
                        "n": a.n, "p": a.p, "mode": a.mode,
                        **({"block_cols": a.block_cols, "block_rotation": a.block_rotation}
                           if a.mode == "block" else {}),
-                       "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                       "parallelism": (f"{world} GPUs: block-column slots sharded, NCCL ring "
+                                       "exchange per step" if sharded else "1 GPU"),
                        "l2": "inputs larger than L2 (G and V^-T are n*n*8 B each)"},
-            "sweeps": res.sweeps_used, "stop_reason": res.stop_reason,
-            "rotations": res.rotations, "skips": res.skips,
+            "sweeps": res_timed.sweeps_used, "stop_reason": res_timed.stop_reason,
+            "rotations": res_timed.rotations, "skips": res_timed.skips,
             "accuracy": acc,
             "roofline": roofline,
             "cpu_baseline": cpu,
@@ -442,15 +482,19 @@ def main():
     if a.impl == "reference":
         run_reference(a, rank, world)
         return
-    if world > 1:
+    dist_on = world > 1 or a.sharded
+    if dist_on:
         import torch
         import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29531")
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        dist.init_process_group("nccl", rank=rank, world_size=world,
+                                device_id=torch.device("cuda", local_rank))
     try:
         run_ours(a, rank, world, local_rank)
     finally:
-        if world > 1:
+        if dist_on:
             import torch.distributed as dist
             dist.destroy_process_group()
 

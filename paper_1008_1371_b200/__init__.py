@@ -56,6 +56,7 @@ from .sharded import (
     ShardedResult,
     drive_local_shards,
     drive_sharded,
+    drive_sharded_device,
     gather_result,
 )
 from .strategies import (

@@ -885,7 +885,8 @@ struct ShardedDriver {
         }
         HSVD_CUDA_OK(sync_all());
 
-        KernelTimer T;
+        // profile mode: CUDA events around shard 0's kernels of sweep 0
+        KernelTimer T, Toff;
         std::vector<Move> mv;
         int64_t sweeps_used = 0, total_rot = 0, total_skip = 0;
         int stop = 2;
@@ -894,12 +895,13 @@ struct ShardedDriver {
         for (int64_t sweep = 0; sweep < cfg->max_sweeps; ++sweep) {
             HSVD_CUDA(cudaSetDevice(x0.dev));
             HSVD_CUDA(cudaEventRecord(x0.t0, x0.s));
+            T.on = cfg->profile && sweep == 0;
             for (int64_t step = 0; step < nb; ++step) {
                 const int full = cfg->inner_full || step == 0;
                 for (auto &x : sh) {
                     HSVD_CUDA(cudaSetDevice(x.dev));
                     HSVD_CUDA_OK(K::step(x.w.Gs, n, (int)n, withV ? x.w.Vs : nullptr, r, (int)r,
-                                         x.w.sl, full, cfg, x.s, T));
+                                         x.w.sl, full, cfg, x.s, &x == &sh[0] ? T : Toff));
                     launches += 3;
                 }
                 HSVD_CUDA_OK(pl.advance(mv));
@@ -920,6 +922,7 @@ struct ShardedDriver {
                                       cudaMemcpyDeviceToHost, x0.s));
             HSVD_CUDA(cudaEventRecord(x0.t1, x0.s));
             HSVD_CUDA_OK(sync_all());
+            if (T.on) T.collect(res);
             float ms = 0.f;
             HSVD_CUDA(cudaEventElapsedTime(&ms, x0.t0, x0.t1));
             int64_t o[5];

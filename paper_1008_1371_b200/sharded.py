@@ -53,6 +53,9 @@ class ShardedResult:
     sweep_gpu_ms: list = field(default_factory=list)
     gpu_launches: int = 0
     host_phase_ms: dict = field(default_factory=dict)
+    #: profile mode: device ms / launches per kernel class of sweep 0 on the
+    #: first local shard (gram, inner, update)
+    kernel_profile: dict = field(default_factory=dict)
 
 
 class ShardComm:
@@ -157,7 +160,11 @@ def _run(comm, nshards, shard_ids, devices, Gts, n, r, J, cfg):
                   sweep_gpu_ms=[float(tele[s].gpu_ms) for s in range(res.sweeps_used)],
                   gpu_launches=int(res.launches),
                   host_phase_ms={"setup": float(res.setup_ms), "sweeps": float(res.sweeps_ms),
-                                 "finish": float(res.finish_ms)})
+                                 "finish": float(res.finish_ms)},
+                  kernel_profile=({nm: {"ms": float(res.kernel_ms[k]),
+                                        "launches": int(res.kernel_launches[k])}
+                                   for k, nm in enumerate(("gram", "inner", "update"))
+                                   if res.kernel_launches[k]} if cfg.profile else {}))
     return [ShardedResult(shard=g, nshards=nshards, cols=o["cols"], sigma=o["sigma"],
                           lam=o["lam"], U_t=o["U"], Vinv_t_t=o["V"], **common)
             for g, o in zip(shard_ids, outs)]
@@ -167,17 +174,31 @@ def drive_sharded(G, J, cfg=None, comm=None):
     """This rank's shard of a block-mode HSVD over ``comm.world`` GPUs.
 
     Every rank passes the same full factor G (numpy n x r, or a CUDA tensor)
-    and returns a ShardedResult with the columns it holds at the end."""
+    and returns a ShardedResult with the columns it holds at the end.  The
+    call is synchronous (it returns when the solve has finished)."""
     if comm is None:
         raise ValueError("drive_sharded needs a ShardComm (use drive_local_shards "
                          "for one process)")
     n, r = (G.shape[0], G.shape[1])
+    dev = _device.require_cuda()
+    return drive_sharded_device(_factor_on(G, dev), J, cfg, comm)
+
+
+def drive_sharded_device(Gt, J, cfg=None, comm=None):
+    """drive_sharded on a factor already in HBM: Gt is the (r, n)
+    C-contiguous float64 CUDA tensor of the column-major n x r factor (read
+    only -- the shard gathers its columns into its own storage)."""
+    if comm is None:
+        raise ValueError("drive_sharded_device needs a ShardComm")
+    if Gt.dtype != torch.float64 or not Gt.is_cuda or not Gt.is_contiguous():
+        raise ValueError("Gt must be a contiguous float64 CUDA tensor (r, n)")
+    r, n = Gt.shape
     if len(J) != r:
         raise ShapeError("signature length must match the column count")
+    if n < r:
+        raise ShapeError("G must have n >= r")
     cfg = _check_cfg(cfg, r)
-    dev = _device.require_cuda()
-    Gt = _factor_on(G, dev)
-    return _run(comm, comm.world, [comm.rank], [dev.index], [Gt], n, r, J, cfg)[0]
+    return _run(comm, comm.world, [comm.rank], [Gt.device.index], [Gt], n, r, J, cfg)[0]
 
 
 def assemble(parts, n, r, to_numpy=True):
