@@ -257,13 +257,19 @@ struct InnerArgs {
     int64_t *ip, *jp, *iblk, *jblk, *cur;
     uint8_t *C;
     uint32_t *rotk, *skipk;
-    uint8_t *wact;
+    uint8_t *tset;  // per slot: [count, touched columns...], kTsetStride bytes
     double *maxt;
     unsigned long long *err;
     int64_t nb, slot_base;
     double eps, teps;
     int full, use_skip;
 };
+
+// Touched-column set of a slot visit: the columns of P that took part in at
+// least one rotation.  W_P is the identity outside T x T, so the update only
+// has to rewrite the columns in T.
+constexpr int kTsetStride = 72;   // count byte + up to 64 column indices
+constexpr int kSparseMax = 24;    // |T| <= this: column update without DMMA
 
 template <int B2>
 struct InnerSmem {
@@ -277,6 +283,7 @@ struct InnerSmem {
     unsigned int rot, skip, big;
     unsigned long long maxt_bits;
     unsigned long long fail;
+    unsigned long long touched;
 };
 
 // Plain-double annihilating rotation for block mode (the pointwise mode keeps
@@ -381,11 +388,13 @@ __global__ void __launch_bounds__(kThreads) k_inner(InnerArgs a)
         S.rot = S.skip = S.big = 0;
         S.maxt_bits = 0;
         S.fail = kNoError;
+        S.touched = 0;
     }
     __syncthreads();
 
     const int rounds = a.full ? B2 - 1 : b;
     unsigned int my_rot = 0, my_skip = 0, my_big = 0;
+    unsigned long long my_touch = 0;
     double my_max = 0.0;
     static_assert(b == 16 || b == 32, "k_inner: b must be 16 or 32");
     constexpr int PSTRIDE = kThreads / b;   // row-pair stride of phase U
@@ -431,6 +440,7 @@ __global__ void __launch_bounds__(kThreads) k_inner(InnerArgs a)
                                                  slot_pos(j, b, I, J)));
             else if (act) {
                 ++my_rot;
+                my_touch |= (1ull << i) | (1ull << j);
                 const double at = fabs(t);
                 my_big |= at > a.teps;
                 my_max = fmax(my_max, at);
@@ -499,6 +509,7 @@ __global__ void __launch_bounds__(kThreads) k_inner(InnerArgs a)
         atomicAdd(&S.skip, my_skip);
         atomicOr(&S.big, my_big);
         atomicMax(&S.maxt_bits, (unsigned long long)__double_as_longlong(my_max));
+        atomicOr(&S.touched, my_touch);
     }
     __syncthreads();
     if (S.fail != kNoError) {
@@ -509,8 +520,16 @@ __global__ void __launch_bounds__(kThreads) k_inner(InnerArgs a)
     double *Wout = a.Wg + (int64_t)slot * B2 * B2;
     for (int e = tid; e < B2 * B2; e += kThreads) Wout[e] = S.W[e % B2][e / B2];
     if (tid == 0) {
-        // W == I exactly when nothing rotated: k_update skips the slot
-        a.wact[slot] = S.rot != 0;
+        // touched columns (W == I outside T x T; T empty: k_update skips)
+        uint8_t *ts = a.tset + (int64_t)slot * kTsetStride;
+        unsigned long long m = S.touched;
+        int cnt = 0;
+        while (m) {
+            const int c = __ffsll((long long)m) - 1;
+            m &= m - 1;
+            ts[1 + cnt++] = (uint8_t)c;
+        }
+        ts[0] = (uint8_t)cnt;
         // convergence code (_kernels.py:227-231 semantics per slot)
         if (S.big) a.C[slot] = 3;
         else if (S.rot) a.C[slot] |= 1;
@@ -556,7 +575,7 @@ template <int B2, int MT>
 __global__ void __launch_bounds__(kThreads, 2) k_update(
     double *__restrict__ G, int64_t ldg, int n, double *__restrict__ V, int64_t ldv, int rv,
     const int64_t *__restrict__ rho, const int64_t *__restrict__ cur,
-    const double *__restrict__ Wg, const uint8_t *__restrict__ wact, int tiles_g,
+    const double *__restrict__ Wg, const uint8_t *__restrict__ tset, int tiles_g,
     const unsigned long long *err)
 {
     extern __shared__ __align__(16) unsigned char usm_raw[];
@@ -564,7 +583,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_update(
     if (*(volatile const unsigned long long *)err != kNoError) return;
     constexpr int b = B2 / 2;
     const int slot = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (!wact[slot]) return;  // no rotation in this slot: W == I
+    const uint8_t *ts = tset + (int64_t)slot * kTsetStride;
+    const int nt = ts[0];
+    if (nt == 0) return;  // no rotation in this slot: W == I
     const bool isV = (int)blockIdx.x >= tiles_g;
     const int tile = isV ? blockIdx.x - tiles_g : blockIdx.x;
     const int nrows = isV ? rv : n;
@@ -572,6 +593,30 @@ __global__ void __launch_bounds__(kThreads, 2) k_update(
     double *M = isV ? V : G;
     const int row0 = tile * MT;
     const int64_t I = cur[2 * slot], J = cur[2 * slot + 1];
+    if (nt <= kSparseMax) {
+        // few touched columns: out[:, T] = X[:, T] W[T, T] on the FMA pipe,
+        // reading and writing only the |T| columns of this row tile
+        if (tid < nt) S.col[tid] = M + rho[slot_pos(ts[1 + tid], b, I, J)] * ld;
+        const double *Wsl = Wg + (int64_t)slot * B2 * B2;
+        for (int e = tid; e < nt * nt; e += kThreads) {
+            const int c = e / nt, k = e % nt;
+            S.w[c][k] = Wsl[ts[1 + c] * B2 + ts[1 + k]];  // W[T_k][T_c]
+        }
+        __syncthreads();
+        for (int e = tid; e < nt * MT; e += kThreads) {
+            const int k = e / MT, rr = e % MT;
+            S.x[k][rr] = row0 + rr < nrows ? S.col[k][row0 + rr] : 0.0;
+        }
+        __syncthreads();
+        for (int e = tid; e < nt * MT; e += kThreads) {
+            const int c = e / MT, rr = e % MT;
+            if (row0 + rr >= nrows) continue;
+            double acc = 0.0;
+            for (int k = 0; k < nt; ++k) acc = fma(S.x[k][rr], S.w[c][k], acc);
+            S.col[c][row0 + rr] = acc;
+        }
+        return;
+    }
     if (tid < B2) S.col[tid] = M + rho[slot_pos(tid, b, I, J)] * ld;
     // W (column-major in global) -> w[c][k]
     const double *Wsrc = Wg + (int64_t)slot * B2 * B2;
@@ -706,7 +751,7 @@ inline int gram_maxseg(const GramPart &g, int64_t nslots)
 struct SlotWs {
     const int64_t *colmap, *js;
     int64_t *ip, *jp, *iblk, *jblk, *cur;
-    uint8_t *C, *wact;
+    uint8_t *C, *tset;
     uint32_t *rotk, *skipk;
     double *maxt;
     unsigned long long *err;
@@ -730,7 +775,7 @@ inline void carve_slots(Carve2 &c, int64_t n, int64_t nslots, int64_t nb, int b,
     t.jblk = c.take<int64_t>(nslots);
     t.cur = c.take<int64_t>(2 * nslots);
     t.C = c.take<uint8_t>(nslots);
-    t.wact = c.take<uint8_t>(nslots);
+    t.tset = c.take<uint8_t>(nslots * kTsetStride);
     t.rotk = c.take<uint32_t>(nslots);
     t.skipk = c.take<uint32_t>(nslots);
     t.maxt = c.take<double>(nslots);
@@ -783,7 +828,7 @@ struct BlockKernels {
         ia.part = gp; ia.maxseg = w.maxseg;
         ia.Apart = w.Apart; ia.Wg = w.Wg; ia.jsign = w.js;
         ia.ip = w.ip; ia.jp = w.jp; ia.iblk = w.iblk; ia.jblk = w.jblk; ia.cur = w.cur;
-        ia.C = w.C; ia.wact = w.wact; ia.rotk = w.rotk; ia.skipk = w.skipk; ia.maxt = w.maxt; ia.err = w.err;
+        ia.C = w.C; ia.tset = w.tset; ia.rotk = w.rotk; ia.skipk = w.skipk; ia.maxt = w.maxt; ia.err = w.err;
         ia.nb = w.nb; ia.slot_base = w.slot_base; ia.eps = cfg->eps; ia.teps = cfg->teps;
         ia.full = full; ia.use_skip = cfg->use_skip;
         T.begin(1, s);
@@ -797,7 +842,7 @@ struct BlockKernels {
         const int tiles_v = V ? (rv + MT - 1) / MT : 0;
         T.begin(2, s);
         k_update<B2, MT><<<dim3(tiles_g + tiles_v, (unsigned)nslots), kThreads, upd_smem(), s>>>(
-            G, ldg, n, V, ldv, rv, w.colmap, w.cur, w.Wg, w.wact, tiles_g, w.err);
+            G, ldg, n, V, ldv, rv, w.colmap, w.cur, w.Wg, w.tset, tiles_g, w.err);
         T.end(s);
         HSVD_LAUNCH_CHECK("k_update");
         return HSVD_OK;
