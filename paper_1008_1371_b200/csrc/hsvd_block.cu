@@ -128,8 +128,9 @@ template <int B2>
 static int block_drive_t(double *G, int64_t n, int64_t r, int64_t ldg, double *V, int64_t ldv,
                          const int8_t *signs_host, int64_t p, const hsvd_config *cfg,
                          double *sigma, double *lam, void *ws, int64_t ws_bytes,
-                         hsvd_result *res, hsvd_telemetry *tele, cudaStream_t s)
+                         hsvd_result *res, hsvd_telemetry *tele, DevCtx &ctx)
 {
+    cudaStream_t s = ctx.s;
     using K = BlockKernels<B2>;
     constexpr int b = B2 / 2;
     const int64_t nb = r / b, nslots = nb / 2;
@@ -142,24 +143,19 @@ static int block_drive_t(double *G, int64_t n, int64_t r, int64_t ldg, double *V
     int st = K::setup();
     if (st) return st;
 
-    int64_t *host = nullptr;
-    cudaEvent_t t0 = nullptr, t1 = nullptr;
+    int64_t *host = ctx.host;
+    cudaEvent_t t0 = ctx.t0, t1 = ctx.t1;
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     struct Cleanup {
-        int64_t *&h; cudaEvent_t &a, &b; cudaGraph_t &g; cudaGraphExec_t &e;
+        cudaGraph_t &g;
+        cudaGraphExec_t &e;
         ~Cleanup()
         {
             if (e) cudaGraphExecDestroy(e);
             if (g) cudaGraphDestroy(g);
-            if (a) cudaEventDestroy(a);
-            if (b) cudaEventDestroy(b);
-            if (h) cudaFreeHost(h);
         }
-    } cleanup{host, t0, t1, graph, exec};
-    HSVD_CUDA(cudaHostAlloc((void **)&host, 16 * sizeof(int64_t), cudaHostAllocDefault));
-    HSVD_CUDA(cudaEventCreate(&t0));
-    HSVD_CUDA(cudaEventCreate(&t1));
+    } cleanup{graph, exec};
 
     if (V) {
         st = launch_identity(V, r, ldv, s);
@@ -279,7 +275,7 @@ static int block_drive_t(double *G, int64_t n, int64_t r, int64_t ldg, double *V
 int block_drive(double *G, int64_t n, int64_t r, int64_t ldg, double *V, int64_t ldv,
                 const int8_t *signs_host, int64_t p, const hsvd_config *cfg, double *sigma,
                 double *lam, void *ws, int64_t ws_bytes, hsvd_result *res,
-                hsvd_telemetry *tele, cudaStream_t s)
+                hsvd_telemetry *tele, DevCtx &ctx)
 {
     const int b = cfg->block_cols;
     if (b != 16 && b != 32) {
@@ -296,9 +292,9 @@ int block_drive(double *G, int64_t n, int64_t r, int64_t ldg, double *V, int64_t
     }
     if (b == 16)
         return block_drive_t<32>(G, n, r, ldg, V, ldv, signs_host, p, cfg, sigma, lam, ws,
-                                 ws_bytes, res, tele, s);
+                                 ws_bytes, res, tele, ctx);
     return block_drive_t<64>(G, n, r, ldg, V, ldv, signs_host, p, cfg, sigma, lam, ws,
-                             ws_bytes, res, tele, s);
+                             ws_bytes, res, tele, ctx);
 }
 
 }  // namespace hsvd

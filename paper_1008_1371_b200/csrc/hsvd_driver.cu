@@ -28,6 +28,91 @@ int cuda_fail(cudaError_t e, const char *what)
     return HSVD_ERR_CUDA;
 }
 
+int DevCtx::host_reserve(int64_t len)
+{
+    if (len <= host_len) return HSVD_OK;
+    if (host) cudaFreeHost(host);
+    host = nullptr;
+    host_len = 0;
+    HSVD_CUDA(cudaHostAlloc((void **)&host, len * sizeof(int64_t), cudaHostAllocDefault));
+    host_len = len;
+    return HSVD_OK;
+}
+
+int DevCtx::extra(size_t k)
+{
+    while (xs.size() < k) {
+        cudaStream_t st;
+        cudaEvent_t a, b, c;
+        HSVD_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        HSVD_CUDA(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+        HSVD_CUDA(cudaEventCreate(&b));
+        HSVD_CUDA(cudaEventCreate(&c));
+        xs.push_back(st);
+        xev.push_back(a);
+        xt0.push_back(b);
+        xt1.push_back(c);
+    }
+    return HSVD_OK;
+}
+
+DevCtx::~DevCtx()
+{
+    // thread exit: the context's device may not be current; best effort
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (dev >= 0) cudaSetDevice(dev);
+    for (size_t i = 0; i < xs.size(); ++i) {
+        cudaStreamDestroy(xs[i]);
+        cudaEventDestroy(xev[i]);
+        cudaEventDestroy(xt0[i]);
+        cudaEventDestroy(xt1[i]);
+    }
+    if (host) cudaFreeHost(host);
+    if (ev) cudaEventDestroy(ev);
+    if (t0) cudaEventDestroy(t0);
+    if (t1) cudaEventDestroy(t1);
+    if (s) cudaStreamDestroy(s);
+    if (cur >= 0) cudaSetDevice(cur);
+}
+
+DevCtx *dev_ctx(int dev, int *status)
+{
+    static thread_local std::vector<DevCtx *> ctxs;
+    *status = HSVD_OK;
+    if (dev < 0) {
+        *status = HSVD_ERR_ARG;
+        return nullptr;
+    }
+    if ((int)ctxs.size() <= dev) ctxs.resize(dev + 1, nullptr);
+    if (ctxs[dev]) return ctxs[dev];
+    struct Owner {
+        std::vector<DevCtx *> *v;
+        ~Owner()
+        {
+            for (auto c : *v) delete c;
+        }
+    };
+    static thread_local Owner owner{&ctxs};
+    (void)owner;
+    DevCtx *c = new DevCtx();
+    c->dev = dev;
+    cudaError_t e = cudaStreamCreateWithFlags(&c->s, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreate(&c->t0);
+    if (e == cudaSuccess) e = cudaEventCreate(&c->t1);
+    if (e == cudaSuccess) e = cudaHostAlloc((void **)&c->host, 64 * sizeof(int64_t),
+                                            cudaHostAllocDefault);
+    if (e != cudaSuccess) {
+        *status = cuda_fail(e, "dev_ctx");
+        delete c;
+        return nullptr;
+    }
+    c->host_len = 64;
+    ctxs[dev] = c;
+    return c;
+}
+
 int launch_identity(double *V, int64_t r, int64_t ldv, cudaStream_t s);
 int launch_init_packages(const int8_t *signs, int64_t r, int64_t *rho,
                          int64_t *jsign, cudaStream_t s);
@@ -38,7 +123,7 @@ int block_drive(double *G, int64_t n, int64_t r, int64_t ldg, double *V,
                 int64_t ldv, const int8_t *signs_host, int64_t p,
                 const hsvd_config *cfg, double *sigma, double *lam,
                 void *ws, int64_t ws_bytes, hsvd_result *res,
-                hsvd_telemetry *tele, cudaStream_t s);
+                hsvd_telemetry *tele, DevCtx &ctx);
 int64_t block_workspace_size(int64_t n, int64_t r, const hsvd_config *cfg);
 
 // Bump allocator over the caller's workspace.
@@ -99,23 +184,14 @@ static int64_t carve_pointwise(Carve &c, int64_t r, const hsvd_config *cfg,
     return c.off + 256;
 }
 
-// RAII for the internal stream, pinned summary and graph.
+// RAII for the per-call graph.
 struct DriveRes {
-    cudaStream_t s = nullptr;
-    cudaEvent_t ev = nullptr;
-    cudaEvent_t t0 = nullptr, t1 = nullptr;
-    int64_t *host = nullptr;
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     ~DriveRes()
     {
         if (exec) cudaGraphExecDestroy(exec);
         if (graph) cudaGraphDestroy(graph);
-        if (host) cudaFreeHost(host);
-        if (ev) cudaEventDestroy(ev);
-        if (t0) cudaEventDestroy(t0);
-        if (t1) cudaEventDestroy(t1);
-        if (s) cudaStreamDestroy(s);
     }
 };
 
@@ -165,8 +241,9 @@ static int pointwise_drive(double *G, int64_t n, int64_t r, int64_t ldg,
                            int64_t p, const hsvd_config *cfg, double *sigma,
                            double *lam, void *ws, int64_t ws_bytes,
                            hsvd_result *res, hsvd_telemetry *tele,
-                           cudaStream_t s, DriveRes &R)
+                           DevCtx &ctx, DriveRes &R)
 {
+    cudaStream_t s = ctx.s;
     Carve c{(char *)ws, 0, ws_bytes};
     PointwiseWs w;
     if (carve_pointwise(c, r, cfg, &w) > ws_bytes) {
@@ -176,7 +253,7 @@ static int pointwise_drive(double *G, int64_t n, int64_t r, int64_t ldg,
     size_t smem;
     int st = pointwise_smem_bytes(n, cfg->chunk, &smem);
     if (st) return st;
-    int64_t *host = R.host;
+    int64_t *host = ctx.host;
 
     if (V) {
         st = launch_identity(V, r, ldv, s);
@@ -230,14 +307,12 @@ static int pointwise_drive(double *G, int64_t n, int64_t r, int64_t ldg,
     const bool rc = cfg->schedule == HSVD_SCHEDULE_ROW_CYCLIC;
     const int64_t per_sweep = (rc ? 1 : r) + 1 + (cfg->sort ? 2 : 0);
     int64_t launches = 1 + (V ? 1 : 0) + 1 + (cfg->sort ? 2 : 0) + (rc ? 0 : 1) + 2;
-    HSVD_CUDA(cudaEventCreate(&R.t0));
-    HSVD_CUDA(cudaEventCreate(&R.t1));
     int64_t sweeps_used = 0, total_rot = 0, total_skip = 0;
     int stop = 2;
     const double t_loop0 = wall_ms();
     res->setup_ms = t_loop0;  // absolute for now; hsvd_drive makes it relative
     for (int64_t sweep = 0; sweep < cfg->max_sweeps; ++sweep) {
-        HSVD_CUDA(cudaEventRecord(R.t0, s));
+        HSVD_CUDA(cudaEventRecord(ctx.t0, s));
         launches += per_sweep;
         if (R.exec) {
             HSVD_CUDA(cudaGraphLaunch(R.exec, s));
@@ -246,11 +321,11 @@ static int pointwise_drive(double *G, int64_t n, int64_t r, int64_t ldg,
             st = enqueue_sweep(G, n, r, ldg, V, ldv, p, cfg, w, host, s, T);
             if (st) return st;
         }
-        HSVD_CUDA(cudaEventRecord(R.t1, s));
+        HSVD_CUDA(cudaEventRecord(ctx.t1, s));
         HSVD_CUDA(cudaStreamSynchronize(s));
         if (T.on) T.collect(res);
         float sweep_ms = 0.f;
-        HSVD_CUDA(cudaEventElapsedTime(&sweep_ms, R.t0, R.t1));
+        HSVD_CUDA(cudaEventElapsedTime(&sweep_ms, ctx.t0, ctx.t1));
         if ((unsigned long long)host[4] != kNoError) {
             unpack_err((unsigned long long)host[4], res->err);
             res->status = HSVD_DEFINITENESS_LOST;
@@ -349,27 +424,28 @@ int hsvd_drive(double *G, int64_t n, int64_t r, int64_t ldg, double *Vinv_t,
     }
     DriveRes R;
     cudaStream_t caller = (cudaStream_t)stream;
-    HSVD_CUDA(cudaStreamCreateWithFlags(&R.s, cudaStreamNonBlocking));
-    HSVD_CUDA(cudaEventCreateWithFlags(&R.ev, cudaEventDisableTiming));
-    HSVD_CUDA(cudaHostAlloc((void **)&R.host, 16 * sizeof(int64_t), cudaHostAllocDefault));
-    HSVD_CUDA(cudaEventRecord(R.ev, caller));
-    HSVD_CUDA(cudaStreamWaitEvent(R.s, R.ev, 0));
+    int dev = 0, cst = 0;
+    HSVD_CUDA(cudaGetDevice(&dev));
+    DevCtx *ctx = dev_ctx(dev, &cst);
+    if (!ctx) return res_host->status = cst;
+    HSVD_CUDA(cudaEventRecord(ctx->ev, caller));
+    HSVD_CUDA(cudaStreamWaitEvent(ctx->s, ctx->ev, 0));
     double *V = cfg->accumulate_v ? Vinv_t : nullptr;
     int st;
     if (cfg->mode == HSVD_MODE_BLOCK)
         st = block_drive(G, n, r, ldg, V, ldv, signs_host, p, cfg, sigma, lam,
-                         workspace, workspace_bytes, res_host, tele_host, R.s);
+                         workspace, workspace_bytes, res_host, tele_host, *ctx);
     else
         st = pointwise_drive(G, n, r, ldg, V, ldv, signs_host, p, cfg, sigma,
                              lam, workspace, workspace_bytes, res_host,
-                             tele_host, R.s, R);
+                             tele_host, *ctx, R);
     res_host->status = st;
     // hand the results back to the caller's stream
-    cudaError_t e1 = cudaEventRecord(R.ev, R.s);
-    cudaError_t e2 = cudaStreamWaitEvent(caller, R.ev, 0);
+    cudaError_t e1 = cudaEventRecord(ctx->ev, ctx->s);
+    cudaError_t e2 = cudaStreamWaitEvent(caller, ctx->ev, 0);
     if (st == HSVD_OK && (e1 != cudaSuccess || e2 != cudaSuccess))
         return cuda_fail(e1 != cudaSuccess ? e1 : e2, "stream join");
-    cudaStreamSynchronize(R.s);
+    cudaStreamSynchronize(ctx->s);
     if (st == HSVD_OK) {
         const double t_loop0 = res_host->setup_ms;
         res_host->setup_ms = t_loop0 - t_entry;

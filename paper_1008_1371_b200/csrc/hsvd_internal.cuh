@@ -86,6 +86,27 @@ struct KernelTimer {
     }
 };
 
+// Per-thread, per-device resources reused across solves: creating and
+// destroying streams, events and pinned buffers per call costs from
+// milliseconds to hundreds of milliseconds (measured), so a solve borrows
+// them from here.  xs/xev/xt0/xt1 are extra streams for the shards of the
+// sharded driver's local transport.
+struct DevCtx {
+    int dev = -1;
+    cudaStream_t s = nullptr;
+    cudaEvent_t ev = nullptr, t0 = nullptr, t1 = nullptr;
+    int64_t *host = nullptr;  // pinned
+    int64_t host_len = 0;
+    std::vector<cudaStream_t> xs;
+    std::vector<cudaEvent_t> xev, xt0, xt1;
+    int host_reserve(int64_t len);  // grow-only
+    int extra(size_t k);            // at least k extra streams
+    ~DevCtx();
+};
+// the calling thread's context of device dev (created on first use; the
+// device must be current)
+DevCtx *dev_ctx(int dev, int *status);
+
 // Packed (block, i, j) error word; min over failing slots = first slot.
 __host__ __device__ inline unsigned long long pack_err(int64_t k, int64_t i,
                                                        int64_t j)

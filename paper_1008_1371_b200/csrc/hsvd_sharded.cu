@@ -468,15 +468,11 @@ struct ShardedDriver {
 
     ~ShardedDriver()
     {
+        // streams, events and pinned memory belong to the device contexts
         for (auto &x : sh) {
             cudaSetDevice(x.dev);
             if (x.s) cudaStreamSynchronize(x.s);
-            if (x.ev) cudaEventDestroy(x.ev);
-            if (x.t0) cudaEventDestroy(x.t0);
-            if (x.t1) cudaEventDestroy(x.t1);
-            if (x.s) cudaStreamDestroy(x.s);
         }
-        if (host) cudaFreeHost(host);
     }
 
     int local_index(int g) const
@@ -807,14 +803,30 @@ struct ShardedDriver {
         rho_off = 8 * std::max<int64_t>(2, (int64_t)sh.size());
         stage_base = rho_off + r;
         host_len = stage_base + (int64_t)sh.size() * (8 * r + 4 * pl.max_areas() * b + 1024);
-        HSVD_CUDA(cudaHostAlloc((void **)&host, host_len * sizeof(int64_t), cudaHostAllocDefault));
+        // borrow streams / events / pinned memory from the device contexts:
+        // the k-th shard on a device takes that device's k-th extra stream
+        std::vector<int> used_on;
         for (auto &x : sh) {
             HSVD_CUDA(cudaSetDevice(x.dev));
             HSVD_CUDA_OK(K::setup());
-            HSVD_CUDA(cudaStreamCreateWithFlags(&x.s, cudaStreamNonBlocking));
-            HSVD_CUDA(cudaEventCreateWithFlags(&x.ev, cudaEventDisableTiming));
-            HSVD_CUDA(cudaEventCreate(&x.t0));
-            HSVD_CUDA(cudaEventCreate(&x.t1));
+            int cst = 0;
+            DevCtx *c = dev_ctx(x.dev, &cst);
+            if (!c) return cst;
+            if ((int)used_on.size() <= x.dev) used_on.resize(x.dev + 1, 0);
+            const int k = used_on[x.dev]++;
+            HSVD_CUDA_OK(c->extra(k + 1));
+            x.s = c->xs[k];
+            x.ev = c->xev[k];
+            x.t0 = c->xt0[k];
+            x.t1 = c->xt1[k];
+        }
+        {
+            HSVD_CUDA(cudaSetDevice(sh[0].dev));
+            int cst = 0;
+            DevCtx *c = dev_ctx(sh[0].dev, &cst);
+            if (!c) return cst;
+            HSVD_CUDA_OK(c->host_reserve(host_len));
+            host = c->host;
         }
         HSVD_CUDA_OK(sync_all());
         // ---- precompute + sort on every shard from the full factor

@@ -57,7 +57,7 @@ class SolverConfig:
     sort: bool = True
     mode: str = "pointwise"
     block_cols: int = 32
-    inner_ordering: str = "oriented"
+    inner_ordering: str = "full"
     use_graph: bool = True
     profile: bool = False
     #: block mode 2x2 rotation: "fast" (plain fp64) or "dd" (the reference's

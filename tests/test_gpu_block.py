@@ -46,7 +46,10 @@ def test_block_matches_reference(case, rot):
     rb, rr = residuals(G, res, signs), residuals(G, ref, signs)
     for k in rb:
         assert rb[k] <= RESID_FACTOR * rr[k] + 1e-15, (k, rb[k], rr[k])
-    assert abs(res.sweeps_used - ref.sweeps_used) <= 3, (res.sweeps_used, ref.sweeps_used)
+    # block sweeps: the full inner ordering (default) rotates every pair of
+    # the pivot block at every step, so it never needs more sweeps than the
+    # reference (up to a small band) and often needs fewer
+    assert res.sweeps_used <= ref.sweeps_used + 3, (res.sweeps_used, ref.sweeps_used)
 
 
 def test_block_big_golden(golden_big):
@@ -66,7 +69,7 @@ def test_block_big_golden(golden_big):
         assert rb["dU"] <= RESID_FACTOR * c["dU"], (c["name"], rb, c["dU"])
         assert rb["vjv"] <= RESID_FACTOR * c["VtJV"], (c["name"], rb, c["VtJV"])
         assert rb["recon"] <= RESID_FACTOR * c["recon"], (c["name"], rb, c["recon"])
-        assert abs(res.sweeps_used - c["sweeps_used"]) <= 3
+        assert res.sweeps_used <= c["sweeps_used"] + 3
 
 
 def test_block_deterministic():
