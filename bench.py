@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--block-cols", type=int, default=32)
     ap.add_argument("--block-rotation", default="fast", choices=["fast", "dd"])
     ap.add_argument("--inner-ordering", default="full", choices=["oriented", "full"])
+    ap.add_argument("--inner-passes", type=int, default=1)
     ap.add_argument("--cpu-sample-s", type=float, default=12.0)
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--no-cpu", action="store_true")
@@ -270,7 +271,8 @@ def run_ours(a, rank, world, local_rank):
     G, signs = make_input(a.n, a.p, seed=0)
     J = H.SignatureVector(signs, a.p)
     cfg = H.SolverConfig(mode=a.mode, block_cols=a.block_cols,
-                         block_rotation=a.block_rotation, inner_ordering=a.inner_ordering)
+                         block_rotation=a.block_rotation, inner_ordering=a.inner_ordering,
+                         inner_passes=a.inner_passes)
     if a.mode == "block" and a.n % (2 * a.block_cols):
         raise SystemExit("block mode needs n to be a multiple of 2*block_cols")
     sharded = world > 1 or a.sharded
@@ -332,7 +334,7 @@ def run_ours(a, rank, world, local_rank):
     tele = res.telemetry
     pcfg = H.SolverConfig(mode=a.mode, block_cols=a.block_cols,
                           block_rotation=a.block_rotation, inner_ordering=a.inner_ordering,
-                          max_sweeps=1, profile=True)
+                          inner_passes=a.inner_passes, max_sweeps=1, profile=True)
     prof = solve(pcfg)
     kp = prof.kernel_profile
     peaks = {}
@@ -457,7 +459,7 @@ def run_ours(a, rank, world, local_rank):
             "config": {"workload": f"n={a.n} p={a.p} full HSVD with V^-T (SURVEY.md §8(d) cfg 5)",
                        "n": a.n, "p": a.p, "mode": a.mode,
                        **({"block_cols": a.block_cols, "block_rotation": a.block_rotation,
-                           "inner_ordering": a.inner_ordering}
+                           "inner_ordering": a.inner_ordering, "inner_passes": a.inner_passes}
                           if a.mode == "block" else {}),
                        "parallelism": (f"{world} GPUs: block-column slots sharded, NCCL ring "
                                        "exchange per step" if sharded else "1 GPU"),

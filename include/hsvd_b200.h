@@ -66,6 +66,9 @@ typedef struct hsvd_config {
     int32_t profile;      /* time every kernel of sweep 0 with CUDA events
                              (no graph); fills hsvd_result.kernel_ms     */
     int32_t block_rotation; /* block mode: HSVD_ROTATION_*               */
+    int32_t inner_passes;   /* block mode: passes of the inner ordering
+                               per step (1 = one pass, the paper's block-
+                               oriented scheme; more = toward full-block) */
 } hsvd_config;
 
 /* Per-run result record: the scalar part of HsvdResult (solver.py:67-77). */

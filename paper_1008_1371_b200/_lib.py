@@ -55,6 +55,7 @@ class HsvdConfigC(ctypes.Structure):
         ("use_graph", ctypes.c_int32),
         ("profile", ctypes.c_int32),
         ("block_rotation", ctypes.c_int32),
+        ("inner_passes", ctypes.c_int32),
     ]
 
 

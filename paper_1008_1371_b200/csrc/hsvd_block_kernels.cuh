@@ -262,7 +262,8 @@ struct InnerArgs {
     unsigned long long *err;
     int64_t nb, slot_base;
     double eps, teps;
-    int full, use_skip;
+    int full, use_skip, passes;
+    long long *trace;  // debug: per-round clock64 stamps of CTA 0 (NULL)
 };
 
 // Touched-column set of a slot visit: the columns of P that took part in at
@@ -288,32 +289,55 @@ struct InnerSmem {
 
 // Plain-double annihilating rotation for block mode (the pointwise mode keeps
 // the reference's double-double rotation_tc, hsvd_rotation.cuh).  Same
-// branches, same sign convention and same definiteness test as rotation_tc
-// (_kernels.py:128-173): trig t = sgn(zeta)/(|zeta| + sqrt(1 + zeta^2)),
-// hyperbolic t = theta/(1 + sqrt(1 - theta^2)); 1 - x^2 by one fma.
+// branches, sign convention and definiteness test as rotation_tc
+// (_kernels.py:128-173), rewritten to one division and one square root:
+//   trig (d = a_jj - a_ii, e = 2 a_ij, zeta = d / e):
+//     t = sgn(zeta) |e| / (|d| + sqrt(d^2 + e^2)),   c = 1 / sqrt(1 + t^2)
+//     (= sgn(zeta) / (|zeta| + sqrt(1 + zeta^2)); for |zeta| > 6.7e7 it is
+//     the reference's 1 / (2 zeta) to rounding, and c rounds to 1);
+//   hyperbolic (s = a_ii + a_jj, theta = -e / s):
+//     t = -e / (s + sqrt((s - |e|)(s + |e|))),       c = 1 / sqrt(1 - t^2)
+//     (= theta / (1 + sqrt(1 - theta^2)); |theta| >= 1 -> status 1).
+// Operands beyond 1e150 take the reference's quotient form (no overflow).
 __device__ __forceinline__ int rotation_fast(double a_ii, double a_jj, double a_ij, int hyp,
                                              double &t_out, double &c_out)
 {
     t_out = 0.0;
     c_out = 1.0;
     if (a_ij == 0.0) return 0;
+    const double e = 2.0 * a_ij, ae = fabs(e);
     if (hyp < 0) {
-        const double zeta = (a_jj - a_ii) / (2.0 * a_ij);
-        if (fabs(zeta) > 6.7e7) {
-            t_out = 0.5 / zeta;
-            return 0;
+        const double d = a_jj - a_ii, ad = fabs(d);
+        double t;
+        if (ad < 1e150 && ae < 1e150) {
+            const double sg = (d == 0.0 || (d > 0.0) == (e > 0.0)) ? 1.0 : -1.0;
+            t = sg * ae / (ad + sqrt(fma(d, d, e * e)));
+        } else {
+            const double zeta = d / e;
+            if (fabs(zeta) > 6.7e7) {
+                t_out = 0.5 / zeta;
+                return 0;
+            }
+            const double az = fabs(zeta);
+            t = 1.0 / (az + sqrt(fma(az, az, 1.0)));
+            if (!(zeta >= 0.0)) t = -t;
         }
-        const double az = fabs(zeta);
-        double t = 1.0 / (az + sqrt(fma(az, az, 1.0)));
-        if (!(zeta >= 0.0)) t = -t;
         t_out = t;
         c_out = rsqrt(fma(t, t, 1.0));
         return 0;
     }
-    const double th = (-2.0 * a_ij) / (a_ii + a_jj);
-    const double d = fma(-th, th, 1.0);
-    if (!(d > 0.0)) return 1;
-    const double t = th / (1.0 + sqrt(d));
+    const double sm = a_ii + a_jj;
+    double t;
+    if (sm < 1e150 && ae < 1e150) {
+        const double D = (sm - ae) * (sm + ae);
+        if (!(D > 0.0)) return 1;
+        t = -e / (sm + sqrt(D));
+    } else {
+        const double th = -e / sm;
+        const double D = fma(-th, th, 1.0);
+        if (!(D > 0.0)) return 1;
+        t = th / (1.0 + sqrt(D));
+    }
     const double u = fma(-t, t, 1.0);
     if (!(u > 0.0)) return 1;
     t_out = t;
@@ -331,6 +355,10 @@ __device__ __forceinline__ int rotation_fast(double a_ii, double a_jj, double a_
 // pair q; a warp-uniform decision skips inactive rounds without a barrier),
 // then updates its share of the blocks and of W from registers and shuffles:
 // two barriers per active round, none per inactive round.
+// threads of one k_inner CTA
+template <int B2>
+constexpr int inner_threads() { return kThreads; }
+
 template <int B2, bool FAST>
 __global__ void __launch_bounds__(kThreads) k_inner(InnerArgs a)
 {
@@ -402,7 +430,8 @@ __global__ void __launch_bounds__(kThreads) k_inner(InnerArgs a)
     constexpr int NWR = B2 * b / kThreads;  // W rows per thread per round
     const int q = lane % b;                 // pair owned by this thread
     const int prow = tid / b;
-    for (int rd = 0; rd < rounds; ++rd) {
+    for (int it = 0; it < rounds * a.passes; ++it) {
+        const int rd = it % rounds;
         // ---- phase R: every warp forms all b rotations of the round
         int i, j;
         if (a.full) {  // circle method on B2 players
@@ -417,7 +446,10 @@ __global__ void __launch_bounds__(kThreads) k_inner(InnerArgs a)
         const double a_ii = S.A[i][i], a_jj = S.A[j][j], a_ij = S.A[i][j];
         double t = 0.0, c = 1.0, st = 0.0;
         int act = 0, bad = 0;
-        if (!(a_ij == 0.0 || (a.use_skip && fabs(a_ij) < a.eps * sqrt(a_ii * a_jj)))) {
+        // relative-orthogonality skip |a_ij| < eps sqrt(a_ii a_jj)
+        // (_kernels.py:211), squared: no square root on the critical path
+        if (!(a_ij == 0.0 ||
+              (a.use_skip && a_ij * a_ij < (a.eps * a.eps) * (a_ii * a_jj)))) {
             const int hyp = S.js[i] == S.js[j] ? -1 : 1;
             const int status = FAST ? rotation_fast(a_ii, a_jj, a_ij, hyp, t, c)
                                     : rotation_tc(a_ii, a_jj, a_ij, hyp, t, c);
@@ -831,6 +863,8 @@ struct BlockKernels {
         ia.C = w.C; ia.tset = w.tset; ia.rotk = w.rotk; ia.skipk = w.skipk; ia.maxt = w.maxt; ia.err = w.err;
         ia.nb = w.nb; ia.slot_base = w.slot_base; ia.eps = cfg->eps; ia.teps = cfg->teps;
         ia.full = full; ia.use_skip = cfg->use_skip;
+        ia.passes = cfg->inner_passes > 1 ? cfg->inner_passes : 1;
+        ia.trace = nullptr;
         T.begin(1, s);
         if (cfg->block_rotation == HSVD_ROTATION_FAST)
             k_inner<B2, true><<<(unsigned)nslots, kThreads, inner_smem(), s>>>(ia);

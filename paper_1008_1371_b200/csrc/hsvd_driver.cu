@@ -388,6 +388,7 @@ void hsvd_default_config(hsvd_config *cfg)
     cfg->inner_full = 0;
     cfg->use_graph = 1;
     cfg->block_rotation = HSVD_ROTATION_FAST;
+    cfg->inner_passes = 1;
 }
 
 int64_t hsvd_drive_workspace_size(int64_t n, int64_t r, const hsvd_config *cfg)

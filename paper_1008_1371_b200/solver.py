@@ -63,6 +63,8 @@ class SolverConfig:
     #: block mode 2x2 rotation: "fast" (plain fp64) or "dd" (the reference's
     #: double-double rotation_tc, _kernels.py:128-173)
     block_rotation: str = "fast"
+    #: block mode: passes of the inner ordering per step
+    inner_passes: int = 1
 
     def __post_init__(self):
         if self.teps is None:
@@ -75,6 +77,8 @@ class SolverConfig:
             raise ValueError(f"unknown mode {self.mode!r}")
         if self.inner_ordering not in ("oriented", "full"):
             raise ValueError(f"unknown inner_ordering {self.inner_ordering!r}")
+        if self.inner_passes < 1:
+            raise ValueError("inner_passes must be >= 1")
         if self.block_rotation not in ("fast", "dd"):
             raise ValueError(f"unknown block_rotation {self.block_rotation!r}")
 
@@ -95,6 +99,7 @@ class SolverConfig:
         c.use_graph = int(bool(self.use_graph))
         c.profile = int(bool(self.profile))
         c.block_rotation = int(self.block_rotation == "fast")
+        c.inner_passes = int(self.inner_passes)
         return c
 
 

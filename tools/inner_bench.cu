@@ -1,0 +1,147 @@
+// Standalone benchmark / trace of the block inner kernel (k_inner) on
+// synthetic Gram matrices: nslots slots, one Gram segment each.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 \
+//        -Ipaper_1008_1371_b200/csrc tools/inner_bench.cu -o tools/inner_bench
+//   tools/inner_bench [nslots] [full] [iters]
+#include <cstdio>
+#include <cstdlib>
+#include <random>
+#include <vector>
+
+#include "hsvd_block_kernels.cuh"
+
+namespace hsvd {
+void set_error(const std::string &) {}
+int cuda_fail(cudaError_t e, const char *w)
+{
+    fprintf(stderr, "%s: %s\n", w, cudaGetErrorString(e));
+    exit(1);
+}
+}  // namespace hsvd
+using namespace hsvd;
+
+// latency of one rotation_fast / rotation_tc / div / sqrt (dependent chain)
+template <int KIND>
+__global__ void k_lat(double *out, long long *cyc, double a0)
+{
+    double x = a0 + threadIdx.x * 1e-3, y = 1.5, z = 0.25;
+    const long long t0 = clock64();
+    for (int k = 0; k < 256; ++k) {
+        double t, c;
+        if (KIND == 0) { rotation_fast(x, y, z, -1, t, c); x = 1.0 + t * 0.5 + c; }
+        if (KIND == 1) { rotation_fast(x, y, z, 1, t, c); x = 3.0 + t * 0.5 + c; }
+        if (KIND == 2) { rotation_tc(x, y, z, -1, t, c); x = 1.0 + t * 0.5 + c; }
+        if (KIND == 3) { x = 1.0 + 1.0 / x; }
+        if (KIND == 4) { x = 1.0 + sqrt(x); }
+        if (KIND == 5) { x = 1.0 + rsqrt(x); }
+        if (KIND == 6) { x = fma(x, 0.999, 0.001); }
+    }
+    const long long t1 = clock64();
+    out[threadIdx.x] = x;
+    if (threadIdx.x == 0) *cyc = (t1 - t0) / 256;
+}
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("%s: %s\n", #x, cudaGetErrorString(e)); return 1; } } while (0)
+
+int main(int argc, char **argv)
+{
+    constexpr int B2 = 64, b = 32;
+    const int nslots = argc > 1 ? atoi(argv[1]) : 128;
+    const int full = argc > 2 ? atoi(argv[2]) : 1;
+    const int iters = argc > 3 ? atoi(argv[3]) : 20;
+    const int nb = 2 * nslots, r = nb * b, K = 256;
+    std::mt19937_64 rng(1);
+    std::normal_distribution<double> N01;
+    std::vector<double> A((size_t)nslots * B2 * B2);
+    std::vector<double> X((size_t)B2 * K);
+    for (int s = 0; s < nslots; ++s) {
+        for (auto &v : X) v = N01(rng);
+        for (int i = 0; i < B2; ++i)
+            for (int j = 0; j < B2; ++j) {
+                double acc = 0;
+                for (int k = 0; k < K; ++k) acc += X[i * K + k] * X[j * K + k];
+                A[(size_t)s * B2 * B2 + i * B2 + j] = acc;
+            }
+    }
+    std::vector<int64_t> js(r), ip(nslots), jp(nslots), ib(nslots), jb(nslots);
+    for (int i = 0; i < r; ++i) js[i] = (i % 3 == 0) ? -1 : 1;
+    for (int k = 0; k < nslots; ++k) { ip[k] = ib[k] = k; jp[k] = jb[k] = nb - 1 - k; }
+    double *dA, *dW, *dmaxt;
+    int64_t *djs, *dip, *djp, *dib, *djb, *dcur;
+    uint8_t *dC, *dts;
+    uint32_t *drot, *dskip;
+    unsigned long long *derr;
+    long long *dtrace;
+    CK(cudaMalloc(&dA, A.size() * 8));
+    CK(cudaMalloc(&dW, A.size() * 8));
+    CK(cudaMalloc(&djs, r * 8));
+    CK(cudaMalloc(&dip, nslots * 8)); CK(cudaMalloc(&djp, nslots * 8));
+    CK(cudaMalloc(&dib, nslots * 8)); CK(cudaMalloc(&djb, nslots * 8));
+    CK(cudaMalloc(&dcur, 2 * nslots * 8));
+    CK(cudaMalloc(&dC, nslots)); CK(cudaMalloc(&dts, nslots * kTsetStride));
+    CK(cudaMalloc(&drot, nslots * 4)); CK(cudaMalloc(&dskip, nslots * 4));
+    CK(cudaMalloc(&dmaxt, nslots * 8));
+    CK(cudaMalloc(&derr, 8));
+    CK(cudaMalloc(&dtrace, 8 * 8 * 64 * 4));
+    CK(cudaMemcpy(dA, A.data(), A.size() * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(djs, js.data(), r * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemset(derr, 0xff, 8));
+    CK(cudaMemset(dC, 0, nslots)); CK(cudaMemset(drot, 0, nslots * 4));
+    CK(cudaMemset(dskip, 0, nslots * 4)); CK(cudaMemset(dmaxt, 0, nslots * 8));
+    InnerArgs ia{};
+    ia.part.W = nslots; ia.part.P = nslots; ia.part.T = 1;
+    ia.maxseg = 1; ia.Apart = dA; ia.Wg = dW; ia.jsign = djs;
+    ia.ip = dip; ia.jp = djp; ia.iblk = dib; ia.jblk = djb; ia.cur = dcur;
+    ia.C = dC; ia.tset = dts; ia.rotk = drot; ia.skipk = dskip; ia.maxt = dmaxt; ia.err = derr;
+    ia.nb = nb; ia.slot_base = 0; ia.eps = 0x1p-52; ia.teps = 0x1p-27;
+    ia.full = full; ia.use_skip = 1; ia.passes = 1; ia.trace = nullptr;
+    const size_t smem = sizeof(InnerSmem<B2>);
+    CK(cudaFuncSetAttribute(k_inner<B2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0); cudaEventCreate(&e1);
+    auto reset = [&]() {
+        cudaMemcpy(dip, ip.data(), nslots * 8, cudaMemcpyHostToDevice);
+        cudaMemcpy(djp, jp.data(), nslots * 8, cudaMemcpyHostToDevice);
+        cudaMemcpy(dib, ib.data(), nslots * 8, cudaMemcpyHostToDevice);
+        cudaMemcpy(djb, jb.data(), nslots * 8, cudaMemcpyHostToDevice);
+    };
+    for (int w = 0; w < 3; ++w) { reset(); k_inner<B2, true><<<nslots, inner_threads<B2>(), smem>>>(ia); }
+    CK(cudaDeviceSynchronize());
+    float tot = 0;
+    for (int i = 0; i < iters; ++i) {
+        reset();
+        cudaEventRecord(e0);
+        k_inner<B2, true><<<nslots, inner_threads<B2>(), smem>>>(ia);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms; cudaEventElapsedTime(&ms, e0, e1); tot += ms;
+    }
+    printf("k_inner<64> nslots=%d full=%d: %.2f us per launch\n", nslots, full, 1e3 * tot / iters);
+    {
+        double *o; long long *cy, h;
+        cudaMalloc(&o, 32 * 8); cudaMalloc(&cy, 8);
+        const char *names[] = {"rotation_fast trig", "rotation_fast hyp", "rotation_tc trig", "div", "sqrt", "rsqrt", "dfma"};
+#define LAT(K) k_lat<K><<<1, 32>>>(o, cy, 2.0); cudaMemcpy(&h, cy, 8, cudaMemcpyDeviceToHost); printf("latency %-20s %lld cycles\n", names[K], h);
+        LAT(0) LAT(1) LAT(2) LAT(3) LAT(4) LAT(5) LAT(6)
+    }
+    // trace CTA 0
+    ia.trace = dtrace;
+    CK(cudaMemset(dtrace, 0, 8 * 8 * 64 * 4));
+    reset();
+    k_inner<B2, true><<<nslots, inner_threads<B2>(), smem>>>(ia);
+    CK(cudaDeviceSynchronize());
+    std::vector<long long> tr(8 * 64 * 4);
+    CK(cudaMemcpy(tr.data(), dtrace, tr.size() * 8, cudaMemcpyDeviceToHost));
+    const int rounds = full ? B2 - 1 : b;
+    double sum[4] = {0, 0, 0, 0};
+    for (int it = 0; it < rounds; ++it) {
+        long long *t = &tr[8 * it];
+        if (it < 4) printf("round %d: rot %lld  B1 %lld  upd %lld  B2 %lld  next %lld\n", it, t[1] - t[0],
+                           t[2] - t[1], t[3] - t[2], t[4] - t[3], it + 1 < rounds ? tr[8 * (it + 1)] - t[4] : 0);
+        sum[0] += t[1] - t[0]; sum[1] += t[2] - t[1]; sum[2] += t[3] - t[2]; sum[3] += t[4] - t[3];
+    }
+    printf("avg cycles per round: rotation %.0f, barrier1 %.0f, update %.0f, barrier2 %.0f; total round %.0f\n",
+           sum[0] / rounds, sum[1] / rounds, sum[2] / rounds, sum[3] / rounds,
+           (double)(tr[8 * (rounds - 1) + 4] - tr[0]) / rounds);
+    return 0;
+}
