@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--block-rotation", default="fast", choices=["fast", "dd"])
     ap.add_argument("--inner-ordering", default="full", choices=["oriented", "full"])
     ap.add_argument("--inner-passes", type=int, default=1)
+    ap.add_argument("--block-streams", type=int, default=2)
     ap.add_argument("--cpu-sample-s", type=float, default=12.0)
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--no-cpu", action="store_true")
@@ -272,7 +273,7 @@ def run_ours(a, rank, world, local_rank):
     J = H.SignatureVector(signs, a.p)
     cfg = H.SolverConfig(mode=a.mode, block_cols=a.block_cols,
                          block_rotation=a.block_rotation, inner_ordering=a.inner_ordering,
-                         inner_passes=a.inner_passes)
+                         inner_passes=a.inner_passes, block_streams=a.block_streams)
     if a.mode == "block" and a.n % (2 * a.block_cols):
         raise SystemExit("block mode needs n to be a multiple of 2*block_cols")
     sharded = world > 1 or a.sharded
@@ -459,7 +460,8 @@ def run_ours(a, rank, world, local_rank):
             "config": {"workload": f"n={a.n} p={a.p} full HSVD with V^-T (SURVEY.md §8(d) cfg 5)",
                        "n": a.n, "p": a.p, "mode": a.mode,
                        **({"block_cols": a.block_cols, "block_rotation": a.block_rotation,
-                           "inner_ordering": a.inner_ordering, "inner_passes": a.inner_passes}
+                           "inner_ordering": a.inner_ordering, "inner_passes": a.inner_passes,
+                           "block_streams": a.block_streams}
                           if a.mode == "block" else {}),
                        "parallelism": (f"{world} GPUs: block-column slots sharded, NCCL ring "
                                        "exchange per step" if sharded else "1 GPU"),

@@ -69,6 +69,11 @@ typedef struct hsvd_config {
     int32_t inner_passes;   /* block mode: passes of the inner ordering
                                per step (1 = one pass, the paper's block-
                                oriented scheme; more = toward full-block) */
+    int32_t block_streams;  /* block mode, one GPU: 2 = the slots run as two
+                               halves on two streams, each half's step
+                               waiting only for the other half's edge slots,
+                               so one half's inner pass overlaps the other's
+                               GEMMs; 1 = one stream */
 } hsvd_config;
 
 /* Per-run result record: the scalar part of HsvdResult (solver.py:67-77). */

@@ -56,6 +56,7 @@ class HsvdConfigC(ctypes.Structure):
         ("profile", ctypes.c_int32),
         ("block_rotation", ctypes.c_int32),
         ("inner_passes", ctypes.c_int32),
+        ("block_streams", ctypes.c_int32),
     ]
 
 

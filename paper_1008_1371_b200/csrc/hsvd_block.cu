@@ -29,7 +29,11 @@
 #include <stdint.h>
 #include <string.h>
 
+#include <cstdio>
+#include <cstdlib>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "hsvd_block_kernels.cuh"
 
@@ -82,7 +86,17 @@ struct BlockWs {
     int64_t *out;
     int8_t *signs;
     SlotWs sl;
+    // split mode: the two half-slot views (shared arrays, own Gram partial
+    // buffers and partitions)
+    SlotWs half[2];
 };
+
+// The slot halves [0, S/2) and [S/2, S) of the step (split mode).
+static void half_range(int64_t nslots, int h, int64_t &lo, int64_t &hi)
+{
+    lo = h ? nslots / 2 : 0;
+    hi = h ? nslots : nslots / 2;
+}
 
 static int64_t carve_block(Carve2 &c, int64_t n, int64_t r, int b, BlockWs *w)
 {
@@ -98,6 +112,30 @@ static int64_t carve_block(Carve2 &c, int64_t n, int64_t r, int b, BlockWs *w)
     carve_slots(c, n, nslots, nb, b, &t.sl);
     t.sl.colmap = t.rho;
     t.sl.js = t.js;
+    const int64_t B2 = 2 * b;
+    for (int h = 0; h < 2; ++h) {
+        int64_t lo, hi;
+        half_range(nslots, h, lo, hi);
+        SlotWs v = t.sl;
+        const int64_t m = hi > lo ? hi - lo : 1;
+        v.ip = t.sl.ip + lo;
+        v.jp = t.sl.jp + lo;
+        v.iblk = t.sl.iblk + lo;
+        v.jblk = t.sl.jblk + lo;
+        v.cur = t.sl.cur + 2 * lo;
+        v.C = t.sl.C + lo;
+        v.tset = t.sl.tset + lo * kTsetStride;
+        v.rotk = t.sl.rotk + lo;
+        v.skipk = t.sl.skipk + lo;
+        v.maxt = t.sl.maxt + lo;
+        v.Wg = t.sl.Wg + lo * B2 * B2;
+        v.nslots = hi - lo;
+        v.slot_base = lo;
+        v.gp = gram_partition(n, m);
+        v.maxseg = gram_maxseg(v.gp, m);
+        v.Apart = c.take<double>(m * v.maxseg * B2 * B2);
+        t.half[h] = v;
+    }
     if (w) *w = t;
     return c.off + 256;
 }
@@ -188,11 +226,96 @@ static int block_drive_t(double *G, int64_t n, int64_t r, int64_t ldg, double *V
     HSVD_CUDA(cudaMemsetAsync(w.sl.err, 0xff, sizeof(unsigned long long), s));
 
     KernelTimer T;
-    auto enqueue_sweep = [&]() -> int {
+    // Split mode: the two slot halves run on two streams.  A block only
+    // crosses between the halves at their edge slots (the stepper is a ring:
+    // a slot trades blocks with slot k +- 1 or the wrap-around), so half h's
+    // Gram at step t waits for the other half's EDGE-slot update of step
+    // t - 1 only; each half updates its edge slots first.  One half's inner
+    // pass then runs beside the other half's GEMMs.
+    const bool split = cfg->block_streams >= 2 && !cfg->profile && nslots >= 4;
+    cudaStream_t s2 = nullptr;
+    cudaEvent_t ev_edge[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}}, ev_fork = nullptr,
+                ev_join = nullptr, ev_stagger = nullptr;
+    if (split) {
+        st = ctx.extra(1);
+        if (st) return st;
+        st = ctx.events(7);
+        if (st) return st;
+        s2 = ctx.xs[0];
+        ev_edge[0][0] = ctx.evs[0];
+        ev_edge[0][1] = ctx.evs[1];
+        ev_edge[1][0] = ctx.evs[2];
+        ev_edge[1][1] = ctx.evs[3];
+        ev_fork = ctx.evs[4];
+        ev_join = ctx.evs[5];
+        ev_stagger = ctx.evs[6];
+    }
+    // debug timeline (HSVD_TIMELINE=1, ungraphed first sweep): events after
+    // each phase of the first steps, printed relative to the sweep start
+    const bool tl_on = getenv("HSVD_TIMELINE") != nullptr;
+    std::vector<std::pair<std::string, cudaEvent_t>> tl;
+    cudaEvent_t tl0 = nullptr;
+    auto mark = [&](const std::string &what, cudaStream_t st) -> int {
+        if (!tl_on || tl.size() > 200) return HSVD_OK;
+        cudaEvent_t e;
+        HSVD_CUDA(cudaEventCreate(&e));
+        HSVD_CUDA(cudaEventRecord(e, st));
+        tl.push_back({what, e});
+        return HSVD_OK;
+    };
+    auto enqueue_steps_split = [&]() -> int {
+        cudaStream_t ss[2] = {s, s2};
+        if (tl_on) {
+            HSVD_CUDA(cudaEventCreate(&tl0));
+            HSVD_CUDA(cudaEventRecord(tl0, s));
+        }
+        HSVD_CUDA(cudaEventRecord(ev_fork, s));
+        HSVD_CUDA(cudaStreamWaitEvent(s2, ev_fork, 0));
         for (int64_t step = 0; step < nb; ++step) {
             const int full = cfg->inner_full || step == 0;
-            int e = K::step(G, ldg, (int)n, V, ldv, (int)r, w.sl, full, cfg, s, T);
+            for (int h = 0; h < 2; ++h) {
+                const SlotWs &hw = w.half[h];
+                const int64_t m = hw.nslots;
+                if (step > 0)
+                    HSVD_CUDA(cudaStreamWaitEvent(ss[h], ev_edge[h ^ 1][(step - 1) & 1], 0));
+                // stagger: the second half starts its sweep after the first
+                // half's first inner pass, so the halves stay half a step
+                // apart (one's inner pass beside the other's update)
+                if (step == 0 && h == 1) HSVD_CUDA(cudaStreamWaitEvent(ss[h], ev_stagger, 0));
+                const std::string tag = std::string(h ? "B" : "A") + std::to_string(step);
+                int e = mark(tag + " start", ss[h]);
+                if (e) return e;
+                e = K::gram_inner(G, ldg, (int)n, hw, full, cfg, ss[h], T);
+                if (e) return e;
+                if (step == 0 && h == 0) HSVD_CUDA(cudaEventRecord(ev_stagger, ss[h]));
+                if ((e = mark(tag + " gram+inner done", ss[h]))) return e;
+                // edge slots first, then the rest
+                e = K::update(G, ldg, (int)n, V, ldv, (int)r, hw, 0, 1, ss[h], T, true);
+                if (e) return e;
+                e = K::update(G, ldg, (int)n, V, ldv, (int)r, hw, m - 1, m, ss[h], T, true);
+                if (e) return e;
+                HSVD_CUDA(cudaEventRecord(ev_edge[h][step & 1], ss[h]));
+                if ((e = mark(tag + " edges done", ss[h]))) return e;
+                e = K::update(G, ldg, (int)n, V, ldv, (int)r, hw, 1, m - 1, ss[h], T);
+                if (e) return e;
+                if ((e = mark(tag + " update done", ss[h]))) return e;
+            }
+        }
+        HSVD_CUDA(cudaEventRecord(ev_join, s2));
+        HSVD_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
+        return HSVD_OK;
+    };
+    bool split_now = split;  // this sweep's mode (see the sweep loop)
+    auto enqueue_sweep = [&]() -> int {
+        if (split_now) {
+            int e = enqueue_steps_split();
             if (e) return e;
+        } else {
+            for (int64_t step = 0; step < nb; ++step) {
+                const int full = cfg->inner_full || step == 0;
+                int e = K::step(G, ldg, (int)n, V, ldv, (int)r, w.sl, full, cfg, s, T);
+                if (e) return e;
+            }
         }
         T.begin(3, s);
         int e = block_norms(G, ldg, n, w, r, nullptr, s);
@@ -208,15 +331,28 @@ static int block_drive_t(double *G, int64_t n, int64_t r, int64_t ldg, double *V
         HSVD_CUDA(cudaMemcpyAsync(host, w.out, 5 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
         return HSVD_OK;
     };
-    if (cfg->use_graph && !cfg->profile) {
+    // Split mode is launched eagerly: replayed graphs do not honour the
+    // kernel priorities that keep the critical path ahead of the bulk update
+    // (measured at n = 8192: 227 vs 218 ms per dense sweep).  Once a sweep
+    // rotates few pairs (most updates are skipped and launch overhead
+    // dominates) the remaining sweeps run as one-stream graph replays.
+    const bool graphs = cfg->use_graph && !cfg->profile && !tl_on;
+    auto capture = [&]() -> int {
+        const bool keep = split_now;
+        split_now = false;
         HSVD_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-        st = enqueue_sweep();
+        int e = enqueue_sweep();
         cudaError_t ce = cudaStreamEndCapture(s, &graph);
-        if (st) return st;
+        split_now = keep;
+        if (e) return e;
         if (ce != cudaSuccess) return cuda_fail(ce, "cudaStreamEndCapture");
         HSVD_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+        return HSVD_OK;
+    };
+    if (graphs && !split) {
+        st = capture();
+        if (st) return st;
     }
-    const int64_t per_sweep = 3 * nb + 1 + 1 + (cfg->sort ? 2 : 0);
     int64_t launches = (V ? 1 : 0) + 1 + 1 + (cfg->sort ? 2 : 0) + 1 + 2;
     int64_t sweeps_used = 0, total_rot = 0, total_skip = 0;
     int stop = 2;
@@ -224,17 +360,38 @@ static int block_drive_t(double *G, int64_t n, int64_t r, int64_t ldg, double *V
     res->setup_ms = t_loop0;  // absolute for now; hsvd_drive makes it relative
     for (int64_t sweep = 0; sweep < cfg->max_sweeps; ++sweep) {
         HSVD_CUDA(cudaEventRecord(t0, s));
-        launches += per_sweep;
-        if (exec) {
-            HSVD_CUDA(cudaGraphLaunch(exec, s));
-        } else {
+        launches += (split_now ? 8 : 3) * nb + 1 + 1 + (cfg->sort ? 2 : 0);
+        if (split_now || !graphs) {
             T.on = cfg->profile && sweep == 0;
             st = enqueue_sweep();
             if (st) return st;
+            // capture the one-stream graph for the late sweeps while the
+            // device works through this sweep
+            if (split_now && graphs && !exec) {
+                st = capture();
+                if (st) return st;
+            }
+        } else {
+            if (!exec) {
+                st = capture();
+                if (st) return st;
+            }
+            HSVD_CUDA(cudaGraphLaunch(exec, s));
         }
         HSVD_CUDA(cudaEventRecord(t1, s));
         HSVD_CUDA(cudaStreamSynchronize(s));
         if (T.on) T.collect(res);
+        if (tl_on && tl0) {
+            for (auto &x : tl) {
+                float ms = 0.f;
+                cudaEventElapsedTime(&ms, tl0, x.second);
+                fprintf(stderr, "timeline %9.1f us  %s\n", 1e3 * ms, x.first.c_str());
+                cudaEventDestroy(x.second);
+            }
+            tl.clear();
+            cudaEventDestroy(tl0);
+            tl0 = nullptr;
+        }
         float ms = 0.f;
         HSVD_CUDA(cudaEventElapsedTime(&ms, t0, t1));
         if ((unsigned long long)host[4] != kNoError) {
@@ -250,6 +407,8 @@ static int block_drive_t(double *G, int64_t n, int64_t r, int64_t ldg, double *V
         sweeps_used = sweep + 1;
         total_rot += host[1];
         total_skip += host[2];
+        // few rotations left: the remaining sweeps skip most updates
+        if (split_now && host[1] < (host[1] + host[2]) / 20) split_now = false;
         if (tele) {
             tele[sweep].sweep = sweep;
             tele[sweep].rotations = host[1];

@@ -607,14 +607,14 @@ template <int B2, int MT>
 __global__ void __launch_bounds__(kThreads, 2) k_update(
     double *__restrict__ G, int64_t ldg, int n, double *__restrict__ V, int64_t ldv, int rv,
     const int64_t *__restrict__ rho, const int64_t *__restrict__ cur,
-    const double *__restrict__ Wg, const uint8_t *__restrict__ tset, int tiles_g,
+    const double *__restrict__ Wg, const uint8_t *__restrict__ tset, int tiles_g, int slot0,
     const unsigned long long *err)
 {
     extern __shared__ __align__(16) unsigned char usm_raw[];
     auto &S = *reinterpret_cast<UpdSmem<B2, MT> *>(usm_raw);
     if (*(volatile const unsigned long long *)err != kNoError) return;
     constexpr int b = B2 / 2;
-    const int slot = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int slot = blockIdx.y + slot0, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint8_t *ts = tset + (int64_t)slot * kTsetStride;
     const int nt = ts[0];
     if (nt == 0) return;  // no rotation in this slot: W == I
@@ -822,6 +822,17 @@ inline void carve_slots(Carve2 &c, int64_t n, int64_t nslots, int64_t nb, int b,
     if (w) *w = t;
 }
 
+inline int inner_priority()
+{
+    static int prio = 1;
+    if (prio == 1) {
+        int lo = 0, hi = 0;
+        if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess) hi = 0;
+        prio = hi;  // numerically lowest = highest priority
+    }
+    return prio;
+}
+
 template <int B2>
 struct BlockKernels {
     static constexpr int KT = kGramKT, STAGES = kGramStages, MT = 128;
@@ -844,16 +855,30 @@ struct BlockKernels {
                                        (int)upd_smem()));
         return HSVD_OK;
     }
-    // one step: Gram -> inner pass -> update
-    static int step(double *G, int64_t ldg, int n, double *V, int64_t ldv, int rv,
-                    const SlotWs &w, int full, const hsvd_config *cfg, cudaStream_t s,
-                    KernelTimer &T)
+    // Gram -> inner pass of one step
+    static int gram_inner(double *G, int64_t ldg, int n, const SlotWs &w, int full,
+                          const hsvd_config *cfg, cudaStream_t s, KernelTimer &T)
     {
         const int64_t nslots = w.nslots;
         const GramPart &gp = w.gp;
         T.begin(0, s);
-        k_gram<B2, KT, STAGES><<<(unsigned)gp.P, kThreads, gram_smem(), s>>>(
-            G, ldg, n, w.colmap, w.iblk, w.jblk, gp, w.maxseg, w.Apart, w.err);
+        {
+            // Gram and inner pass are the critical path of a step: highest
+            // priority (split mode runs a bulk update on another stream)
+            cudaLaunchConfig_t lc = {};
+            lc.gridDim = dim3((unsigned)gp.P);
+            lc.blockDim = dim3(kThreads);
+            lc.dynamicSmemBytes = gram_smem();
+            lc.stream = s;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributePriority;
+            at[0].val.priority = inner_priority();
+            lc.attrs = at;
+            lc.numAttrs = 1;
+            HSVD_CUDA(cudaLaunchKernelEx(&lc, k_gram<B2, KT, STAGES>, G, ldg, n, w.colmap,
+                                         (const int64_t *)w.iblk, (const int64_t *)w.jblk, gp,
+                                         w.maxseg, w.Apart, (const unsigned long long *)w.err));
+        }
         T.end(s);
         HSVD_LAUNCH_CHECK("k_gram");
         InnerArgs ia;
@@ -866,20 +891,64 @@ struct BlockKernels {
         ia.passes = cfg->inner_passes > 1 ? cfg->inner_passes : 1;
         ia.trace = nullptr;
         T.begin(1, s);
-        if (cfg->block_rotation == HSVD_ROTATION_FAST)
-            k_inner<B2, true><<<(unsigned)nslots, kThreads, inner_smem(), s>>>(ia);
-        else
-            k_inner<B2, false><<<(unsigned)nslots, kThreads, inner_smem(), s>>>(ia);
+        {
+            // the inner pass is latency bound on few SMs: launched at the
+            // highest priority, its CTAs take SMs ahead of queued GEMM CTAs
+            // of a concurrent stream (split mode)
+            cudaLaunchConfig_t lc = {};
+            lc.gridDim = dim3((unsigned)nslots);
+            lc.blockDim = dim3(kThreads);
+            lc.dynamicSmemBytes = inner_smem();
+            lc.stream = s;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributePriority;
+            at[0].val.priority = inner_priority();
+            lc.attrs = at;
+            lc.numAttrs = 1;
+            if (cfg->block_rotation == HSVD_ROTATION_FAST)
+                HSVD_CUDA(cudaLaunchKernelEx(&lc, k_inner<B2, true>, ia));
+            else
+                HSVD_CUDA(cudaLaunchKernelEx(&lc, k_inner<B2, false>, ia));
+        }
         T.end(s);
         HSVD_LAUNCH_CHECK("k_inner");
+        return HSVD_OK;
+    }
+    // update of the slots [lo, hi) of w
+    static int update(double *G, int64_t ldg, int n, double *V, int64_t ldv, int rv,
+                      const SlotWs &w, int64_t lo, int64_t hi, cudaStream_t s, KernelTimer &T,
+                      bool urgent = false)
+    {
+        if (hi <= lo) return HSVD_OK;
         const int tiles_g = (n + MT - 1) / MT;
         const int tiles_v = V ? (rv + MT - 1) / MT : 0;
         T.begin(2, s);
-        k_update<B2, MT><<<dim3(tiles_g + tiles_v, (unsigned)nslots), kThreads, upd_smem(), s>>>(
-            G, ldg, n, V, ldv, rv, w.colmap, w.cur, w.Wg, w.tset, tiles_g, w.err);
+        cudaLaunchConfig_t lc = {};
+        lc.gridDim = dim3(tiles_g + tiles_v, (unsigned)(hi - lo));
+        lc.blockDim = dim3(kThreads);
+        lc.dynamicSmemBytes = upd_smem();
+        lc.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributePriority;
+        at[0].val.priority = urgent ? inner_priority() : 0;
+        lc.attrs = at;
+        lc.numAttrs = 1;
+        HSVD_CUDA(cudaLaunchKernelEx(&lc, k_update<B2, MT>, G, ldg, n, V, ldv, rv,
+                                     (const int64_t *)w.colmap, (const int64_t *)w.cur,
+                                     (const double *)w.Wg, (const uint8_t *)w.tset, tiles_g,
+                                     (int)lo, (const unsigned long long *)w.err));
         T.end(s);
         HSVD_LAUNCH_CHECK("k_update");
         return HSVD_OK;
+    }
+    // one step: Gram -> inner pass -> update
+    static int step(double *G, int64_t ldg, int n, double *V, int64_t ldv, int rv,
+                    const SlotWs &w, int full, const hsvd_config *cfg, cudaStream_t s,
+                    KernelTimer &T)
+    {
+        int e = gram_inner(G, ldg, n, w, full, cfg, s, T);
+        if (e) return e;
+        return update(G, ldg, n, V, ldv, rv, w, 0, w.nslots, s, T);
     }
 };
 

@@ -56,12 +56,23 @@ int DevCtx::extra(size_t k)
     return HSVD_OK;
 }
 
+int DevCtx::events(size_t k)
+{
+    while (evs.size() < k) {
+        cudaEvent_t e;
+        HSVD_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        evs.push_back(e);
+    }
+    return HSVD_OK;
+}
+
 DevCtx::~DevCtx()
 {
     // thread exit: the context's device may not be current; best effort
     int cur = -1;
     cudaGetDevice(&cur);
     if (dev >= 0) cudaSetDevice(dev);
+    for (auto e : evs) cudaEventDestroy(e);
     for (size_t i = 0; i < xs.size(); ++i) {
         cudaStreamDestroy(xs[i]);
         cudaEventDestroy(xev[i]);
@@ -389,6 +400,7 @@ void hsvd_default_config(hsvd_config *cfg)
     cfg->use_graph = 1;
     cfg->block_rotation = HSVD_ROTATION_FAST;
     cfg->inner_passes = 1;
+    cfg->block_streams = 2;
 }
 
 int64_t hsvd_drive_workspace_size(int64_t n, int64_t r, const hsvd_config *cfg)

@@ -99,8 +99,10 @@ struct DevCtx {
     int64_t host_len = 0;
     std::vector<cudaStream_t> xs;
     std::vector<cudaEvent_t> xev, xt0, xt1;
+    std::vector<cudaEvent_t> evs;   // plain (non-timing) events
     int host_reserve(int64_t len);  // grow-only
     int extra(size_t k);            // at least k extra streams
+    int events(size_t k);           // at least k plain events
     ~DevCtx();
 };
 // the calling thread's context of device dev (created on first use; the

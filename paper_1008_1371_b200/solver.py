@@ -65,6 +65,9 @@ class SolverConfig:
     block_rotation: str = "fast"
     #: block mode: passes of the inner ordering per step
     inner_passes: int = 1
+    #: block mode on one GPU: 2 = two half-slot streams (inner passes overlap
+    #: GEMMs), 1 = one stream
+    block_streams: int = 2
 
     def __post_init__(self):
         if self.teps is None:
@@ -77,6 +80,8 @@ class SolverConfig:
             raise ValueError(f"unknown mode {self.mode!r}")
         if self.inner_ordering not in ("oriented", "full"):
             raise ValueError(f"unknown inner_ordering {self.inner_ordering!r}")
+        if self.block_streams not in (1, 2):
+            raise ValueError("block_streams must be 1 or 2")
         if self.inner_passes < 1:
             raise ValueError("inner_passes must be >= 1")
         if self.block_rotation not in ("fast", "dd"):
@@ -100,6 +105,7 @@ class SolverConfig:
         c.profile = int(bool(self.profile))
         c.block_rotation = int(self.block_rotation == "fast")
         c.inner_passes = int(self.inner_passes)
+        c.block_streams = int(self.block_streams)
         return c
 
 
