@@ -61,7 +61,7 @@ typedef struct hsvd_config {
     int32_t sort;         /* 1                                            */
     int32_t mode;         /* HSVD_MODE_*                                  */
     int32_t block_cols;   /* block mode: b, columns per block (32 or 64)  */
-    int32_t inner_full;   /* block mode: 1 = full inner pass every step   */
+    int32_t inner_full;   /* block mode: 1 = full inner pass every step (default), 0 = block-oriented */
     int32_t use_graph;    /* capture each sweep as a CUDA graph           */
     int32_t profile;      /* time every kernel of sweep 0 with CUDA events
                              (no graph); fills hsvd_result.kernel_ms     */

@@ -396,7 +396,7 @@ void hsvd_default_config(hsvd_config *cfg)
     cfg->sort = 1;
     cfg->mode = HSVD_MODE_POINTWISE;
     cfg->block_cols = 32;
-    cfg->inner_full = 0;
+    cfg->inner_full = 1;
     cfg->use_graph = 1;
     cfg->block_rotation = HSVD_ROTATION_FAST;
     cfg->inner_passes = 1;
