@@ -106,6 +106,9 @@ typedef struct hsvd_telemetry {
 
 HSVD_API const char *hsvd_last_error(void);
 HSVD_API int hsvd_version(void);
+/* sizeof(hsvd_config), sizeof(hsvd_result), sizeof(hsvd_telemetry) into
+ * out[0..3): lets a binding check its struct layouts against the library. */
+HSVD_API void hsvd_abi_sizes(int64_t *out);
 HSVD_API void hsvd_default_config(hsvd_config *cfg);
 
 /* ---- reference-kernel mirrors ------------------------------------------ */

@@ -26,7 +26,7 @@ SCHEDULE_ROW_CYCLIC = 1
 
 #: every symbol include/hsvd_b200.h declares (checked by the CPU tests)
 EXPORTED = (
-    "hsvd_last_error", "hsvd_version", "hsvd_default_config",
+    "hsvd_last_error", "hsvd_version", "hsvd_abi_sizes", "hsvd_default_config",
     "hsvd_dot_chunked", "hsvd_fused_pair_update", "hsvd_rotation_batch",
     "hsvd_precompute", "hsvd_step_blocks", "hsvd_advance_stepper",
     "hsvd_stepper_init", "hsvd_sort_diagonal", "hsvd_reduce_sweep",
@@ -95,6 +95,7 @@ _D = ctypes.c_double
 _SIGS = {
     "hsvd_last_error": (ctypes.c_char_p, []),
     "hsvd_version": (ctypes.c_int, []),
+    "hsvd_abi_sizes": (None, [_P]),
     "hsvd_default_config": (None, [ctypes.POINTER(HsvdConfigC)]),
     "hsvd_dot_chunked": (ctypes.c_int, [_P, _P, _I64, _I64, _P, _P]),
     "hsvd_fused_pair_update": (ctypes.c_int, [_P, _P, _I64, _D, _D, _D, _P]),

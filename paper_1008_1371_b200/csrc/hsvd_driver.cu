@@ -383,6 +383,13 @@ const char *hsvd_last_error(void) { return g_last_error.c_str(); }
 
 int hsvd_version(void) { return 100; }
 
+void hsvd_abi_sizes(int64_t *out)
+{
+    out[0] = (int64_t)sizeof(hsvd_config);
+    out[1] = (int64_t)sizeof(hsvd_result);
+    out[2] = (int64_t)sizeof(hsvd_telemetry);
+}
+
 void hsvd_default_config(hsvd_config *cfg)
 {
     memset(cfg, 0, sizeof(*cfg));

@@ -56,9 +56,12 @@ def test_solverconfig_defaults_mirror_reference():
 
 
 def test_struct_sizes():
-    assert ctypes.sizeof(_lib.HsvdConfigC) == 72
-    assert ctypes.sizeof(_lib.HsvdResultC) == 152
-    assert ctypes.sizeof(_lib.HsvdTelemetryC) == 40
+    """The ctypes mirrors have the C layouts (sizes reported by the library)."""
+    out = (ctypes.c_int64 * 3)()
+    _lib.load().hsvd_abi_sizes(out)
+    assert ctypes.sizeof(_lib.HsvdConfigC) == out[0]
+    assert ctypes.sizeof(_lib.HsvdResultC) == out[1]
+    assert ctypes.sizeof(_lib.HsvdTelemetryC) == out[2]
 
 
 def test_workspace_size_query():
