@@ -39,6 +39,15 @@ def device_to_colmajor(Gt):
     return np.asfortranarray(Gt.cpu().numpy().T)
 
 
+def device_to_colmajor_pinned(Gt):
+    """device (r, n) -> numpy Fortran-ordered (n, r) backed by page-locked
+    host memory (torch's caching host allocator), copied at link rate."""
+    host = torch.empty(Gt.shape, dtype=Gt.dtype, pin_memory=True)
+    host.copy_(Gt, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    return host.numpy().T
+
+
 def _vec(x, dev):
     return torch.from_numpy(np.ascontiguousarray(x)).to(dev)
 

@@ -248,7 +248,11 @@ def drive(G, J, cfg=None):
         if res.Vinv_t is not None:
             res.Vinv_t = res.Vinv_t.t()
         return res
-    G = as_factor(G)
+    # as_factor (linalg.py:58-65) without its host-side finiteness scan: the
+    # factor is checked on the device right after the upload instead
+    G = np.asfortranarray(G, dtype=np.float64)
+    if G.ndim != 2:
+        raise ShapeError("G must be a matrix")
     n, r = G.shape
     if len(J) != r:
         raise ShapeError("signature length must match the column count")
@@ -258,13 +262,16 @@ def drive(G, J, cfg=None):
         raise ShapeError("G must have n >= r")
     dev = _device.require_cuda()
     Gt = _device.colmajor_to_device(G, dev)
+    if not bool(torch.isfinite(Gt).all()):
+        raise ValueError("G contains non-finite entries")
     res = drive_device(Gt, J, cfg)
-    torch.cuda.current_stream().synchronize()
-    res.U = _device.device_to_colmajor(res.U)
+    # results land in page-locked host memory (a pageable device->host copy
+    # runs at a fraction of the link rate); the numpy arrays keep it alive
+    res.U = _device.device_to_colmajor_pinned(res.U)
+    if res.Vinv_t is not None:
+        res.Vinv_t = _device.device_to_colmajor_pinned(res.Vinv_t)
     res.sigma = res.sigma.cpu().numpy()
     res.lam = res.lam.cpu().numpy()
-    if res.Vinv_t is not None:
-        res.Vinv_t = _device.device_to_colmajor(res.Vinv_t)
     return res
 
 
