@@ -493,6 +493,8 @@ def run_ours(a, rank, world, local_rank):
 
 
 def main():
+    # NCCL's version banner goes to stdout; keep stdout to the one JSON line
+    os.environ.setdefault("NCCL_DEBUG", "WARN")
     a = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -56,6 +56,18 @@ int DevCtx::extra(size_t k)
     return HSVD_OK;
 }
 
+int DevCtx::extra_hi(size_t k)
+{
+    int lo = 0, hi = 0;
+    HSVD_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    while (xhi.size() < k) {
+        cudaStream_t st;
+        HSVD_CUDA(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, hi));
+        xhi.push_back(st);
+    }
+    return HSVD_OK;
+}
+
 int DevCtx::events(size_t k)
 {
     while (evs.size() < k) {
@@ -73,6 +85,7 @@ DevCtx::~DevCtx()
     cudaGetDevice(&cur);
     if (dev >= 0) cudaSetDevice(dev);
     for (auto e : evs) cudaEventDestroy(e);
+    for (auto st : xhi) cudaStreamDestroy(st);
     for (size_t i = 0; i < xs.size(); ++i) {
         cudaStreamDestroy(xs[i]);
         cudaEventDestroy(xev[i]);

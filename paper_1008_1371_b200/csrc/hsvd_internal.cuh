@@ -100,9 +100,11 @@ struct DevCtx {
     std::vector<cudaStream_t> xs;
     std::vector<cudaEvent_t> xev, xt0, xt1;
     std::vector<cudaEvent_t> evs;   // plain (non-timing) events
+    std::vector<cudaStream_t> xhi;  // extra streams at the highest priority
     int host_reserve(int64_t len);  // grow-only
     int extra(size_t k);            // at least k extra streams
     int events(size_t k);           // at least k plain events
+    int extra_hi(size_t k);         // at least k high-priority streams
     ~DevCtx();
 };
 // the calling thread's context of device dev (created on first use; the

@@ -400,6 +400,7 @@ struct ShardWs {
     int8_t *signs;
     double *sigma, *lam;
     SlotWs sl;
+    SlotWs half[2];  // split mode: the two halves of the shard's slots
 };
 
 static int64_t carve_shard(Carve2 &c, const ShardPlan &pl, int g, int64_t n, int64_t r, int b,
@@ -434,6 +435,29 @@ static int64_t carve_shard(Carve2 &c, const ShardPlan &pl, int g, int64_t n, int
     t.sl.colmap = t.loc;
     t.sl.js = t.js;
     t.sl.slot_base = pl.s0[g];
+    const int64_t B2 = 2 * b;
+    for (int h = 0; h < 2; ++h) {
+        const int64_t lo = h ? m / 2 : 0, hi = h ? m : m / 2;
+        const int64_t mh = hi > lo ? hi - lo : 1;
+        SlotWs v = t.sl;
+        v.ip = t.sl.ip + lo;
+        v.jp = t.sl.jp + lo;
+        v.iblk = t.sl.iblk + lo;
+        v.jblk = t.sl.jblk + lo;
+        v.cur = t.sl.cur + 2 * lo;
+        v.C = t.sl.C + lo;
+        v.tset = t.sl.tset + lo * kTsetStride;
+        v.rotk = t.sl.rotk + lo;
+        v.skipk = t.sl.skipk + lo;
+        v.maxt = t.sl.maxt + lo;
+        v.Wg = t.sl.Wg + lo * B2 * B2;
+        v.nslots = hi - lo;
+        v.slot_base = pl.s0[g] + lo;
+        v.gp = gram_partition(n, mh);
+        v.maxseg = gram_maxseg(v.gp, mh);
+        v.Apart = c.take<double>(mh * v.maxseg * B2 * B2);
+        t.half[h] = v;
+    }
     if (w) *w = t;
     return c.off + 256;
 }
@@ -444,6 +468,13 @@ struct Shard {
     cudaEvent_t ev = nullptr, t0 = nullptr, t1 = nullptr;
     const double *G = nullptr;  // the caller's full factor on this device
     ShardWs w;
+    // split mode: half B's stream, the (high-priority) exchange stream and
+    // their events: edge updates per half and step parity, exchange per
+    // step parity, sweep fork / join, first-step stagger
+    cudaStream_t s2 = nullptr, sc = nullptr;
+    cudaEvent_t e_edge[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+    cudaEvent_t e_comm[2] = {nullptr, nullptr}, e_fork = nullptr, e_join = nullptr,
+                e_join2 = nullptr, e_stag = nullptr;
 };
 
 // ---------------------------------------------------------------------
@@ -465,6 +496,7 @@ struct ShardedDriver {
     int64_t *host = nullptr;
     int64_t host_len = 0, rho_off = 0, stage_base = 0, stage_off = 0;
     int64_t launches = 0;
+    bool split = false;
 
     ~ShardedDriver()
     {
@@ -794,12 +826,135 @@ struct ShardedDriver {
         return HSVD_OK;
     }
 
+    // One sweep in split mode.  Per shard, the two halves of its slots run
+    // on two streams as in the one-GPU driver (Gram, inner pass and edge-slot
+    // updates at high priority, the bulk update behind them); half h's step
+    // t + 1 waits for the other half's edge updates and for the shard's
+    // exchange of step t.  The exchange of step t runs on a high-priority
+    // stream as soon as the edge slots (the only ones that can hold an
+    // outgoing block) are updated, so it overlaps the bulk updates.
+    int sweep_split(std::vector<Move> &mv)
+    {
+        const int64_t nb = pl.nb;
+        KernelTimer Toff;
+        for (auto &x : sh) {
+            HSVD_CUDA(cudaSetDevice(x.dev));
+            HSVD_CUDA(cudaEventRecord(x.e_fork, x.s));
+            HSVD_CUDA(cudaStreamWaitEvent(x.s2, x.e_fork, 0));
+            HSVD_CUDA(cudaStreamWaitEvent(x.sc, x.e_fork, 0));
+        }
+        for (int64_t step = 0; step < nb; ++step) {
+            const int full = cfg->inner_full || step == 0;
+            const int par = step & 1;
+            for (auto &x : sh) {
+                HSVD_CUDA(cudaSetDevice(x.dev));
+                cudaStream_t ss[2] = {x.s, x.s2};
+                for (int h = 0; h < 2; ++h) {
+                    const SlotWs &hw = x.w.half[h];
+                    const int64_t m = hw.nslots;
+                    if (step > 0) {
+                        HSVD_CUDA(cudaStreamWaitEvent(ss[h], x.e_edge[h ^ 1][par ^ 1], 0));
+                        HSVD_CUDA(cudaStreamWaitEvent(ss[h], x.e_comm[par ^ 1], 0));
+                    } else if (h == 1) {
+                        HSVD_CUDA(cudaStreamWaitEvent(ss[h], x.e_stag, 0));
+                    }
+                    double *V = withV ? x.w.Vs : nullptr;
+                    HSVD_CUDA_OK(K::gram_inner(x.w.Gs, n, (int)n, hw, full, cfg, ss[h], Toff));
+                    if (step == 0 && h == 0) HSVD_CUDA(cudaEventRecord(x.e_stag, ss[h]));
+                    HSVD_CUDA_OK(K::update(x.w.Gs, n, (int)n, V, r, (int)r, hw, 0, 1, ss[h], Toff,
+                                           true));
+                    HSVD_CUDA_OK(K::update(x.w.Gs, n, (int)n, V, r, (int)r, hw, m - 1, m, ss[h],
+                                           Toff, true));
+                    HSVD_CUDA(cudaEventRecord(x.e_edge[h][par], ss[h]));
+                    HSVD_CUDA_OK(K::update(x.w.Gs, n, (int)n, V, r, (int)r, hw, 1, m - 1, ss[h],
+                                           Toff));
+                    launches += 5;
+                }
+            }
+            HSVD_CUDA_OK(pl.advance(mv));
+            // exchange of step t on each shard's exchange stream
+            for (auto &x : sh) {
+                HSVD_CUDA(cudaSetDevice(x.dev));
+                if (comm) {
+                    HSVD_CUDA(cudaStreamWaitEvent(x.sc, x.e_edge[0][par], 0));
+                    HSVD_CUDA(cudaStreamWaitEvent(x.sc, x.e_edge[1][par], 0));
+                } else {  // local transport: the sources are other shards
+                    for (auto &y : sh) {
+                        HSVD_CUDA(cudaStreamWaitEvent(x.sc, y.e_edge[0][par], 0));
+                        HSVD_CUDA(cudaStreamWaitEvent(x.sc, y.e_edge[1][par], 0));
+                        if (step > 0 && &y != &x)
+                            HSVD_CUDA(cudaStreamWaitEvent(x.sc, y.e_comm[par ^ 1], 0));
+                    }
+                }
+            }
+            if (comm && !mv.empty()) {
+                Shard &x = sh[0];
+                NcclApi *Nc = nccl();
+                HSVD_NCCL(Nc->GroupStart());
+                for (const auto &mm : mv) {
+                    if (mm.from == x.g) {
+                        HSVD_NCCL(Nc->Send(x.w.Gs + (int64_t)mm.from_area * b * n, (size_t)b * n,
+                                           ncclFloat64, mm.to, comm->comm, x.sc));
+                        if (withV)
+                            HSVD_NCCL(Nc->Send(x.w.Vs + (int64_t)mm.from_area * b * r,
+                                               (size_t)b * r, ncclFloat64, mm.to, comm->comm, x.sc));
+                    }
+                    if (mm.to == x.g) {
+                        HSVD_NCCL(Nc->Recv(x.w.Gs + (int64_t)mm.to_area * b * n, (size_t)b * n,
+                                           ncclFloat64, mm.from, comm->comm, x.sc));
+                        if (withV)
+                            HSVD_NCCL(Nc->Recv(x.w.Vs + (int64_t)mm.to_area * b * r,
+                                               (size_t)b * r, ncclFloat64, mm.from, comm->comm,
+                                               x.sc));
+                    }
+                }
+                HSVD_NCCL(Nc->GroupEnd());
+            }
+            for (const auto &mm : mv) {
+                const int li = local_index(mm.to);
+                if (li < 0) continue;
+                Shard &dst = sh[li];
+                HSVD_CUDA(cudaSetDevice(dst.dev));
+                if (!comm) {
+                    Shard &src = sh[local_index(mm.from)];
+                    HSVD_CUDA(cudaMemcpyPeerAsync(dst.w.Gs + (int64_t)mm.to_area * b * n, dst.dev,
+                                                  src.w.Gs + (int64_t)mm.from_area * b * n,
+                                                  src.dev, sizeof(double) * b * n, dst.sc));
+                    if (withV)
+                        HSVD_CUDA(cudaMemcpyPeerAsync(dst.w.Vs + (int64_t)mm.to_area * b * r,
+                                                      dst.dev,
+                                                      src.w.Vs + (int64_t)mm.from_area * b * r,
+                                                      src.dev, sizeof(double) * b * r, dst.sc));
+                }
+                k_set_loc<<<1, 64, 0, dst.sc>>>(dst.w.loc, mm.P, mm.to_area, b);
+                HSVD_LAUNCH_CHECK("k_set_loc");
+                ++launches;
+            }
+            for (auto &x : sh) {
+                HSVD_CUDA(cudaSetDevice(x.dev));
+                HSVD_CUDA(cudaEventRecord(x.e_comm[par], x.sc));
+            }
+        }
+        // join: the sweep-end work runs on the shard's main stream
+        for (auto &x : sh) {
+            HSVD_CUDA(cudaSetDevice(x.dev));
+            HSVD_CUDA(cudaEventRecord(x.e_join, x.s2));
+            HSVD_CUDA(cudaEventRecord(x.e_join2, x.sc));
+            HSVD_CUDA(cudaStreamWaitEvent(x.s, x.e_join, 0));
+            HSVD_CUDA(cudaStreamWaitEvent(x.s, x.e_join2, 0));
+        }
+        return HSVD_OK;
+    }
+
     int run(int8_t const *signs_host, double *const *U_out, double *const *V_out,
             int64_t *const *cols_host, double *const *sigma_out, double *const *lam_out,
             hsvd_result *res, hsvd_telemetry *tele)
     {
         const int64_t nb = r / b;
         HSVD_CUDA_OK(pl.init(nb, (int)(comm ? comm->nranks : sh.size())));
+        split = cfg->block_streams >= 2 && !cfg->profile;
+        for (auto &x : sh)
+            if (pl.m(x.g) < 4) split = false;
         rho_off = 8 * std::max<int64_t>(2, (int64_t)sh.size());
         stage_base = rho_off + r;
         host_len = stage_base + (int64_t)sh.size() * (8 * r + 4 * pl.max_areas() * b + 1024);
@@ -814,11 +969,26 @@ struct ShardedDriver {
             if (!c) return cst;
             if ((int)used_on.size() <= x.dev) used_on.resize(x.dev + 1, 0);
             const int k = used_on[x.dev]++;
-            HSVD_CUDA_OK(c->extra(k + 1));
-            x.s = c->xs[k];
-            x.ev = c->xev[k];
-            x.t0 = c->xt0[k];
-            x.t1 = c->xt1[k];
+            HSVD_CUDA_OK(c->extra(2 * k + 2));
+            HSVD_CUDA_OK(c->extra_hi(k + 1));
+            HSVD_CUDA_OK(c->events(10 * k + 10));
+            x.s = c->xs[2 * k];
+            x.ev = c->xev[2 * k];
+            x.t0 = c->xt0[2 * k];
+            x.t1 = c->xt1[2 * k];
+            x.s2 = c->xs[2 * k + 1];
+            x.sc = c->xhi[k];
+            cudaEvent_t *e = &c->evs[10 * k];
+            x.e_edge[0][0] = e[0];
+            x.e_edge[0][1] = e[1];
+            x.e_edge[1][0] = e[2];
+            x.e_edge[1][1] = e[3];
+            x.e_comm[0] = e[4];
+            x.e_comm[1] = e[5];
+            x.e_fork = e[6];
+            x.e_join = e[7];
+            x.e_join2 = e[8];
+            x.e_stag = e[9];
         }
         {
             HSVD_CUDA(cudaSetDevice(sh[0].dev));
@@ -908,16 +1078,21 @@ struct ShardedDriver {
             HSVD_CUDA(cudaSetDevice(x0.dev));
             HSVD_CUDA(cudaEventRecord(x0.t0, x0.s));
             T.on = cfg->profile && sweep == 0;
-            for (int64_t step = 0; step < nb; ++step) {
-                const int full = cfg->inner_full || step == 0;
-                for (auto &x : sh) {
-                    HSVD_CUDA(cudaSetDevice(x.dev));
-                    HSVD_CUDA_OK(K::step(x.w.Gs, n, (int)n, withV ? x.w.Vs : nullptr, r, (int)r,
-                                         x.w.sl, full, cfg, x.s, &x == &sh[0] ? T : Toff));
-                    launches += 3;
+            if (split && !T.on) {
+                HSVD_CUDA_OK(sweep_split(mv));
+            } else {
+                for (int64_t step = 0; step < nb; ++step) {
+                    const int full = cfg->inner_full || step == 0;
+                    for (auto &x : sh) {
+                        HSVD_CUDA(cudaSetDevice(x.dev));
+                        HSVD_CUDA_OK(K::step(x.w.Gs, n, (int)n, withV ? x.w.Vs : nullptr, r,
+                                             (int)r, x.w.sl, full, cfg, x.s,
+                                             &x == &sh[0] ? T : Toff));
+                        launches += 3;
+                    }
+                    HSVD_CUDA_OK(pl.advance(mv));
+                    HSVD_CUDA_OK(exchange(mv));
                 }
-                HSVD_CUDA_OK(pl.advance(mv));
-                HSVD_CUDA_OK(exchange(mv));
             }
             // ---- sweep end: norms, convergence word, sort, redistribution
             HSVD_CUDA_OK(gather_norms());

@@ -49,6 +49,10 @@ def test_one_shard_is_the_one_gpu_solver(b):
     (512, 512, 128, 2, "gauss", 32, 4),
     (520, 512, 200, 2, "gauss", 32, 8),
     (512, 512, 256, 0, "graded12", 32, 4),
+    # >= 4 slots per shard: split-stream steps with the overlapped exchange
+    (1024, 1024, 512, 4, "gauss", 32, 2),
+    (1024, 1024, 700, 5, "gauss", 32, 3),
+    (1024, 1024, 256, 6, "graded12", 16, 4),
 ], ids=lambda c: f"n{c[0]}r{c[1]}p{c[2]}{c[4]}b{c[5]}N{c[6]}")
 def test_sharded_matches_reference(case):
     n, r, p, seed, kind, b, N = case
@@ -63,6 +67,17 @@ def test_sharded_matches_reference(case):
     for k in rs:
         assert rs[k] <= 4.0 * r1[k] + 1e-15, (k, rs[k], r1[k])
     assert abs(s.sweeps_used - one.sweeps_used) <= 1, (s.sweeps_used, one.sweeps_used)
+
+
+@pytest.mark.parametrize("N", [1, 2])
+def test_sharded_split_matches_one_stream(N):
+    """Split-stream steps (two slot halves + overlapped exchange per shard)
+    against the one-stream sharded solver: same tolerance to each other."""
+    G, signs, J = _case(1024, 1024, 512, 7)
+    a = H.drive_local_shards(G, J, H.SolverConfig(mode="block", block_streams=1), nshards=N)
+    b = H.drive_local_shards(G, J, H.SolverConfig(mode="block", block_streams=2), nshards=N)
+    assert sigma_class_reldiff(a.sigma, a.lam, b.sigma, b.lam) <= 1e-12
+    assert abs(a.sweeps_used - b.sweeps_used) <= 1
 
 
 def test_sharded_is_deterministic():
