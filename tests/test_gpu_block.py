@@ -94,3 +94,21 @@ def test_block_rejects_bad_width():
     with pytest.raises(NotImplementedError):
         H.drive(np.eye(40), H.SignatureVector.from_p(40, 20),
                 H.SolverConfig(mode="block", block_cols=32))
+
+
+def test_block_config3_n4096_p3072_against_pointwise():
+    """BASELINE config 3 (n = 4096, p = 3072): block mode against the
+    pointwise mode, which is bit-exact with the reference (test_gpu_parity);
+    sigma per class within the north-star 1e-10, residuals at or below the
+    reference's own (factor 2 band), sweeps not above the reference's."""
+    n, p = 4096, 3072
+    G = make_case_input(n, n, 0, "gauss")
+    signs = np.array([1] * p + [-1] * (n - p), np.int8)
+    J = H.SignatureVector(signs, p)
+    ref = H.drive(G, J, H.SolverConfig(mode="pointwise"))
+    res = H.drive(G, J, H.SolverConfig(mode="block"))
+    assert sigma_class_reldiff(res.sigma, res.lam, ref.sigma, ref.lam) <= SIGMA_RTOL
+    rb, rr = residuals(G, res, signs), residuals(G, ref, signs)
+    for k in rb:
+        assert rb[k] <= 2.0 * rr[k], (k, rb[k], rr[k])
+    assert res.sweeps_used <= ref.sweeps_used
