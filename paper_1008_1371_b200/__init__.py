@@ -23,6 +23,7 @@ from .linalg import (
     fused_pair_update,
     orthonormality_distance,
 )
+from .matio import read_csv_matrix, read_gjh, write_csv_matrix, write_gjh
 from .rotation import (
     CODE_BIG,
     CODE_NONE,

@@ -1,0 +1,138 @@
+"""GJH1 / CSV files and the hsvd/eig command line (the reference's
+test_io.py and test_cli.py::TestEig, on the solver path)."""
+
+import filecmp
+import os
+
+import numpy as np
+import pytest
+from numpy.testing import assert_allclose
+
+import paper_1008_1371_b200 as H
+from paper_1008_1371_b200.cli import main
+from paper_1008_1371_b200.matio import (read_csv_matrix, read_gjh, write_csv_matrix,
+                                        write_gjh)
+
+
+def run(*argv):
+    return main([str(a) for a in argv])
+
+
+def write_bundle(path, G, p, lambda_true=None):
+    os.makedirs(path, exist_ok=True)
+    write_gjh(os.path.join(path, "G.gjh"), G, p)
+    if lambda_true is not None:
+        write_csv_matrix(os.path.join(path, "lambda_true.csv"),
+                         np.asarray(lambda_true)[np.newaxis, :])
+
+
+# ---- files (CPU) ------------------------------------------------------------
+
+def test_gjh_round_trip_bit_exact(tmp_path):
+    M = np.random.default_rng(0).standard_normal((5, 3))
+    write_gjh(tmp_path / "m.gjh", M, 2)
+    M2, p = read_gjh(tmp_path / "m.gjh")
+    assert p == 2 and M2.flags.f_contiguous and np.array_equal(M, M2)
+
+
+def test_gjh_layout(tmp_path):
+    M = np.arange(6.0).reshape(2, 3)
+    write_gjh(tmp_path / "m.gjh", M, 1)
+    raw = (tmp_path / "m.gjh").read_bytes()
+    assert raw[:4] == b"GJH1" and len(raw) == 16 + 48
+    payload = np.frombuffer(raw[16:], dtype="<f8")
+    assert np.array_equal(payload, M.ravel(order="F"))  # column-major
+
+
+@pytest.mark.parametrize("mutate,msg", [
+    (lambda b: b"XJH1" + b[4:], "bad magic"),
+    (lambda b: b[:10], "truncated GJH1 header"),
+    (lambda b: b[:-8], "truncated GJH1 payload"),
+])
+def test_gjh_errors(tmp_path, mutate, msg):
+    write_gjh(tmp_path / "m.gjh", np.eye(2), 1)
+    (tmp_path / "m.gjh").write_bytes(mutate((tmp_path / "m.gjh").read_bytes()))
+    with pytest.raises(ValueError, match=msg):
+        read_gjh(tmp_path / "m.gjh")
+
+
+def test_gjh_invalid_p(tmp_path):
+    with pytest.raises(ValueError):
+        write_gjh(tmp_path / "m.gjh", np.eye(2), 3)
+
+
+def test_csv_round_trip_exact(tmp_path):
+    M = np.random.default_rng(1).standard_normal((3, 4)) * 1e-300
+    write_csv_matrix(tmp_path / "m.csv", M)
+    assert np.array_equal(read_csv_matrix(tmp_path / "m.csv"), M)
+    write_csv_matrix(tmp_path / "v.csv", np.arange(3.0))
+    assert read_csv_matrix(tmp_path / "v.csv").shape == (1, 3)
+
+
+# ---- command line: usage and I/O errors (CPU, before any device work) --------
+
+def test_missing_bundle_exit_3(tmp_path):
+    assert run("eig", "--in", tmp_path / "nope", "--out", tmp_path / "r") == 3
+
+
+def test_odd_r_without_border_exit_2(tmp_path):
+    G = np.random.default_rng(1).standard_normal((3, 3))
+    write_bundle(tmp_path / "b", G, 3)
+    assert run("eig", "--in", tmp_path / "b", "--out", tmp_path / "r") == 2
+
+
+# ---- command line on the GPU ---------------------------------------------------
+
+@pytest.mark.gpu
+def test_eig_diagonal_bundle(tmp_path):
+    write_bundle(tmp_path / "b", np.diag([2.0, 1.0]), 1, [-1.0, 4.0])
+    assert run("eig", "--in", tmp_path / "b", "--out", tmp_path / "r") == 0
+    lam = read_csv_matrix(tmp_path / "r" / "lambda.csv").ravel()
+    assert_allclose(np.sort(lam), [-1.0, 4.0], rtol=0)
+    rec = (tmp_path / "r" / "record.csv").read_text().splitlines()
+    assert rec[0].startswith("n,r,p,sweeps") and rec[1].split(",")[3] == "1"
+
+
+@pytest.mark.gpu
+def test_eig_nonconvergence_exit_6(tmp_path):
+    write_bundle(tmp_path / "b", np.random.default_rng(0).standard_normal((8, 8)), 4)
+    assert run("eig", "--in", tmp_path / "b", "--out", tmp_path / "r", "--max-sweeps", 1) == 6
+
+
+@pytest.mark.gpu
+def test_eig_border(tmp_path):
+    G = np.random.default_rng(1).standard_normal((3, 3))
+    lam = np.linalg.eigvalsh(G @ G.T)
+    write_bundle(tmp_path / "b", G, 3, lam)
+    assert run("eig", "--in", tmp_path / "b", "--out", tmp_path / "r", "--border") == 0
+    out = read_csv_matrix(tmp_path / "r" / "lambda.csv").ravel()
+    assert out.shape == (3,)
+    assert_allclose(np.sort(out), lam, rtol=1e-12)
+
+
+@pytest.mark.gpu
+def test_eig_workers_identical_files_and_no_v(tmp_path):
+    G = np.random.default_rng(3).standard_normal((12, 12))
+    write_bundle(tmp_path / "b", G, 5)
+    run("eig", "--in", tmp_path / "b", "--out", tmp_path / "r1")
+    run("eig", "--in", tmp_path / "b", "--out", tmp_path / "r2", "--workers", 4)
+    for name in ("lambda.csv", "sigma.csv", "U.gjh", "V.gjh"):
+        assert filecmp.cmp(tmp_path / "r1" / name, tmp_path / "r2" / name, shallow=False)
+    assert run("eig", "--in", tmp_path / "b", "--out", tmp_path / "r3",
+               "--no-accumulate-v") == 0
+    assert not (tmp_path / "r3" / "V.gjh").exists()
+
+
+@pytest.mark.gpu
+def test_hsvd_block_and_shards(tmp_path):
+    n, p = 256, 100
+    G = np.random.default_rng(4).standard_normal((n, n))
+    J = H.SignatureVector.from_p(n, p)
+    ref = H.drive(G, J)  # pointwise: bit-exact with the reference
+    write_bundle(tmp_path / "b", G, p, ref.lam)
+    for extra in ([], ["--shards", "2"]):
+        out = tmp_path / ("r" + "".join(extra))
+        assert run("hsvd", "--in", tmp_path / "b", "--out", out, "--mode", "block",
+                   "--block-cols", 16, *extra) == 0
+        rec = (out / "record.csv").read_text().splitlines()[1].split(",")
+        assert float(rec[6]) <= 1e-10  # max_rel_eig_err against lambda_true
