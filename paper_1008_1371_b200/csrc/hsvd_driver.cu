@@ -274,9 +274,15 @@ static int pointwise_drive(double *G, int64_t n, int64_t r, int64_t ldg,
         set_error("workspace too small");
         return HSVD_ERR_ARG;
     }
+    // the row-cyclic walk stages both columns in shared memory (the
+    // modulus steps stream them and have no size limit)
     size_t smem;
-    int st = pointwise_smem_bytes(n, cfg->chunk, &smem);
-    if (st) return st;
+    int st = cfg->schedule == HSVD_SCHEDULE_ROW_CYCLIC ? pointwise_smem_bytes(n, cfg->chunk, &smem)
+                                                       : (cfg->chunk < 1 ? HSVD_ERR_ARG : HSVD_OK);
+    if (st) {
+        if (st == HSVD_ERR_ARG) set_error("chunk must be >= 1");
+        return st;
+    }
     int64_t *host = ctx.host;
 
     if (V) {

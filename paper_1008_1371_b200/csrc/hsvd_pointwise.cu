@@ -238,6 +238,174 @@ __global__ void __launch_bounds__(NT) k_pointwise_step(StepArgs a)
     }
 }
 
+// ---- streaming step kernel ------------------------------------------------
+// The same pair computation without staging the two columns in shared
+// memory: thread b owns chunk b of the chunked dot (_kernels.py:44-51) and
+// reads it straight from global memory (16-byte loads when aligned), the
+// partials go through the same adjacent-pair tree, and the update pass
+// rewrites chunk b and accumulates the new squared norms of the chunk in the
+// same sequential FMA order as dot_chunked(g, g) (_kernels.py:221-222).
+// Only the m chunk partials live in shared memory, so several pairs are
+// resident per SM (the staged kernel holds one: two 8192-long columns are
+// 135 KB) and one pair's tree / rotation latency hides behind another
+// pair's memory traffic.
+template <int CH, bool VEC>
+__device__ __forceinline__ double chunk_dot(const double *x, const double *y, int lo, int hi)
+{
+    double acc = 0.0;
+    if (CH > 0 && VEC && hi - lo == CH) {
+        const double2 *x2 = reinterpret_cast<const double2 *>(x + lo);
+        const double2 *y2 = reinterpret_cast<const double2 *>(y + lo);
+#pragma unroll
+        for (int e = 0; e < CH / 2; ++e) {
+            const double2 xv = x2[e], yv = y2[e];
+            acc = __fma_rn(xv.x, yv.x, acc);
+            acc = __fma_rn(xv.y, yv.y, acc);
+        }
+        return acc;
+    }
+    for (int e = lo; e < hi; ++e) acc = __fma_rn(x[e], y[e], acc);
+    return acc;
+}
+
+// update chunk [lo, hi) of the pair in place, returning the chunk's new
+// squared norms (sequential FMA from 0.0)
+template <int CH, bool VEC>
+__device__ __forceinline__ void chunk_update(double *x, double *y, int lo, int hi, double t,
+                                             double c, double st, double &nx2, double &ny2)
+{
+    double ax = 0.0, ay = 0.0;
+    if (CH > 0 && VEC && hi - lo == CH) {
+        double2 *x2 = reinterpret_cast<double2 *>(x + lo);
+        double2 *y2 = reinterpret_cast<double2 *>(y + lo);
+#pragma unroll
+        for (int e = 0; e < CH / 2; ++e) {
+            const double2 xv = x2[e], yv = y2[e];
+            double2 nx, ny;
+            nx.x = __dmul_rn(__fma_rn(st, yv.x, xv.x), c);
+            ny.x = __dmul_rn(__fma_rn(t, xv.x, yv.x), c);
+            nx.y = __dmul_rn(__fma_rn(st, yv.y, xv.y), c);
+            ny.y = __dmul_rn(__fma_rn(t, xv.y, yv.y), c);
+            x2[e] = nx;
+            y2[e] = ny;
+            ax = __fma_rn(nx.x, nx.x, ax);
+            ax = __fma_rn(nx.y, nx.y, ax);
+            ay = __fma_rn(ny.x, ny.x, ay);
+            ay = __fma_rn(ny.y, ny.y, ay);
+        }
+    } else {
+        for (int e = lo; e < hi; ++e) {
+            const double xi = x[e], yi = y[e];
+            const double nx = __dmul_rn(__fma_rn(st, yi, xi), c);
+            const double ny = __dmul_rn(__fma_rn(t, xi, yi), c);
+            x[e] = nx;
+            y[e] = ny;
+            ax = __fma_rn(nx, nx, ax);
+            ay = __fma_rn(ny, ny, ay);
+        }
+    }
+    nx2 = ax;
+    ny2 = ay;
+}
+
+template <int NT, int CH, bool VEC>
+__global__ void __launch_bounds__(NT) k_pointwise_stream(StepArgs a)
+{
+    extern __shared__ double smem[];
+    __shared__ double s_t, s_c, s_s;
+    __shared__ int s_act;
+    if (*(volatile unsigned long long *)a.err != kNoError) return;
+    const int64_t k = a.k0 + blockIdx.x;
+    int64_t i = a.iblk[k], j = a.jblk[k];
+    if (i > j) { int64_t tmp = i; i = j; j = tmp; }
+    const int64_t ci = a.rho[i], cj = a.rho[j];
+    double *gi = a.G + ci * a.ldg;
+    double *gj = a.G + cj * a.ldg;
+    const int n = a.n, chunk = CH > 0 ? CH : a.chunk, m = a.m;
+    double *p0 = smem, *p1 = p0 + m, *p2 = p1 + m, *p3 = p2 + m;
+
+    for (int bch = threadIdx.x; bch < m; bch += NT) {
+        const int lo = bch * chunk, hi = min(lo + chunk, n);
+        p0[bch] = chunk_dot<CH, VEC>(gi, gj, lo, hi);
+    }
+    const double a_ij = tree_sum<NT>(p0, p1, m);
+    if (threadIdx.x == 0) {
+        const double a_ii = a.d[i], a_jj = a.d[j];
+        int act;
+        if (a_ij == 0.0 ||
+            (a.use_skip && fabs(a_ij) < __dmul_rn(a.eps, __dsqrt_rn(__dmul_rn(a_ii, a_jj))))) {
+            act = 0;
+            a.skipk[k] += 1u;
+        } else {
+            const int64_t hyp = a.jsign[i] == a.jsign[j] ? -1 : 1;
+            double t, c;
+            const int st = rotation_tc(a_ii, a_jj, a_ij, hyp, t, c);
+            if (st != 0) {
+                atomicMin(a.err, pack_err(k, i, j));
+                act = 2;
+            } else {
+                act = 1;
+                s_t = t;
+                s_c = c;
+                s_s = hyp < 0 ? -1.0 : 1.0;
+            }
+        }
+        s_act = act;
+    }
+    __syncthreads();
+    const int act = s_act;
+    if (act == 2) return;
+    if (act == 1) {
+        const double t = s_t, c = s_c, st = __dmul_rn(s_s, s_t);
+        for (int bch = threadIdx.x; bch < m; bch += NT) {
+            const int lo = bch * chunk, hi = min(lo + chunk, n);
+            double nx2, ny2;
+            chunk_update<CH, VEC>(gi, gj, lo, hi, t, c, st, nx2, ny2);
+            p0[bch] = nx2;
+            p2[bch] = ny2;
+        }
+        if (a.V) {
+            double *vi = a.V + ci * a.ldv;
+            double *vj = a.V + cj * a.ldv;
+            for (int e = threadIdx.x; e < a.rv; e += NT) {
+                const double xi = vi[e], yi = vj[e];
+                vi[e] = __dmul_rn(__fma_rn(st, yi, xi), c);
+                vj[e] = __dmul_rn(__fma_rn(t, xi, yi), c);
+            }
+        }
+        double di, dj;
+        tree_sum2<NT>(p0, p1, p2, p3, m, di, dj);
+        if (threadIdx.x == 0) {
+            a.d[i] = di;
+            a.d[j] = dj;
+            const double at = fabs(t);
+            if (at > a.teps) a.C[k] = 3;
+            else a.C[k] |= 1;
+            a.rotk[k] += 1u;
+            if (at > a.maxt[k]) a.maxt[k] = at;
+        }
+    }
+    if (a.advance && threadIdx.x == 0) {
+        // advance_stepper (_kernels.py:238-251), this slot only
+        const int64_t r = a.r, half = r / 2;
+        int64_t ip = a.ip[k], jp = a.jp[k];
+        if (ip + jp >= r - 1) {
+            ip += 1;
+            if (ip == jp) {
+                ip -= half;
+                jp = ip;
+            }
+            a.ip[k] = ip;
+            a.jp[k] = jp;
+            a.iblk[k] = ip;
+        } else {
+            jp += 1;
+            a.jp[k] = jp;
+            a.jblk[k] = jp;
+        }
+    }
+}
+
 // Sequential row-cyclic quasi-sweep (solver.py:204-209, 231-243): one CTA
 // walks all r(r-1)/2 pairs in order; code per pair, counters at slot 0.
 template <int NT>
@@ -545,17 +713,27 @@ int launch_pointwise_step(double *G, int64_t n, int64_t ldg, double *V,
                           unsigned long long *err, cudaStream_t s)
 {
     if (k1 <= k0) return HSVD_OK;
-    size_t smem;
-    int st = pointwise_smem_bytes(n, chunk, &smem);
-    if (st) return st;
-    HSVD_CUDA(cudaFuncSetAttribute(k_pointwise_step<kStepThreads>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem));
+    if (chunk < 1) {
+        set_error("chunk must be >= 1");
+        return HSVD_ERR_ARG;
+    }
     StepArgs a = make_args(G, n, ldg, V, rv, ldv, d, rho, jsign, ip, jp, iblk,
                            jblk, r, C, k0, eps, teps, use_skip, chunk, advance,
                            rotk, skipk, maxt, err);
-    k_pointwise_step<kStepThreads><<<(unsigned)(k1 - k0), kStepThreads, smem, s>>>(a);
-    HSVD_LAUNCH_CHECK("k_pointwise_step");
+    // the streaming kernel keeps only the chunk partials in shared memory
+    const size_t smem = sizeof(double) * 4 * (size_t)a.m;
+    const unsigned grid = (unsigned)(k1 - k0);
+    const bool vec = chunk == 32 && ldg % 2 == 0 && ((uintptr_t)G & 15) == 0;
+    if (vec) {
+        HSVD_CUDA(cudaFuncSetAttribute(k_pointwise_stream<kStepThreads, 32, true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_pointwise_stream<kStepThreads, 32, true><<<grid, kStepThreads, smem, s>>>(a);
+    } else {
+        HSVD_CUDA(cudaFuncSetAttribute(k_pointwise_stream<kStepThreads, 0, false>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_pointwise_stream<kStepThreads, 0, false><<<grid, kStepThreads, smem, s>>>(a);
+    }
+    HSVD_LAUNCH_CHECK("k_pointwise_stream");
     return HSVD_OK;
 }
 
