@@ -3,13 +3,13 @@
 //
 // Built with -fmad=false (see hsvd_internal.cuh).  The per-pair work of
 // _kernels.step_blocks (/root/reference/pkg/src/hjsvd/_kernels.py:188-235)
-// runs as ONE CTA PER PIVOT SLOT: both columns are staged in shared memory
-// (coalesced loads), the chunked dot is formed from smem, one thread
-// builds the double-double rotation, the CTA updates the columns in smem and
-// streams them back, re-forms the two norms from the stored values and
-// streams the V^{-T} columns through registers.  HBM traffic per rotated
-// pair = read+write of 2 G columns and 2 V columns (the algorithmic 32(n+r)
-// bytes); a skipped pair reads its 2 G columns only.
+// runs as ONE CTA PER PIVOT SLOT.  The modulus steps use the streaming
+// kernel (k_pointwise_stream): chunk partials straight from global memory,
+// only the partials in shared memory, several pairs per SM.  The sequential
+// row-cyclic walk (one CTA for all pairs) stages both columns in shared
+// memory (process_pair).  HBM traffic per rotated pair = read+write of 2 G
+// columns and 2 V columns (the algorithmic 32(n+r) bytes); a skipped pair
+// reads its 2 G columns only.
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -207,35 +207,6 @@ __device__ int process_pair(const StepArgs &a, int64_t k, int64_t i,
     }
     __syncthreads();  // smem reuse by a following pair (row-cyclic)
     return 0;
-}
-
-template <int NT>
-__global__ void __launch_bounds__(NT) k_pointwise_step(StepArgs a)
-{
-    extern __shared__ double smem[];
-    if (*(volatile unsigned long long *)a.err != kNoError) return;
-    const int64_t k = a.k0 + blockIdx.x;
-    const int64_t i = a.iblk[k], j = a.jblk[k];
-    if (process_pair<NT>(a, k, i, j, k, smem)) return;
-    if (a.advance && threadIdx.x == 0) {
-        // advance_stepper (_kernels.py:238-251), this slot only
-        const int64_t r = a.r, half = r / 2;
-        int64_t ip = a.ip[k], jp = a.jp[k];
-        if (ip + jp >= r - 1) {
-            ip += 1;
-            if (ip == jp) {
-                ip -= half;
-                jp = ip;
-            }
-            a.ip[k] = ip;
-            a.jp[k] = jp;
-            a.iblk[k] = ip;
-        } else {
-            jp += 1;
-            a.jp[k] = jp;
-            a.jblk[k] = jp;
-        }
-    }
 }
 
 // ---- streaming step kernel ------------------------------------------------
