@@ -128,3 +128,18 @@ def test_recover_v():
 def test_no_cpu_fallback():
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         H.drive(np.eye(4), H.SignatureVector.from_p(4, 2))
+
+
+def test_sharded_api_validation():
+    """The sharded entry points reject bad calls before touching a device."""
+    G = np.zeros((64, 64))
+    J = H.SignatureVector.from_p(64, 32)
+    with pytest.raises(ValueError):
+        H.drive_sharded(G, J, H.SolverConfig(mode="block"), comm=None)
+    L = _lib.load()
+    # 2 slots of b=16 cannot feed 4 shards; r not a multiple of b
+    assert L.hsvd_shard_columns(64, 16, 4, 0) == -1
+    assert L.hsvd_shard_columns(63, 16, 1, 0) == -1
+    assert L.hsvd_shard_columns(128, 16, 2, 1) == 64
+    c = H.SolverConfig(mode="block", block_cols=16).to_c()
+    assert L.hsvd_sharded_workspace_size(128, 128, 2, 0, c) > 0
