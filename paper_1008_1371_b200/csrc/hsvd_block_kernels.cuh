@@ -699,19 +699,19 @@ __global__ void __launch_bounds__(kThreads, 2) k_update(
                 for (int j = 0; j < NI; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], bb[j]);
         }
     }
-    __syncthreads();  // everyone done reading x
+    // results straight from the accumulators: a warp store covers 8
+    // consecutive rows of 4 columns (full 32-byte sectors); the tile's rows
+    // belong to this CTA alone, and its input is already in shared memory
 #pragma unroll
-    for (int i = 0; i < MI; ++i)
+    for (int i = 0; i < MI; ++i) {
+        const int row = row0 + m0 + 8 * i + fr;
+        if (row < nrows)
 #pragma unroll
-        for (int j = 0; j < NI; ++j) {
-            const int row = m0 + 8 * i + fr, col = n0 + 8 * j + 2 * fk;
-            S.x[col][row] = acc[i][j][0];
-            S.x[col + 1][row] = acc[i][j][1];
-        }
-    __syncthreads();
-    for (int q = tid; q < B2 * MT; q += kThreads) {
-        const int c = q / MT, rr = q % MT;
-        if (row0 + rr < nrows) S.col[c][row0 + rr] = S.x[c][rr];
+            for (int j = 0; j < NI; ++j) {
+                const int col = n0 + 8 * j + 2 * fk;
+                S.col[col][row] = acc[i][j][0];
+                S.col[col + 1][row] = acc[i][j][1];
+            }
     }
 }
 
