@@ -129,6 +129,7 @@ static int64_t carve_block(Carve2 &c, int64_t n, int64_t r, int b, BlockWs *w)
         v.skipk = t.sl.skipk + lo;
         v.maxt = t.sl.maxt + lo;
         v.Wg = t.sl.Wg + lo * B2 * B2;
+        v.colidx = t.sl.colidx + lo * B2;
         v.nslots = hi - lo;
         v.slot_base = lo;
         v.gp = gram_partition(n, m);

@@ -258,6 +258,8 @@ struct InnerArgs {
     uint8_t *C;
     uint32_t *rotk, *skipk;
     uint8_t *tset;  // per slot: [count, touched columns...], kTsetStride bytes
+    const int64_t *colmap;  // position -> storage column
+    int64_t *colidx;        // per slot: storage column of each of its 2b columns
     double *maxt;
     unsigned long long *err;
     int64_t nb, slot_base;
@@ -548,6 +550,8 @@ __global__ void __launch_bounds__(kThreads) k_inner(InnerArgs a)
         if (tid == 0) atomicMin(a.err, S.fail);
         return;
     }
+    // storage columns of the slot's 2b columns, for the update's prologue
+    if (tid < B2) a.colidx[(int64_t)slot * B2 + tid] = a.colmap[slot_pos(tid, b, I, J)];
     // W column-major: Wg[slot][c * B2 + k] = W[k][c]
     double *Wout = a.Wg + (int64_t)slot * B2 * B2;
     for (int e = tid; e < B2 * B2; e += kThreads) Wout[e] = S.W[e % B2][e / B2];
@@ -606,29 +610,29 @@ struct UpdSmem {
 template <int B2, int MT>
 __global__ void __launch_bounds__(kThreads, 2) k_update(
     double *__restrict__ G, int64_t ldg, int n, double *__restrict__ V, int64_t ldv, int rv,
-    const int64_t *__restrict__ rho, const int64_t *__restrict__ cur,
-    const double *__restrict__ Wg, const uint8_t *__restrict__ tset, int tiles_g, int slot0,
-    const unsigned long long *err)
+    const int64_t *__restrict__ colidx, const double *__restrict__ Wg,
+    const uint8_t *__restrict__ tset, int tiles_g, int slot0, const unsigned long long *err)
 {
     extern __shared__ __align__(16) unsigned char usm_raw[];
     auto &S = *reinterpret_cast<UpdSmem<B2, MT> *>(usm_raw);
-    if (*(volatile const unsigned long long *)err != kNoError) return;
-    constexpr int b = B2 / 2;
     const int slot = blockIdx.y + slot0, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // the error word and the touched count are independent loads (no
+    // dependent chain in front of the tile loads)
+    const unsigned long long e0 = *err;
     const uint8_t *ts = tset + (int64_t)slot * kTsetStride;
     const int nt = ts[0];
-    if (nt == 0) return;  // no rotation in this slot: W == I
+    if (e0 != kNoError || nt == 0) return;  // failed run, or W == I
     const bool isV = (int)blockIdx.x >= tiles_g;
     const int tile = isV ? blockIdx.x - tiles_g : blockIdx.x;
     const int nrows = isV ? rv : n;
     const int64_t ld = isV ? ldv : ldg;
     double *M = isV ? V : G;
     const int row0 = tile * MT;
-    const int64_t I = cur[2 * slot], J = cur[2 * slot + 1];
+    const int64_t *cix = colidx + (int64_t)slot * B2;
     if (nt <= kSparseMax) {
         // few touched columns: out[:, T] = X[:, T] W[T, T] on the FMA pipe,
         // reading and writing only the |T| columns of this row tile
-        if (tid < nt) S.col[tid] = M + rho[slot_pos(ts[1 + tid], b, I, J)] * ld;
+        if (tid < nt) S.col[tid] = M + cix[ts[1 + tid]] * ld;
         const double *Wsl = Wg + (int64_t)slot * B2 * B2;
         for (int e = tid; e < nt * nt; e += kThreads) {
             const int c = e / nt, k = e % nt;
@@ -649,13 +653,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_update(
         }
         return;
     }
-    if (tid < B2) S.col[tid] = M + rho[slot_pos(tid, b, I, J)] * ld;
-    // W (column-major in global) -> w[c][k]
+    // W (column-major in global) -> w[c][k]: issued before the column bases
     const double *Wsrc = Wg + (int64_t)slot * B2 * B2;
     for (int q = tid; q < B2 * B2 / 2; q += kThreads) {
         const int c = (2 * q) / B2, k = (2 * q) % B2;
         cp_async16(&S.w[c][k], Wsrc + 2 * q, 16);
     }
+    if (tid < B2) S.col[tid] = M + cix[tid] * ld;
     __syncthreads();
     // X tile in two commit groups (K halves) so the first half's DMMAs
     // overlap the second half's loads
@@ -788,6 +792,7 @@ struct SlotWs {
     double *maxt;
     unsigned long long *err;
     double *Apart, *Wg;
+    int64_t *colidx;
     int64_t nslots, nb, slot_base;
     GramPart gp;
     int maxseg;
@@ -814,6 +819,7 @@ inline void carve_slots(Carve2 &c, int64_t n, int64_t nslots, int64_t nb, int b,
     t.err = c.take<unsigned long long>(1);
     t.Apart = c.take<double>(nslots * ks * B2 * B2);
     t.Wg = c.take<double>(nslots * B2 * B2);
+    t.colidx = c.take<int64_t>(nslots * B2);
     t.nslots = nslots;
     t.nb = nb;
     t.slot_base = 0;
@@ -885,7 +891,7 @@ struct BlockKernels {
         ia.part = gp; ia.maxseg = w.maxseg;
         ia.Apart = w.Apart; ia.Wg = w.Wg; ia.jsign = w.js;
         ia.ip = w.ip; ia.jp = w.jp; ia.iblk = w.iblk; ia.jblk = w.jblk; ia.cur = w.cur;
-        ia.C = w.C; ia.tset = w.tset; ia.rotk = w.rotk; ia.skipk = w.skipk; ia.maxt = w.maxt; ia.err = w.err;
+        ia.C = w.C; ia.tset = w.tset; ia.colmap = w.colmap; ia.colidx = w.colidx; ia.rotk = w.rotk; ia.skipk = w.skipk; ia.maxt = w.maxt; ia.err = w.err;
         ia.nb = w.nb; ia.slot_base = w.slot_base; ia.eps = cfg->eps; ia.teps = cfg->teps;
         ia.full = full; ia.use_skip = cfg->use_skip;
         ia.passes = cfg->inner_passes > 1 ? cfg->inner_passes : 1;
@@ -934,9 +940,9 @@ struct BlockKernels {
         lc.attrs = at;
         lc.numAttrs = 1;
         HSVD_CUDA(cudaLaunchKernelEx(&lc, k_update<B2, MT>, G, ldg, n, V, ldv, rv,
-                                     (const int64_t *)w.colmap, (const int64_t *)w.cur,
-                                     (const double *)w.Wg, (const uint8_t *)w.tset, tiles_g,
-                                     (int)lo, (const unsigned long long *)w.err));
+                                     (const int64_t *)w.colidx, (const double *)w.Wg,
+                                     (const uint8_t *)w.tset, tiles_g, (int)lo,
+                                     (const unsigned long long *)w.err));
         T.end(s);
         HSVD_LAUNCH_CHECK("k_update");
         return HSVD_OK;

@@ -451,6 +451,7 @@ static int64_t carve_shard(Carve2 &c, const ShardPlan &pl, int g, int64_t n, int
         v.skipk = t.sl.skipk + lo;
         v.maxt = t.sl.maxt + lo;
         v.Wg = t.sl.Wg + lo * B2 * B2;
+        v.colidx = t.sl.colidx + lo * B2;
         v.nslots = hi - lo;
         v.slot_base = pl.s0[g] + lo;
         v.gp = gram_partition(n, mh);
