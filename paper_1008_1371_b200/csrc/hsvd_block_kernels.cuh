@@ -187,9 +187,11 @@ __global__ void __launch_bounds__(kThreads, 3) k_gram(
 
     constexpr int CHUNKS = B2 * (KT / 2);
     constexpr int PER_T = (CHUNKS + kThreads - 1) / kThreads;
-    auto load_stage = [&](int st, int64_t item) {
-        const int si = (int)(item / part.T - slot0);
-        const int k0 = (int)(item % part.T) * KT;
+    // the item stream (slot, k-tile) is walked with 32-bit counters: no
+    // 64-bit division per k-tile
+    const int T = (int)part.T;
+    auto load_stage = [&](int st, int si, int kt) {
+        const int k0 = kt * KT;
 #pragma unroll
         for (int u = 0; u < PER_T; ++u) {
             const int q = tid + u * kThreads;
@@ -207,26 +209,47 @@ __global__ void __launch_bounds__(kThreads, 3) k_gram(
     double acc[Roles::NACC][2];
 #pragma unroll
     for (int q = 0; q < Roles::NACC; ++q) acc[q][0] = acc[q][1] = 0.0;
-    const int64_t nitems = it1 - it0;
+    const int nitems = (int)(it1 - it0);
+    const int kt0 = (int)(it0 - slot0 * part.T);
+    int ld_si = 0, ld_k = kt0;  // next item to load
+    auto ld_next = [&]() {
+        if (++ld_k == T) {
+            ld_k = 0;
+            ++ld_si;
+        }
+    };
 #pragma unroll
     for (int s = 0; s < STAGES - 1; ++s) {
-        if (s < nitems) load_stage(s, it0 + s);
+        if (s < nitems) {
+            load_stage(s, ld_si, ld_k);
+            ld_next();
+        }
         cp_async_commit();
     }
     const int fr = lane >> 2, fk = lane & 3;
-    for (int64_t i = 0; i < nitems; ++i) {
+    int c_si = 0, c_k = kt0;  // item being computed
+    int st_c = 0, st_l = STAGES - 1;
+    for (int i = 0; i < nitems; ++i) {
         cp_async_wait<STAGES - 2>();
         __syncthreads();
-        const int64_t nxt = i + STAGES - 1;
-        if (nxt < nitems) load_stage((int)(nxt % STAGES), it0 + nxt);
+        if (i + STAGES - 1 < nitems) {
+            load_stage(st_l, ld_si, ld_k);
+            ld_next();
+        }
         cp_async_commit();
-        const auto X = S.x[i % STAGES];
+        st_l = st_l + 1 == STAGES ? 0 : st_l + 1;
+        const auto X = S.x[st_c];
+        st_c = st_c + 1 == STAGES ? 0 : st_c + 1;
 #pragma unroll
         for (int kk = 0; kk < KT; kk += 4) Roles::mma(warp, X, kk, fr, fk, acc);
-        const int64_t item = it0 + i;
-        if (i + 1 == nitems || (item + 1) % part.T == 0) {
+        const bool seg_end = i + 1 == nitems || c_k == T - 1;
+        const int64_t slot = slot0 + c_si;
+        if (++c_k == T) {
+            c_k = 0;
+            ++c_si;
+        }
+        if (seg_end) {
             // flush this slot segment's partial (upper tiles only)
-            const int64_t slot = item / part.T;
             const int64_t seg = cta - part.first_cta(slot);
             double *out = Apart + (slot * maxseg + seg) * (B2 * B2);
 #pragma unroll
