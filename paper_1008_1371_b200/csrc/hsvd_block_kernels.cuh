@@ -90,7 +90,11 @@ struct GramRoles;
 
 template <>
 struct GramRoles<64> {
-    static constexpr int NACC = 6;  // accumulator tiles per warp (max)
+    // 36 upper 8x8 tiles over 8 warps, 9 per SM sub-partition (warps w and
+    // w + 4) and at most 5 per warp: warps 0-5 own one off-diagonal 16x16
+    // super-tile (4 tiles); warps 4 and 5 add one diagonal tile each, (1,1)
+    // and (3,3); warps 6 and 7 own the remaining 10 diagonal-block tiles.
+    static constexpr int NACC = 5;  // accumulator tiles per warp (max)
     __device__ static void mma(int warp, const double (*X)[GramSmem<64, 32, 4>::LD], int kk,
                                int fr, int fk, double (&acc)[NACC][2])
     {
@@ -103,16 +107,21 @@ struct GramRoles<64> {
             dmma(acc[1][0], acc[1][1], a0, b1);
             dmma(acc[2][0], acc[2][1], a1, b0);
             dmma(acc[3][0], acc[3][1], a1, b1);
+            if (warp >= 4) {  // tile (1,1) (warp 4) or (3,3) (warp 5)
+                const double e = X[8 * (2 * warp - 7) + fr][kk + fk];
+                dmma(acc[4][0], acc[4][1], e, e);
+            }
         } else {
-            const int D0 = 2 * (warp - 6), D1 = D0 + 1;
-            const double f0 = X[16 * D0 + fr][kk + fk], f1 = X[16 * D0 + 8 + fr][kk + fk];
-            const double g0 = X[16 * D1 + fr][kk + fk], g1 = X[16 * D1 + 8 + fr][kk + fk];
+            // warp 6: (0,0) (0,1) (4,4) (4,5) (5,5); warp 7: (2,2) (2,3) (6,6) (6,7) (7,7)
+            const int d = warp - 6;  // diagonal super-tiles d and d + 2
+            const double f0 = X[16 * d + fr][kk + fk], f1 = X[16 * d + 8 + fr][kk + fk];
+            const double g0 = X[16 * (d + 2) + fr][kk + fk];
+            const double g1 = X[16 * (d + 2) + 8 + fr][kk + fk];
             dmma(acc[0][0], acc[0][1], f0, f0);
             dmma(acc[1][0], acc[1][1], f0, f1);
-            dmma(acc[2][0], acc[2][1], f1, f1);
-            dmma(acc[3][0], acc[3][1], g0, g0);
-            dmma(acc[4][0], acc[4][1], g0, g1);
-            dmma(acc[5][0], acc[5][1], g1, g1);
+            dmma(acc[2][0], acc[2][1], g0, g0);
+            dmma(acc[3][0], acc[3][1], g0, g1);
+            dmma(acc[4][0], acc[4][1], g1, g1);
         }
     }
     // (row-tile, col-tile) of accumulator q of this warp; -1 if unused
@@ -122,12 +131,19 @@ struct GramRoles<64> {
         if (warp < 6) {
             const int R = warp < 3 ? 0 : (warp < 5 ? 1 : 2);
             const int C = warp < 3 ? warp + 1 : (warp < 5 ? warp - 1 : 3);
-            if (q < 4) { rt = 2 * R + (q >> 1); ct = 2 * C + (q & 1); }
+            if (q < 4) {
+                rt = 2 * R + (q >> 1);
+                ct = 2 * C + (q & 1);
+            } else if (warp >= 4) {
+                rt = ct = 2 * warp - 7;  // 1 or 3
+            }
         } else {
-            const int D = 2 * (warp - 6) + (q >= 3 ? 1 : 0);
-            const int qq = q % 3;
-            rt = 2 * D + (qq == 2 ? 1 : 0);
-            ct = 2 * D + (qq == 0 ? 0 : 1);
+            const int d = warp - 6;
+            if (q == 0) { rt = 2 * d; ct = 2 * d; }
+            else if (q == 1) { rt = 2 * d; ct = 2 * d + 1; }
+            else if (q == 2) { rt = ct = 2 * (d + 2); }
+            else if (q == 3) { rt = 2 * (d + 2); ct = 2 * (d + 2) + 1; }
+            else { rt = ct = 2 * (d + 2) + 1; }
         }
     }
 };
