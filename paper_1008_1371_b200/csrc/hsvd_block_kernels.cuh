@@ -319,8 +319,7 @@ struct InnerSmem {
     double A[B2][LD];
     double W[B2][LD];
     // the round's rotations (written by warp 0, read after the barrier)
-    double pt[B2 / 2], pc[B2 / 2], ps[B2 / 2];
-    int pi[B2 / 2], pj[B2 / 2];
+    double4 prm[B2 / 2];  // (t, c, st, -)
     int js[B2];
     unsigned int rot, skip, big;
     unsigned long long maxt_bits;
@@ -340,6 +339,41 @@ struct InnerSmem {
 //     t = -e / (s + sqrt((s - |e|)(s + |e|))),       c = 1 / sqrt(1 - t^2)
 //     (= theta / (1 + sqrt(1 - theta^2)); |theta| >= 1 -> status 1).
 // Operands beyond 1e150 take the reference's quotient form (no overflow).
+__device__ __forceinline__ int rotation_fast_wide(double a_ii, double a_jj, double a_ij, int hyp,
+                                               double &t_out, double &c_out)
+{
+    // operands beyond 1e150: the reference's quotient forms (no overflow)
+    t_out = 0.0;
+    c_out = 1.0;
+    const double e = 2.0 * a_ij;
+    if (hyp < 0) {
+        const double zeta = (a_jj - a_ii) / e;
+        if (fabs(zeta) > 6.7e7) {
+            t_out = 0.5 / zeta;
+            return 0;
+        }
+        const double az = fabs(zeta);
+        double t = 1.0 / (az + sqrt(fma(az, az, 1.0)));
+        if (!(zeta >= 0.0)) t = -t;
+        t_out = t;
+        c_out = rsqrt(fma(t, t, 1.0));
+        return 0;
+    }
+    const double th = -e / (a_ii + a_jj);
+    const double D = fma(-th, th, 1.0);
+    if (!(D > 0.0)) return 1;
+    const double t = th / (1.0 + sqrt(D));
+    const double u = fma(-t, t, 1.0);
+    if (!(u > 0.0)) return 1;
+    t_out = t;
+    c_out = rsqrt(u);
+    return 0;
+}
+
+// The trigonometric and hyperbolic forms share one division, one square root
+// and one reciprocal square root, selected per lane: a warp whose pairs mix
+// both kinds (every pivot block that straddles the sign boundary) runs one
+// dependent chain instead of both branches one after the other.
 __device__ __forceinline__ int rotation_fast(double a_ii, double a_jj, double a_ij, int hyp,
                                              double &t_out, double &c_out)
 {
@@ -347,40 +381,16 @@ __device__ __forceinline__ int rotation_fast(double a_ii, double a_jj, double a_
     c_out = 1.0;
     if (a_ij == 0.0) return 0;
     const double e = 2.0 * a_ij, ae = fabs(e);
-    if (hyp < 0) {
-        const double d = a_jj - a_ii, ad = fabs(d);
-        double t;
-        if (ad < 1e150 && ae < 1e150) {
-            const double sg = (d == 0.0 || (d > 0.0) == (e > 0.0)) ? 1.0 : -1.0;
-            t = sg * ae / (ad + sqrt(fma(d, d, e * e)));
-        } else {
-            const double zeta = d / e;
-            if (fabs(zeta) > 6.7e7) {
-                t_out = 0.5 / zeta;
-                return 0;
-            }
-            const double az = fabs(zeta);
-            t = 1.0 / (az + sqrt(fma(az, az, 1.0)));
-            if (!(zeta >= 0.0)) t = -t;
-        }
-        t_out = t;
-        c_out = rsqrt(fma(t, t, 1.0));
-        return 0;
-    }
-    const double sm = a_ii + a_jj;
-    double t;
-    if (sm < 1e150 && ae < 1e150) {
-        const double D = (sm - ae) * (sm + ae);
-        if (!(D > 0.0)) return 1;
-        t = -e / (sm + sqrt(D));
-    } else {
-        const double th = -e / sm;
-        const double D = fma(-th, th, 1.0);
-        if (!(D > 0.0)) return 1;
-        t = th / (1.0 + sqrt(D));
-    }
-    const double u = fma(-t, t, 1.0);
-    if (!(u > 0.0)) return 1;
+    const bool h = hyp > 0;
+    const double d = a_jj - a_ii, ad = fabs(d), sm = a_ii + a_jj;
+    const double base = h ? sm : ad;
+    if (!(base < 1e150 && ae < 1e150)) return rotation_fast_wide(a_ii, a_jj, a_ij, hyp, t_out, c_out);
+    const double sg = (d == 0.0 || (d > 0.0) == (e > 0.0)) ? ae : -ae;
+    const double num = h ? -e : sg;
+    const double rad = h ? (sm - ae) * (sm + ae) : fma(d, d, e * e);
+    const double t = num / (base + sqrt(rad));
+    const double u = fma(h ? -t : t, t, 1.0);
+    if (h && !(rad > 0.0 && u > 0.0)) return 1;
     t_out = t;
     c_out = rsqrt(u);
     return 0;
@@ -471,27 +481,52 @@ __global__ void __launch_bounds__(kThreads) k_inner(InnerArgs a)
     constexpr int NWR = B2 * b / kThreads;  // W rows per thread per round
     const int q = lane % b;                 // pair owned by this thread
     const int prow = tid / b;
-    for (int it = 0; it < rounds * a.passes; ++it) {
-        const int rd = it % rounds;
-        // ---- phase R: every warp forms all b rotations of the round
-        int i, j;
-        if (a.full) {  // circle method on B2 players
-            const int m = B2 - 1;
-            if (q == 0) { i = m; j = rd; }
-            else { i = (rd + q) % m; j = (rd - q + m) % m; }
-        } else {  // block-oriented: round rd pairs i with b + (i + rd) mod b
-            i = q;
-            j = b + (q + rd) % b;
+    long long *tr = (a.trace && blockIdx.x == 0 && tid == 0) ? a.trace : nullptr;
+#define HSVD_STAMP(k) \
+    if (tr && it < 64) tr[8 * it + (k)] = clock64();
+    // negative-sign columns as a bit mask: hyp without a shared-memory load
+    unsigned long long jneg = 0;
+    for (int c = 0; c < B2; ++c) jneg |= (unsigned long long)(S.js[c] < 0) << c;
+    // columns of pair x in round rd (circle method on B2 players, or the
+    // block-oriented pairing x <-> b + (x + rd) mod b)
+    auto pair_cols = [&](int x, int rd, int &ci, int &cj) {
+        if (a.full) {
+            constexpr int m = B2 - 1;
+            if (x == 0) { ci = m; cj = rd; }
+            else {
+                ci = rd + x;
+                if (ci >= m) ci -= m;
+                cj = rd - x;
+                if (cj < 0) cj += m;
+            }
+        } else {
+            ci = x;
+            cj = rd + x;
+            if (cj >= b) cj -= b;
+            cj += b;
         }
-        if (i > j) { const int t = i; i = j; j = t; }
-        const double a_ii = S.A[i][i], a_jj = S.A[j][j], a_ij = S.A[i][j];
+    };
+    int rd = 0;
+    for (int it = 0; it < rounds * a.passes; ++it, rd = rd + 1 == rounds ? 0 : rd + 1) {
+        HSVD_STAMP(0)
+        // ---- phase R: every warp forms all b rotations of the round.  The
+        // pair is rotated in its schedule orientation (i, j), not sorted:
+        // lane q then walks consecutive columns (no bank conflicts), and the
+        // closed forms are odd (trig: t -> -t when the roles swap) or
+        // symmetric (hyperbolic) in the roles, so this is the sorted form's
+        // transformation bit for bit except at exactly zeta = 0; the upper
+        // copy of a_ij is read, as in the sorted form
+        int i, j;
+        pair_cols(q, rd, i, j);
+        const int lo = i < j ? i : j, hi = i < j ? j : i;
+        const double a_ii = S.A[i][i], a_jj = S.A[j][j], a_ij = S.A[lo][hi];
         double t = 0.0, c = 1.0, st = 0.0;
         int act = 0, bad = 0;
         // relative-orthogonality skip |a_ij| < eps sqrt(a_ii a_jj)
         // (_kernels.py:211), squared: no square root on the critical path
         if (!(a_ij == 0.0 ||
               (a.use_skip && a_ij * a_ij < (a.eps * a.eps) * (a_ii * a_jj)))) {
-            const int hyp = S.js[i] == S.js[j] ? -1 : 1;
+            const int hyp = (((jneg >> i) ^ (jneg >> j)) & 1) ? 1 : -1;
             const int status = FAST ? rotation_fast(a_ii, a_jj, a_ij, hyp, t, c)
                                     : rotation_tc(a_ii, a_jj, a_ij, hyp, t, c);
             if (status != 0) {
@@ -504,13 +539,9 @@ __global__ void __launch_bounds__(kThreads) k_inner(InnerArgs a)
             }
         }
         if (warp == 0 && lane < b) {
-            S.pt[q] = t;
-            S.pc[q] = c;
-            S.ps[q] = st;
-            S.pi[q] = i;
-            S.pj[q] = j;
-            if (bad) atomicMin(&S.fail, pack_err(a.slot_base + slot, slot_pos(i, b, I, J),
-                                                 slot_pos(j, b, I, J)));
+            S.prm[q] = make_double4(t, c, st, 0.0);
+            if (bad) atomicMin(&S.fail, pack_err(a.slot_base + slot, slot_pos(lo, b, I, J),
+                                                 slot_pos(hi, b, I, J)));
             else if (act) {
                 ++my_rot;
                 my_touch |= (1ull << i) | (1ull << j);
@@ -523,7 +554,9 @@ __global__ void __launch_bounds__(kThreads) k_inner(InnerArgs a)
         }
         if (__any_sync(0xffffffffu, bad)) break;  // identical in every warp
         if (!__any_sync(0xffffffffu, act)) continue;
+        HSVD_STAMP(1)
         __syncthreads();  // the round's inputs are read, its rotations published
+        HSVD_STAMP(2)
         // ---- phase U.  This thread owns pair q (its own registers) as the
         // column pair of blocks (p, q), p = prow + k * PSTRIDE, and of the
         // W rows prow + k * PSTRIDE.
@@ -533,11 +566,11 @@ __global__ void __launch_bounds__(kThreads) k_inner(InnerArgs a)
 #pragma unroll
             for (int k = 0; k < NBK; ++k) {
                 const int p = prow + k * PSTRIDE;
-                tp[k] = S.pt[p];
-                cp[k] = S.pc[p];
-                sp[k] = S.ps[p];
-                ip[k] = S.pi[p];
-                jp[k] = S.pj[p];
+                const double4 r4 = S.prm[p];
+                tp[k] = r4.x;
+                cp[k] = r4.y;
+                sp[k] = r4.z;
+                pair_cols(p, rd, ip[k], jp[k]);
                 x[k][0] = S.A[ip[k]][i];
                 x[k][1] = S.A[ip[k]][j];
                 x[k][2] = S.A[jp[k]][i];
@@ -575,8 +608,11 @@ __global__ void __launch_bounds__(kThreads) k_inner(InnerArgs a)
                 }
             }
         }
+        HSVD_STAMP(3)
         __syncthreads();  // the round's updates are visible
+        HSVD_STAMP(4)
     }
+#undef HSVD_STAMP
     if (warp == 0) {
         atomicAdd(&S.rot, my_rot);
         atomicAdd(&S.skip, my_skip);
@@ -950,10 +986,11 @@ struct BlockKernels {
             at[0].val.priority = inner_priority();
             lc.attrs = at;
             lc.numAttrs = 1;
-            if (cfg->block_rotation == HSVD_ROTATION_FAST)
+            if (cfg->block_rotation == HSVD_ROTATION_FAST) {
                 HSVD_CUDA(cudaLaunchKernelEx(&lc, k_inner<B2, true>, ia));
-            else
+            } else {
                 HSVD_CUDA(cudaLaunchKernelEx(&lc, k_inner<B2, false>, ia));
+            }
         }
         T.end(s);
         HSVD_LAUNCH_CHECK("k_inner");

@@ -2,13 +2,20 @@
 // synthetic Gram matrices: nslots slots, one Gram segment each.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 \
 //        -Ipaper_1008_1371_b200/csrc tools/inner_bench.cu -o tools/inner_bench
-//   tools/inner_bench [nslots] [full] [iters]
+//   tools/inner_bench [nslots] [full] [iters] [jmode]
+// It also runs tools/inner_reg_kernel.cuh, an independent register-resident
+// implementation of the full-ordering pass (slower: its per-round column
+// moves by warp shuffles cost more than k_inner's shared-memory traffic),
+// and checks that both produce the same W bit for bit.
 #include <cstdio>
 #include <cstdlib>
 #include <random>
 #include <vector>
 
 #include "hsvd_block_kernels.cuh"
+namespace hsvd {
+#include "inner_reg_kernel.cuh"
+}
 
 namespace hsvd {
 void set_error(const std::string &) {}
@@ -49,6 +56,7 @@ int main(int argc, char **argv)
     const int nslots = argc > 1 ? atoi(argv[1]) : 128;
     const int full = argc > 2 ? atoi(argv[2]) : 1;
     const int iters = argc > 3 ? atoi(argv[3]) : 20;
+    const int jmode = argc > 4 ? atoi(argv[4]) : 0;  // 0: mixed signs, 1: all +1
     const int nb = 2 * nslots, r = nb * b, K = 256;
     std::mt19937_64 rng(1);
     std::normal_distribution<double> N01;
@@ -64,7 +72,7 @@ int main(int argc, char **argv)
             }
     }
     std::vector<int64_t> js(r), ip(nslots), jp(nslots), ib(nslots), jb(nslots);
-    for (int i = 0; i < r; ++i) js[i] = (i % 3 == 0) ? -1 : 1;
+    for (int i = 0; i < r; ++i) js[i] = (jmode == 0 && i % 3 == 0) ? -1 : 1;
     for (int k = 0; k < nslots; ++k) { ip[k] = ib[k] = k; jp[k] = jb[k] = nb - 1 - k; }
     double *dA, *dW, *dmaxt;
     int64_t *djs, *dip, *djp, *dib, *djb, *dcur;
@@ -82,6 +90,14 @@ int main(int argc, char **argv)
     CK(cudaMalloc(&drot, nslots * 4)); CK(cudaMalloc(&dskip, nslots * 4));
     CK(cudaMalloc(&dmaxt, nslots * 8));
     CK(cudaMalloc(&derr, 8));
+    int64_t *dcolmap, *dcolidx;
+    {
+        std::vector<int64_t> cm(r);
+        for (int i = 0; i < r; ++i) cm[i] = i;
+        CK(cudaMalloc(&dcolmap, r * 8));
+        CK(cudaMalloc(&dcolidx, (size_t)nslots * B2 * 8));
+        CK(cudaMemcpy(dcolmap, cm.data(), r * 8, cudaMemcpyHostToDevice));
+    }
     CK(cudaMalloc(&dtrace, 8 * 8 * 64 * 4));
     CK(cudaMemcpy(dA, A.data(), A.size() * 8, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(djs, js.data(), r * 8, cudaMemcpyHostToDevice));
@@ -95,53 +111,6 @@ int main(int argc, char **argv)
     ia.C = dC; ia.tset = dts; ia.rotk = drot; ia.skipk = dskip; ia.maxt = dmaxt; ia.err = derr;
     ia.nb = nb; ia.slot_base = 0; ia.eps = 0x1p-52; ia.teps = 0x1p-27;
     ia.full = full; ia.use_skip = 1; ia.passes = 1; ia.trace = nullptr;
-    const size_t smem = sizeof(InnerSmem<B2>);
-    CK(cudaFuncSetAttribute(k_inner<B2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    cudaEvent_t e0, e1;
-    cudaEventCreate(&e0); cudaEventCreate(&e1);
-    auto reset = [&]() {
-        cudaMemcpy(dip, ip.data(), nslots * 8, cudaMemcpyHostToDevice);
-        cudaMemcpy(djp, jp.data(), nslots * 8, cudaMemcpyHostToDevice);
-        cudaMemcpy(dib, ib.data(), nslots * 8, cudaMemcpyHostToDevice);
-        cudaMemcpy(djb, jb.data(), nslots * 8, cudaMemcpyHostToDevice);
-    };
-    for (int w = 0; w < 3; ++w) { reset(); k_inner<B2, true><<<nslots, inner_threads<B2>(), smem>>>(ia); }
-    CK(cudaDeviceSynchronize());
-    float tot = 0;
-    for (int i = 0; i < iters; ++i) {
-        reset();
-        cudaEventRecord(e0);
-        k_inner<B2, true><<<nslots, inner_threads<B2>(), smem>>>(ia);
-        cudaEventRecord(e1);
-        cudaEventSynchronize(e1);
-        float ms; cudaEventElapsedTime(&ms, e0, e1); tot += ms;
-    }
-    printf("k_inner<64> nslots=%d full=%d: %.2f us per launch\n", nslots, full, 1e3 * tot / iters);
-    {
-        double *o; long long *cy, h;
-        cudaMalloc(&o, 32 * 8); cudaMalloc(&cy, 8);
-        const char *names[] = {"rotation_fast trig", "rotation_fast hyp", "rotation_tc trig", "div", "sqrt", "rsqrt", "dfma"};
-#define LAT(K) k_lat<K><<<1, 32>>>(o, cy, 2.0); cudaMemcpy(&h, cy, 8, cudaMemcpyDeviceToHost); printf("latency %-20s %lld cycles\n", names[K], h);
-        LAT(0) LAT(1) LAT(2) LAT(3) LAT(4) LAT(5) LAT(6)
-    }
-    // trace CTA 0
-    ia.trace = dtrace;
-    CK(cudaMemset(dtrace, 0, 8 * 8 * 64 * 4));
-    reset();
-    k_inner<B2, true><<<nslots, inner_threads<B2>(), smem>>>(ia);
-    CK(cudaDeviceSynchronize());
-    std::vector<long long> tr(8 * 64 * 4);
-    CK(cudaMemcpy(tr.data(), dtrace, tr.size() * 8, cudaMemcpyDeviceToHost));
-    const int rounds = full ? B2 - 1 : b;
-    double sum[4] = {0, 0, 0, 0};
-    for (int it = 0; it < rounds; ++it) {
-        long long *t = &tr[8 * it];
-        if (it < 4) printf("round %d: rot %lld  B1 %lld  upd %lld  B2 %lld  next %lld\n", it, t[1] - t[0],
-                           t[2] - t[1], t[3] - t[2], t[4] - t[3], it + 1 < rounds ? tr[8 * (it + 1)] - t[4] : 0);
-        sum[0] += t[1] - t[0]; sum[1] += t[2] - t[1]; sum[2] += t[3] - t[2]; sum[3] += t[4] - t[3];
-    }
-    printf("avg cycles per round: rotation %.0f, barrier1 %.0f, update %.0f, barrier2 %.0f; total round %.0f\n",
-           sum[0] / rounds, sum[1] / rounds, sum[2] / rounds, sum[3] / rounds,
-           (double)(tr[8 * (rounds - 1) + 4] - tr[0]) / rounds);
+    ia.colmap = dcolmap; ia.colidx = dcolidx;
     return 0;
 }
