@@ -112,5 +112,87 @@ int main(int argc, char **argv)
     ia.nb = nb; ia.slot_base = 0; ia.eps = 0x1p-52; ia.teps = 0x1p-27;
     ia.full = full; ia.use_skip = 1; ia.passes = 1; ia.trace = nullptr;
     ia.colmap = dcolmap; ia.colidx = dcolidx;
+    const size_t smem = sizeof(InnerSmem<B2>), smem_reg = sizeof(InnerRegSmem);
+    CK(cudaFuncSetAttribute(k_inner<B2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(cudaFuncSetAttribute(k_inner_reg<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_reg));
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0); cudaEventCreate(&e1);
+    auto reset = [&]() {
+        cudaMemcpy(dip, ip.data(), nslots * 8, cudaMemcpyHostToDevice);
+        cudaMemcpy(djp, jp.data(), nslots * 8, cudaMemcpyHostToDevice);
+        cudaMemcpy(dib, ib.data(), nslots * 8, cudaMemcpyHostToDevice);
+        cudaMemcpy(djb, jb.data(), nslots * 8, cudaMemcpyHostToDevice);
+        cudaMemset(drot, 0, nslots * 4);
+        cudaMemset(dskip, 0, nslots * 4);
+        cudaMemset(dW, 0, A.size() * 8);
+    };
+    auto launch = [&](int kind) {
+        if (kind == 0) k_inner<B2, true><<<nslots, inner_threads<B2>(), smem>>>(ia);
+        else k_inner_reg<true><<<nslots, kThreads, smem_reg>>>(ia);
+    };
+    const int rounds = full ? B2 - 1 : b;
+    std::vector<double> Wk[2];
+    std::vector<uint32_t> rotk[2];
+    std::vector<uint8_t> tsk[2];
+    for (int kind = 0; kind < (full ? 2 : 1); ++kind) {
+        ia.trace = nullptr;
+        for (int w = 0; w < 3; ++w) { reset(); launch(kind); }
+        CK(cudaDeviceSynchronize());
+        float tot = 0;
+        for (int i = 0; i < iters; ++i) {
+            reset();
+            cudaEventRecord(e0);
+            launch(kind);
+            cudaEventRecord(e1);
+            cudaEventSynchronize(e1);
+            float ms; cudaEventElapsedTime(&ms, e0, e1); tot += ms;
+        }
+        printf("%s nslots=%d full=%d jmode=%d: %.2f us per launch\n", kind ? "k_inner_reg" : "k_inner<64>",
+               nslots, full, jmode, 1e3 * tot / iters);
+        Wk[kind].resize(A.size());
+        rotk[kind].resize(nslots);
+        tsk[kind].resize((size_t)nslots * kTsetStride);
+        CK(cudaMemcpy(Wk[kind].data(), dW, A.size() * 8, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(rotk[kind].data(), drot, nslots * 4, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(tsk[kind].data(), dts, tsk[kind].size(), cudaMemcpyDeviceToHost));
+        // trace CTA 0: clock64 stamps per round (phase boundaries of each kernel)
+        ia.trace = dtrace;
+        CK(cudaMemset(dtrace, 0, 8 * 8 * 64 * 4));
+        reset();
+        launch(kind);
+        CK(cudaDeviceSynchronize());
+        ia.trace = nullptr;
+        std::vector<long long> tr(8 * 64 * 4);
+        CK(cudaMemcpy(tr.data(), dtrace, tr.size() * 8, cudaMemcpyDeviceToHost));
+        double sum[4] = {0, 0, 0, 0};
+        for (int it = 0; it < rounds; ++it) {
+            long long *t = &tr[8 * it];
+            sum[0] += t[1] - t[0]; sum[1] += t[2] - t[1]; sum[2] += t[3] - t[2]; sum[3] += t[4] - t[3];
+        }
+        printf("  avg cycles per round: phases %.0f / %.0f / %.0f / %.0f; total round %.0f\n",
+               sum[0] / rounds, sum[1] / rounds, sum[2] / rounds, sum[3] / rounds,
+               (double)(tr[8 * (rounds - 1) + 4] - tr[0]) / rounds);
+    }
+    if (full) {
+        size_t diff = 0;
+        double maxd = 0;
+        for (size_t e = 0; e < A.size(); ++e)
+            if (Wk[0][e] != Wk[1][e]) {
+                ++diff;
+                maxd = fmax(maxd, fabs(Wk[0][e] - Wk[1][e]));
+            }
+        size_t rdiff = 0, tdiff = 0;
+        for (int k = 0; k < nslots; ++k) rdiff += rotk[0][k] != rotk[1][k];
+        for (size_t e = 0; e < tsk[0].size(); ++e) tdiff += tsk[0][e] != tsk[1][e];
+        printf("reg vs smem kernel: W entries differing %zu of %zu (max |diff| %.3e), rot counts differing %zu, tset bytes differing %zu\n",
+               diff, A.size(), maxd, rdiff, tdiff);
+    }
+    {
+        double *o; long long *cy, h;
+        cudaMalloc(&o, 32 * 8); cudaMalloc(&cy, 8);
+        const char *names[] = {"rotation_fast trig", "rotation_fast hyp", "rotation_tc trig", "div", "sqrt", "rsqrt", "dfma"};
+#define LAT(K) k_lat<K><<<1, 32>>>(o, cy, 2.0); cudaMemcpy(&h, cy, 8, cudaMemcpyDeviceToHost); printf("latency %-20s %lld cycles\n", names[K], h);
+        LAT(0) LAT(1) LAT(2) LAT(3) LAT(4) LAT(5) LAT(6)
+    }
     return 0;
 }
