@@ -36,6 +36,9 @@ __device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b)
 }
 
 constexpr int kThreads = 256;
+#ifndef HSVD_INNER_THREADS
+#define HSVD_INNER_THREADS 256
+#endif
 
 // position of column c (0..2b) of slot P = (I, J), I < J
 __device__ __forceinline__ int64_t slot_pos(int c, int b, int64_t I, int64_t J)
@@ -319,7 +322,8 @@ struct InnerSmem {
     double A[B2][LD];
     double W[B2][LD];
     // the round's rotations (written by warp 0, read after the barrier)
-    double4 prm[B2 / 2];  // (t, c, st, -)
+    double4 prm[2][B2 / 2];  // (t, c, st, -) of the round, by round parity
+    int flag[2];             // bit 0: some pair rotated, bit 1: a pair failed
     int js[B2];
     unsigned int rot, skip, big;
     unsigned long long maxt_bits;
@@ -407,12 +411,14 @@ __device__ __forceinline__ int rotation_fast(double a_ii, double a_jj, double a_
 // then updates its share of the blocks and of W from registers and shuffles:
 // two barriers per active round, none per inactive round.
 // threads of one k_inner CTA
+constexpr int kInnerThreads = HSVD_INNER_THREADS;
 template <int B2>
-constexpr int inner_threads() { return kThreads; }
+__host__ __device__ constexpr int inner_threads() { return B2 == 64 ? kInnerThreads : 256; }
 
 template <int B2, bool FAST>
-__global__ void __launch_bounds__(kThreads) k_inner(InnerArgs a)
+__global__ void __launch_bounds__(inner_threads<B2>()) k_inner(InnerArgs a)
 {
+    constexpr int NT = inner_threads<B2>();
     extern __shared__ __align__(16) unsigned char ism_raw[];
     auto &S = *reinterpret_cast<InnerSmem<B2> *>(ism_raw);
     if (*(volatile unsigned long long *)a.err != kNoError) return;
@@ -426,10 +432,10 @@ __global__ void __launch_bounds__(kThreads) k_inner(InnerArgs a)
     // segments are issued before the sums
     const double *P0 = a.Apart + (int64_t)slot * a.maxseg * (B2 * B2);
     const int nseg = (int)a.part.nseg(slot);
-    constexpr int PER = B2 * B2 / kThreads;
+    constexpr int PER = B2 * B2 / NT;
 #pragma unroll
     for (int k = 0; k < PER; ++k) {
-        const int e = tid + k * kThreads, i = e / B2, j = e % B2;
+        const int e = tid + k * NT, i = e / B2, j = e % B2;
         S.W[i][j] = i == j ? 1.0 : 0.0;
     }
     {
@@ -443,7 +449,7 @@ __global__ void __launch_bounds__(kThreads) k_inner(InnerArgs a)
             for (int u = 0; u < BATCH; ++u)
 #pragma unroll
                 for (int k = 0; k < PER; ++k) {
-                    const int e = tid + k * kThreads;
+                    const int e = tid + k * NT;
                     x[u][k] = (s0 + u < nseg && e / B2 <= e % B2)
                                   ? P0[(int64_t)(s0 + u) * B2 * B2 + e] : 0.0;
                 }
@@ -455,7 +461,7 @@ __global__ void __launch_bounds__(kThreads) k_inner(InnerArgs a)
         }
 #pragma unroll
         for (int k = 0; k < PER; ++k) {
-            const int e = tid + k * kThreads, i = e / B2, j = e % B2;
+            const int e = tid + k * NT, i = e / B2, j = e % B2;
             if (i <= j) {
                 S.A[i][j] = v[k];
                 S.A[j][i] = v[k];
@@ -476,9 +482,8 @@ __global__ void __launch_bounds__(kThreads) k_inner(InnerArgs a)
     unsigned long long my_touch = 0;
     double my_max = 0.0;
     static_assert(b == 16 || b == 32, "k_inner: b must be 16 or 32");
-    constexpr int PSTRIDE = kThreads / b;   // row-pair stride of phase U
-    constexpr int NBK = b * b / kThreads;   // A blocks per thread per round
-    constexpr int NWR = B2 * b / kThreads;  // W rows per thread per round
+    constexpr int PSTRIDE = NT / b;   // row-pair stride of phase U
+    constexpr int NBK = b * b / NT;   // A blocks per thread per round
     const int q = lane % b;                 // pair owned by this thread
     const int prow = tid / b;
     long long *tr = (a.trace && blockIdx.x == 0 && tid == 0) ? a.trace : nullptr;
@@ -506,67 +511,115 @@ __global__ void __launch_bounds__(kThreads) k_inner(InnerArgs a)
             cj += b;
         }
     };
-    int rd = 0;
+    // W <- W R of round wrd (parameters prm[wpar]) on the W worker rows:
+    // warps 1-3 and 5-7 (every SM sub-partition but warp 0's), pair q =
+    // lane % b, rows g, g + WG, ...
+    constexpr int NWW = (NT / 32) * 3 / 4;  // W worker warps
+    constexpr int WG = NWW * 32 / b;
+    const int wwarp = (warp & 3) - 1 + 3 * (warp >> 2);  // 0..5 unless warp % 4 == 0
+    const int wg = lane / b + (32 / b) * wwarp;
+    auto w_update = [&](int wrd, int wpar) {
+        const double4 r4 = S.prm[wpar][q];
+        const double tw = r4.x, cw = r4.y, sw = r4.z;
+        if (tw == 0.0) return;
+        int wi, wj;
+        pair_cols(q, wrd, wi, wj);
+        constexpr int NR = (B2 + WG - 1) / WG;
+        double wx[NR], wy[NR];
+#pragma unroll
+        for (int k = 0; k < NR; ++k) {
+            const int row = wg + k * WG;
+            if (row < B2) {
+                wx[k] = S.W[row][wi];
+                wy[k] = S.W[row][wj];
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < NR; ++k) {
+            const int row = wg + k * WG;
+            if (row < B2) {
+                S.W[row][wi] = fma(sw, wy[k], wx[k]) * cw;
+                S.W[row][wj] = fma(tw, wx[k], wy[k]) * cw;
+            }
+        }
+    };
+    const bool w_worker = (warp & 3) != 0;
+    int rd = 0, prev_rd = 0;
+    bool prev_act = false, failed = false;
     for (int it = 0; it < rounds * a.passes; ++it, rd = rd + 1 == rounds ? 0 : rd + 1) {
         HSVD_STAMP(0)
-        // ---- phase R: every warp forms all b rotations of the round.  The
-        // pair is rotated in its schedule orientation (i, j), not sorted:
-        // lane q then walks consecutive columns (no bank conflicts), and the
-        // closed forms are odd (trig: t -> -t when the roles swap) or
-        // symmetric (hyperbolic) in the roles, so this is the sorted form's
-        // transformation bit for bit except at exactly zeta = 0; the upper
-        // copy of a_ij is read, as in the sorted form
-        int i, j;
-        pair_cols(q, rd, i, j);
-        const int lo = i < j ? i : j, hi = i < j ? j : i;
-        const double a_ii = S.A[i][i], a_jj = S.A[j][j], a_ij = S.A[lo][hi];
-        double t = 0.0, c = 1.0, st = 0.0;
-        int act = 0, bad = 0;
-        // relative-orthogonality skip |a_ij| < eps sqrt(a_ii a_jj)
-        // (_kernels.py:211), squared: no square root on the critical path
-        if (!(a_ij == 0.0 ||
-              (a.use_skip && a_ij * a_ij < (a.eps * a.eps) * (a_ii * a_jj)))) {
-            const int hyp = (((jneg >> i) ^ (jneg >> j)) & 1) ? 1 : -1;
-            const int status = FAST ? rotation_fast(a_ii, a_jj, a_ij, hyp, t, c)
-                                    : rotation_tc(a_ii, a_jj, a_ij, hyp, t, c);
-            if (status != 0) {
-                bad = 1;
-                t = 0.0;
-                c = 1.0;
-            } else {
-                act = 1;
-                st = hyp < 0 ? -t : t;
+        const int par = it & 1;
+        if (warp == 0) {
+            // ---- phase R: warp 0 forms the round's b rotations.  The pair
+            // is rotated in its schedule orientation (i, j), not sorted: lane
+            // q then walks consecutive columns (no bank conflicts), and the
+            // closed forms are odd (trig: t -> -t when the roles swap) or
+            // symmetric (hyperbolic) in the roles, so this is the sorted
+            // form's transformation bit for bit except at exactly zeta = 0;
+            // the upper copy of a_ij is read, as in the sorted form
+            int i, j;
+            pair_cols(q, rd, i, j);
+            const int lo = i < j ? i : j, hi = i < j ? j : i;
+            const double a_ii = S.A[i][i], a_jj = S.A[j][j], a_ij = S.A[lo][hi];
+            double t = 0.0, c = 1.0, st = 0.0;
+            int act = 0, bad = 0;
+            // relative-orthogonality skip |a_ij| < eps sqrt(a_ii a_jj)
+            // (_kernels.py:211), squared: no square root on the critical path
+            if (!(a_ij == 0.0 ||
+                  (a.use_skip && a_ij * a_ij < (a.eps * a.eps) * (a_ii * a_jj)))) {
+                const int hyp = (((jneg >> i) ^ (jneg >> j)) & 1) ? 1 : -1;
+                const int status = FAST ? rotation_fast(a_ii, a_jj, a_ij, hyp, t, c)
+                                        : rotation_tc(a_ii, a_jj, a_ij, hyp, t, c);
+                if (status != 0) {
+                    bad = 1;
+                    t = 0.0;
+                    c = 1.0;
+                } else {
+                    act = 1;
+                    st = hyp < 0 ? -t : t;
+                }
             }
-        }
-        if (warp == 0 && lane < b) {
-            S.prm[q] = make_double4(t, c, st, 0.0);
-            if (bad) atomicMin(&S.fail, pack_err(a.slot_base + slot, slot_pos(lo, b, I, J),
-                                                 slot_pos(hi, b, I, J)));
-            else if (act) {
-                ++my_rot;
-                my_touch |= (1ull << i) | (1ull << j);
-                const double at = fabs(t);
-                my_big |= at > a.teps;
-                my_max = fmax(my_max, at);
-            } else {
-                ++my_skip;
+            if (lane < b) {
+                S.prm[par][q] = make_double4(t, c, st, 0.0);
+                if (bad) atomicMin(&S.fail, pack_err(a.slot_base + slot, slot_pos(lo, b, I, J),
+                                                     slot_pos(hi, b, I, J)));
+                else if (act) {
+                    ++my_rot;
+                    my_touch |= (1ull << i) | (1ull << j);
+                    const double at = fabs(t);
+                    my_big |= at > a.teps;
+                    my_max = fmax(my_max, at);
+                } else {
+                    ++my_skip;
+                }
             }
+            const int f = (__any_sync(0xffffffffu, act) ? 1 : 0) | (__any_sync(0xffffffffu, bad) ? 2 : 0);
+            if (lane == 0) S.flag[par] = f;
+        } else if (w_worker && prev_act) {
+            // the previous round's W update runs beside this round's rotations
+            w_update(prev_rd, par ^ 1);
         }
-        if (__any_sync(0xffffffffu, bad)) break;  // identical in every warp
-        if (!__any_sync(0xffffffffu, act)) continue;
         HSVD_STAMP(1)
-        __syncthreads();  // the round's inputs are read, its rotations published
+        __syncthreads();  // the round's rotations are published
         HSVD_STAMP(2)
-        // ---- phase U.  This thread owns pair q (its own registers) as the
-        // column pair of blocks (p, q), p = prow + k * PSTRIDE, and of the
-        // W rows prow + k * PSTRIDE.
+        const int f = S.flag[par];
+        if (f & 2) { failed = true; break; }
+        prev_act = f & 1;
+        prev_rd = rd;
+        if (!prev_act) continue;
+        // ---- phase U (A only).  This thread owns pair q as the column pair
+        // of blocks (p, q), p = prow + k * PSTRIDE.
         {
+            int i, j;
+            pair_cols(q, rd, i, j);
+            const double4 rq = S.prm[par][q];
+            const double t = rq.x, c = rq.y, st = rq.z;
             double x[NBK][4], tp[NBK], cp[NBK], sp[NBK];
             int ip[NBK], jp[NBK];
 #pragma unroll
             for (int k = 0; k < NBK; ++k) {
                 const int p = prow + k * PSTRIDE;
-                const double4 r4 = S.prm[p];
+                const double4 r4 = S.prm[par][p];
                 tp[k] = r4.x;
                 cp[k] = r4.y;
                 sp[k] = r4.z;
@@ -594,24 +647,13 @@ __global__ void __launch_bounds__(kThreads) k_inner(InnerArgs a)
                     S.A[jp[k]][i] = fma(tp[k], y00, y10) * cp[k];
                 }
             }
-            if (t != 0.0) {  // W <- W R_q on this thread's rows
-                double wx[NWR], wy[NWR];
-#pragma unroll
-                for (int k = 0; k < NWR; ++k) {
-                    wx[k] = S.W[prow + k * PSTRIDE][i];
-                    wy[k] = S.W[prow + k * PSTRIDE][j];
-                }
-#pragma unroll
-                for (int k = 0; k < NWR; ++k) {
-                    S.W[prow + k * PSTRIDE][i] = fma(st, wy[k], wx[k]) * c;
-                    S.W[prow + k * PSTRIDE][j] = fma(t, wx[k], wy[k]) * c;
-                }
-            }
         }
         HSVD_STAMP(3)
         __syncthreads();  // the round's updates are visible
         HSVD_STAMP(4)
     }
+    // the last active round's W update
+    if (!failed && prev_act && w_worker) w_update(prev_rd, ((rounds * a.passes) - 1) & 1);
 #undef HSVD_STAMP
     if (warp == 0) {
         atomicAdd(&S.rot, my_rot);
@@ -629,7 +671,7 @@ __global__ void __launch_bounds__(kThreads) k_inner(InnerArgs a)
     if (tid < B2) a.colidx[(int64_t)slot * B2 + tid] = a.colmap[slot_pos(tid, b, I, J)];
     // W column-major: Wg[slot][c * B2 + k] = W[k][c]
     double *Wout = a.Wg + (int64_t)slot * B2 * B2;
-    for (int e = tid; e < B2 * B2; e += kThreads) Wout[e] = S.W[e % B2][e / B2];
+    for (int e = tid; e < B2 * B2; e += NT) Wout[e] = S.W[e % B2][e / B2];
     if (tid == 0) {
         // touched columns (W == I outside T x T; T empty: k_update skips)
         uint8_t *ts = a.tset + (int64_t)slot * kTsetStride;
@@ -978,7 +1020,7 @@ struct BlockKernels {
             // of a concurrent stream (split mode)
             cudaLaunchConfig_t lc = {};
             lc.gridDim = dim3((unsigned)nslots);
-            lc.blockDim = dim3(kThreads);
+            lc.blockDim = dim3(inner_threads<B2>());
             lc.dynamicSmemBytes = inner_smem();
             lc.stream = s;
             cudaLaunchAttribute at[1];

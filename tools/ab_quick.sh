@@ -5,7 +5,7 @@ python - <<'PY'
 import json
 try:
     d = json.loads(open('/tmp/b.json').read().strip().splitlines()[-1])
-    print(round(d['value'], 4), d.get('sweeps'), d['roofline'].get('kernel_ms_sweep0'))
+    print(round(d['value'], 4), d.get('sweeps'), d['roofline'].get('kernel_ms_sweep0'), [round(x, 1) for x in d.get('sweep_gpu_ms', [])])
 except Exception as e:
     print('bench parse failed', e)
 PY

@@ -128,7 +128,7 @@ int main(int argc, char **argv)
     };
     auto launch = [&](int kind) {
         if (kind == 0) k_inner<B2, true><<<nslots, inner_threads<B2>(), smem>>>(ia);
-        else k_inner_reg<true><<<nslots, kThreads, smem_reg>>>(ia);
+        else k_inner_reg<true><<<nslots, 256, smem_reg>>>(ia);
     };
     const int rounds = full ? B2 - 1 : b;
     std::vector<double> Wk[2];
