@@ -16,6 +16,7 @@
 #ifndef HSVD_B200_H
 #define HSVD_B200_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #if defined(__GNUC__)
@@ -33,6 +34,7 @@ extern "C" {
 #define HSVD_DEFINITENESS_LOST 1 /* DefinitenessLostError(block, i, j)   */
 #define HSVD_RANK_DEFICIENT 2    /* RankDeficiencyError (zero column)     */
 #define HSVD_SHAPE_ERROR 3       /* ShapeError                            */
+#define HSVD_NUMERICAL_SINGULARITY 4 /* NumericalSingularityError (factor)  */
 #define HSVD_ERR_CUDA (-1)
 #define HSVD_ERR_ARG (-2)
 #define HSVD_ERR_UNSUPPORTED (-3)
@@ -252,6 +254,22 @@ HSVD_API int hsvd_drive_sharded(void *comm, int32_t nshards, int32_t nlocal,
                                 double *const *lam_out, void *const *ws,
                                 const int64_t *ws_bytes, hsvd_result *res_host,
                                 hsvd_telemetry *tele_host);
+
+/* ---- eigen-pipeline front end (hjsvd.factory, factory.py:136-282) ------
+ * Complete-pivoting Bunch-Parlett factorization M = G J G^T in
+ * double-double, bit-identical to bunch_parlett_factor.  M (device, n x n,
+ * exactly symmetric, leading dimension ldm), G out (device, column-major,
+ * ldg; rows un-permuted, +1 columns first), signs out (device int8, +1
+ * first), perm out (device int64: the symmetric pivot permutation), *p_out
+ * (host) = number of +1 signs.  thresh = n * eps * ||M||_F (the reference's
+ * singularity threshold, computed by the caller).  Returns
+ * HSVD_NUMERICAL_SINGULARITY with *stage_out = the pivot stage when every
+ * remaining pivot candidate is <= thresh.  ws: device workspace of
+ * hsvd_bp_workspace_size bytes (4 n^2 doubles + O(n)). */
+HSVD_API int hsvd_bp_workspace_size(int64_t n, size_t *bytes);
+HSVD_API int hsvd_bp_factor(const double *M, int64_t n, int64_t ldm, double thresh, double *G,
+                            int64_t ldg, int8_t *signs, int64_t *perm, int64_t *p_out,
+                            int64_t *stage_out, void *ws, size_t ws_bytes, void *stream);
 
 /* The shard plan alone (host only, no GPU): the stepper of all slots, the
  * block placement and the per-step block moves, for tests of the exchange

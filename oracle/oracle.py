@@ -66,6 +66,8 @@ def lib():
         L.orc_sample_steps.restype = _i64
         L.orc_sample_steps.argtypes = [_p, _i64, _i64, _p, _i64, _i64, _i64,
                                        ctypes.c_int, ctypes.POINTER(_d)]
+        L.orc_bp_factor.restype = ctypes.c_int
+        L.orc_bp_factor.argtypes = [_p, _i64, _d, _p, _p, _p, _p, _p]
         _lib = L
     return _lib
 
@@ -173,3 +175,23 @@ def sample_steps(G, signs, p, steps, workers, accumulate_v=True):
     rot = int(lib().orc_sample_steps(_ptr(G), n, r, _ptr(signs), p, steps,
                                      workers, int(accumulate_v), ctypes.byref(el)))
     return rot, el.value
+
+
+def bp_factor(M):
+    """Bunch-Parlett factor of a symmetric M, bit-identical to
+    hjsvd.factory.bunch_parlett_factor (factory.py:270-282): returns
+    (G column-major, signs (+1 first), perm, p); raises ArithmeticError on a
+    numerical singularity."""
+    M = np.ascontiguousarray(M, dtype=np.float64)
+    n = M.shape[0]
+    thresh = n * EPS * np.linalg.norm(M, "fro")
+    G = np.zeros((n, n), order="F")
+    signs = np.zeros(n, np.int8)
+    perm = np.zeros(n, np.int64)
+    p = np.zeros(1, np.int64)
+    stage = np.zeros(1, np.int64)
+    st = lib().orc_bp_factor(_ptr(M), n, thresh, _ptr(G), _ptr(signs), _ptr(perm), _ptr(p),
+                             _ptr(stage))
+    if st == 3:
+        raise ArithmeticError(f"numerical singularity at stage {int(stage[0])}")
+    return G, signs, perm, int(p[0])

@@ -23,6 +23,16 @@ from .linalg import (
     fused_pair_update,
     orthonormality_distance,
 )
+from .factory import (
+    ALPHA,
+    GAP,
+    FactorPair,
+    SpectrumSpec,
+    bunch_parlett_factor,
+    bunch_parlett_factor_device,
+    draw_spectrum,
+    eigvalsh,
+)
 from .matio import read_csv_matrix, read_gjh, write_csv_matrix, write_gjh
 from .rotation import (
     CODE_BIG,

@@ -36,6 +36,7 @@ UNITS = {
     "hsvd_driver.cu": ["-fmad=false"],
     "hsvd_block.cu": [],
     "hsvd_sharded.cu": ["-I" + NCCL_INC],
+    "hsvd_factor.cu": ["-fmad=false"],
 }
 
 

@@ -5,7 +5,8 @@ CUDA device is present, every compute entry point raises."""
 import ctypes
 import os
 
-from .errors import (DefinitenessLostError, HsvdCudaError, RankDeficiencyError,
+from .errors import (DefinitenessLostError, HsvdCudaError, NumericalSingularityError,
+                     RankDeficiencyError,
                      ShapeError)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -15,6 +16,7 @@ HSVD_OK = 0
 HSVD_DEFINITENESS_LOST = 1
 HSVD_RANK_DEFICIENT = 2
 HSVD_SHAPE_ERROR = 3
+HSVD_NUMERICAL_SINGULARITY = 4
 HSVD_ERR_CUDA = -1
 HSVD_ERR_ARG = -2
 HSVD_ERR_UNSUPPORTED = -3
@@ -36,6 +38,7 @@ EXPORTED = (
     "hsvd_shard_columns", "hsvd_sharded_workspace_size", "hsvd_drive_sharded",
     "hsvd_plan_create", "hsvd_plan_destroy", "hsvd_plan_advance", "hsvd_plan_state",
     "hsvd_plan_redistribute", "hsvd_plan_place",
+    "hsvd_bp_workspace_size", "hsvd_bp_factor",
 )
 
 
@@ -135,6 +138,9 @@ _SIGS = {
     "hsvd_plan_state": (ctypes.c_int, [_P, _P, _P, _P, _P, _P]),
     "hsvd_plan_redistribute": (ctypes.c_int, [_P, _I32, _P, _P, _I64, _I32, _P, _P, _P, _P]),
     "hsvd_plan_place": (None, [_P]),
+    "hsvd_bp_workspace_size": (ctypes.c_int, [_I64, _P]),
+    "hsvd_bp_factor": (ctypes.c_int, [_P, _I64, _I64, _D, _P, _I64, _P, _P, _P, _P, _P,
+                                      ctypes.c_size_t, _P]),
 }
 
 _lib = None
@@ -173,6 +179,8 @@ def check(status, err=None):
         raise RankDeficiencyError(msg)
     if status == HSVD_SHAPE_ERROR:
         raise ShapeError(msg)
+    if status == HSVD_NUMERICAL_SINGULARITY:
+        raise NumericalSingularityError(msg)
     if status == HSVD_ERR_ARG:
         raise ValueError(msg)
     if status == HSVD_ERR_UNSUPPORTED:

@@ -1,0 +1,630 @@
+// hsvd_factor.cu -- eigen-pipeline front end on the GPU: the complete-
+// pivoting Bunch-Parlett factorization M = G J G^T in double-double
+// (hjsvd.factory.bunch_parlett_factor, factory.py:136-282).
+//
+// Compiled with -fmad=false: every double-double primitive below is the
+// reference's (_dd.py:25-93, Dekker's split, no FMA), evaluated with one
+// rounding per operation, so the factor, the signs and the permutation are
+// bit-identical to the reference's (tests/test_gpu_factor.py).
+//
+// Layout in HBM (n x n, row-major; M is exactly symmetric, so the storage
+// order of the input does not matter):
+//   Ah, Al  the trailing matrix (hi, lo), kept exactly symmetric
+//   Lh, Ll  the unit lower factor, rows permuted with the pivots
+//   vectors of the current pivot (multipliers and pivot columns), the
+//   pivot-search partials, the block records and a device-side state.
+//
+// One pivot step is two kernels and no host round trip:
+//   k_bp_pivot   (one CTA)  reduces the search partials, takes the 1x1 or
+//                2x2 decision, swaps rows/columns, forms the multipliers;
+//   k_bp_update  (upper-triangle 64x64 tiles) applies the rank-1/2 update
+//                and the symmetrization to the new trailing block, writes
+//                each tile and its mirror, and searches the updated block
+//                for the next pivot (per-tile partial maxima).
+// The trailing update is HBM-bound: 16 B read + 32 B written per element
+// pair of the upper triangle (the symmetrized value of (i, j) needs only
+// A_ij = A_ji and the pivot vectors).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include <string.h>
+
+#include "hsvd_internal.cuh"
+
+namespace hsvd {
+namespace {
+
+struct dd {
+    double h, l;
+};
+
+// ---- _dd.py:25-93 ----------------------------------------------------------
+__device__ __forceinline__ dd two_sum(double a, double b)
+{
+    const double s = __dadd_rn(a, b), bb = __dsub_rn(s, a);
+    return {s, __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb))};
+}
+__device__ __forceinline__ dd quick_two_sum(double a, double b)
+{
+    const double s = __dadd_rn(a, b);
+    return {s, __dsub_rn(b, __dsub_rn(s, a))};
+}
+__device__ __forceinline__ void split(double a, double &hi, double &lo)
+{
+    const double t = __dmul_rn(134217729.0, a);
+    hi = __dsub_rn(t, __dsub_rn(t, a));
+    lo = __dsub_rn(a, hi);
+}
+__device__ __forceinline__ dd two_prod(double a, double b)
+{
+    const double p = __dmul_rn(a, b);
+    double ah, al, bh, bl;
+    split(a, ah, al);
+    split(b, bh, bl);
+    const double e = __dadd_rn(__dadd_rn(__dadd_rn(__dsub_rn(__dmul_rn(ah, bh), p), __dmul_rn(ah, bl)),
+                                         __dmul_rn(al, bh)),
+                               __dmul_rn(al, bl));
+    return {p, e};
+}
+__device__ __forceinline__ dd dd_add(dd x, dd y)
+{
+    const dd s = two_sum(x.h, y.h);
+    return quick_two_sum(s.h, __dadd_rn(s.l, __dadd_rn(x.l, y.l)));
+}
+__device__ __forceinline__ dd dd_neg(dd x) { return {-x.h, -x.l}; }
+__device__ __forceinline__ dd dd_sub(dd x, dd y) { return dd_add(x, dd_neg(y)); }
+__device__ __forceinline__ dd dd_mul(dd x, dd y)
+{
+    const dd p = two_prod(x.h, y.h);
+    return quick_two_sum(p.h, __dadd_rn(p.l, __dadd_rn(__dmul_rn(x.h, y.l), __dmul_rn(x.l, y.h))));
+}
+__device__ __forceinline__ dd dd_mul_f(dd x, double f)
+{
+    const dd p = two_prod(x.h, f);
+    return quick_two_sum(p.h, __dadd_rn(p.l, __dmul_rn(x.l, f)));
+}
+__device__ __forceinline__ dd dd_div(dd x, dd y)
+{
+    const double q1 = __ddiv_rn(x.h, y.h);
+    const dd r = dd_sub(x, dd_mul_f(y, q1));
+    const double q2 = __ddiv_rn(__dadd_rn(r.h, r.l), y.h);
+    return quick_two_sum(q1, q2);
+}
+__device__ __forceinline__ dd dd_sqrt(dd x)
+{
+    const double r = __dsqrt_rn(x.h);
+    const dd rr = two_prod(r, r);
+    const dd diff = dd_sub(x, rr);
+    const double corr = r > 0.0 ? __ddiv_rn(__dadd_rn(diff.h, diff.l), __dmul_rn(2.0, r)) : 0.0;
+    return quick_two_sum(r, corr);
+}
+__device__ __forceinline__ dd dd_abs(dd x) { return x.h < 0.0 ? dd_neg(x) : x; }
+
+// ---- device state and workspace ------------------------------------------
+struct BpState {
+    int64_t k;       // first row/column of the trailing block
+    int64_t nb;      // blocks recorded
+    int64_t kind;    // size of the pivot taken by the last k_bp_pivot (0: none)
+    int64_t status;  // 0, or 3 = numerical singularity
+    int64_t stage;   // k at the singularity
+    int64_t p;       // number of +1 signs (after post-processing)
+};
+struct Cand {
+    double v;
+    int64_t i;
+};
+__device__ __forceinline__ bool better(double v, int64_t i, double bv, int64_t bi)
+{
+    return v > bv || (v == bv && i < bi);
+}
+
+constexpr int TB = 64;          // update tile
+constexpr int UPD_THREADS = 256;
+constexpr int PIV_THREADS = 1024;
+
+struct BpWs {
+    double *Ah, *Al, *Lh, *Ll;
+    double *v0h, *v0l, *v1h, *v1l;  // pivot columns c / W0, W1
+    double *l0h, *l0l, *l1h, *l1l;  // multipliers l / l0, l1
+    Cand *poff, *pdiag;             // per-tile search partials
+    int64_t *bcol, *bsz;
+    dd *bd;                         // 3 per block
+    dd *bp;                         // post-processing parameters, 4 per block
+    int8_t *sg;                     // signs in pivot order
+    int64_t *ocol;                  // output column of each pivot column
+    BpState *st;
+};
+
+__host__ __device__ inline int64_t tiles_of(int64_t m) { return (m + TB - 1) / TB; }
+__host__ __device__ inline int64_t tri_count(int64_t m)
+{
+    const int64_t T = tiles_of(m);
+    return T * (T + 1) / 2;
+}
+// linear upper-triangle tile index -> (I, J), I <= J (column-major over J)
+__device__ __forceinline__ void tri_tile(int64_t idx, int &I, int &J)
+{
+    int j = (int)((sqrt(8.0 * (double)idx + 1.0) - 1.0) * 0.5);
+    while ((int64_t)(j + 1) * (j + 2) / 2 <= idx) ++j;
+    while ((int64_t)j * (j + 1) / 2 > idx) --j;
+    J = j;
+    I = (int)(idx - (int64_t)j * (j + 1) / 2);
+}
+
+template <int NT>
+__device__ void block_argmax(double &v, int64_t &i, double &v2, int64_t &i2)
+{
+    // two independent (value, index) maxima over the CTA; result in thread 0
+    __shared__ double sv[NT / 32], sv2[NT / 32];
+    __shared__ int64_t si[NT / 32], si2[NT / 32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_down_sync(0xffffffffu, v, o);
+        const int64_t oi = __shfl_down_sync(0xffffffffu, i, o);
+        const double ov2 = __shfl_down_sync(0xffffffffu, v2, o);
+        const int64_t oi2 = __shfl_down_sync(0xffffffffu, i2, o);
+        if (better(ov, oi, v, i)) { v = ov; i = oi; }
+        if (better(ov2, oi2, v2, i2)) { v2 = ov2; i2 = oi2; }
+    }
+    if (lane == 0) { sv[w] = v; si[w] = i; sv2[w] = v2; si2[w] = i2; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int k = 1; k < NT / 32; ++k) {
+            if (better(sv[k], si[k], v, i)) { v = sv[k]; i = si[k]; }
+            if (better(sv2[k], si2[k], v2, i2)) { v2 = sv2[k]; i2 = si2[k]; }
+        }
+    }
+    __syncthreads();
+}
+
+// ---- setup ---------------------------------------------------------------------
+__global__ void k_bp_init(const double *M, int64_t ldm, int64_t n, BpWs w)
+{
+    const int64_t N = n * n;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < N;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e / n, j = e % n;
+        w.Ah[e] = M[i * ldm + j];
+        w.Al[e] = 0.0;
+        w.Lh[e] = i == j ? 1.0 : 0.0;
+        w.Ll[e] = 0.0;
+    }
+}
+__global__ void k_bp_init_state(int64_t n, BpWs w, int64_t *perm)
+{
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) perm[i] = i;
+    if (threadIdx.x == 0) *w.st = BpState{0, 0, 0, 0, 0, 0};
+}
+
+// pivot search of the whole matrix (step 0); per-tile partials
+__global__ void __launch_bounds__(UPD_THREADS) k_bp_search(int64_t n, BpWs w)
+{
+    const int64_t m = n;
+    if (blockIdx.x >= tri_count(m)) return;
+    int I, J;
+    tri_tile(blockIdx.x, I, J);
+    const int tx = threadIdx.x % TB, ty = threadIdx.x / TB;
+    double bo = -1.0, bd = -1.0;
+    int64_t io = 0, id = 0;
+    const int64_t c = (int64_t)J * TB + tx;
+    for (int r0 = ty; r0 < TB; r0 += UPD_THREADS / TB) {
+        const int64_t r = (int64_t)I * TB + r0;
+        if (r >= m || c >= m) continue;
+        const double v = fabs(w.Ah[r * n + c]);
+        if (r < c) {
+            if (better(v, r * m + c, bo, io)) { bo = v; io = r * m + c; }
+        } else if (r == c) {
+            if (better(v, r, bd, id)) { bd = v; id = r; }
+        }
+    }
+    block_argmax<UPD_THREADS>(bo, io, bd, id);
+    if (threadIdx.x == 0) {
+        w.poff[blockIdx.x] = Cand{bo, io};
+        w.pdiag[blockIdx.x] = Cand{bd, id};
+    }
+}
+
+// symmetric swap of rows/columns a and b inside the trailing block [k:]
+// (_swap_sym, factory.py:117-121) plus the rows of L left of k and perm
+__device__ void sym_swap(BpWs &w, int64_t *perm, int64_t n, int64_t k, int64_t a, int64_t b)
+{
+    for (int64_t c = k + threadIdx.x; c < n; c += blockDim.x) {
+        double t = w.Ah[a * n + c]; w.Ah[a * n + c] = w.Ah[b * n + c]; w.Ah[b * n + c] = t;
+        t = w.Al[a * n + c]; w.Al[a * n + c] = w.Al[b * n + c]; w.Al[b * n + c] = t;
+    }
+    __syncthreads();
+    for (int64_t r = k + threadIdx.x; r < n; r += blockDim.x) {
+        double t = w.Ah[r * n + a]; w.Ah[r * n + a] = w.Ah[r * n + b]; w.Ah[r * n + b] = t;
+        t = w.Al[r * n + a]; w.Al[r * n + a] = w.Al[r * n + b]; w.Al[r * n + b] = t;
+    }
+    for (int64_t c = threadIdx.x; c < k; c += blockDim.x) {
+        double t = w.Lh[a * n + c]; w.Lh[a * n + c] = w.Lh[b * n + c]; w.Lh[b * n + c] = t;
+        t = w.Ll[a * n + c]; w.Ll[a * n + c] = w.Ll[b * n + c]; w.Ll[b * n + c] = t;
+    }
+    if (threadIdx.x == 0) {
+        const int64_t t = perm[a];
+        perm[a] = perm[b];
+        perm[b] = t;
+    }
+    __syncthreads();
+}
+
+// ---- one pivot decision (factory.py:153-232 up to the update) -------------
+__global__ void __launch_bounds__(PIV_THREADS) k_bp_pivot(int64_t n, double thresh, double alpha,
+                                                          BpWs w, int64_t *perm)
+{
+    __shared__ BpState S;
+    __shared__ int64_t sh_i0, sh_off;
+    __shared__ double sh_mu0, sh_mu1;
+    if (threadIdx.x == 0) S = *w.st;
+    __syncthreads();
+    if (S.status != 0 || S.k >= n) {
+        if (threadIdx.x == 0) w.st->kind = 0;
+        return;
+    }
+    const int64_t k = S.k, m = n - k, cnt = tri_count(m);
+    // reduce the search partials of the trailing block
+    double bo = -1.0, bd = -1.0;
+    int64_t io = 0, id = 0;
+    for (int64_t e = threadIdx.x; e < cnt; e += blockDim.x) {
+        const Cand o = w.poff[e], d = w.pdiag[e];
+        if (better(o.v, o.i, bo, io)) { bo = o.v; io = o.i; }
+        if (better(d.v, d.i, bd, id)) { bd = d.v; id = d.i; }
+    }
+    block_argmax<PIV_THREADS>(bo, io, bd, id);
+    if (threadIdx.x == 0) {
+        // no off-diagonal candidate (m == 1): mu1 = 0 (numpy: argmax of zeros)
+        sh_mu1 = bo < 0.0 ? 0.0 : bo;
+        sh_off = bo < 0.0 ? 0 : io;
+        sh_mu0 = bd;
+        sh_i0 = id;
+    }
+    __syncthreads();
+    const double mu0 = sh_mu0, mu1 = sh_mu1;
+    if (!(fmax(mu0, mu1) > thresh)) {
+        if (threadIdx.x == 0) {
+            w.st->status = 3;
+            w.st->stage = k;
+            w.st->kind = 0;
+        }
+        return;
+    }
+    const bool one = m == 1 || mu0 >= alpha * mu1;
+    if (one) {
+        if (sh_i0 != 0) sym_swap(w, perm, n, k, k, k + sh_i0);
+        const dd d = {w.Ah[k * n + k], w.Al[k * n + k]};
+        for (int64_t i = k + 1 + threadIdx.x; i < n; i += blockDim.x) {
+            const dd c = {w.Ah[k * n + i], w.Al[k * n + i]};  // A[i][k] = A[k][i]
+            const dd l = dd_div(c, d);
+            w.Lh[i * n + k] = l.h;
+            w.Ll[i * n + k] = l.l;
+            w.v0h[i] = c.h; w.v0l[i] = c.l;
+            w.l0h[i] = l.h; w.l0l[i] = l.l;
+        }
+        if (threadIdx.x == 0) {
+            const int64_t q = S.nb;
+            w.bcol[q] = k;
+            w.bsz[q] = 1;
+            w.bd[3 * q] = d;
+            w.st->nb = q + 1;
+            w.st->k = k + 1;
+            w.st->kind = 1;
+        }
+    } else {
+        // largest off-diagonal entry at (a, b), a < b: the reference's
+        // (i1, j1) = (b, a); rows/columns k <- k + j1, then k + 1 <- k + i1
+        const int64_t a = sh_off / m, b = sh_off % m;
+        if (a != 0) sym_swap(w, perm, n, k, k, k + a);
+        if (b != 1) sym_swap(w, perm, n, k, k + 1, k + b);
+        const dd ea = {w.Ah[k * n + k], w.Al[k * n + k]};
+        const dd eb = {w.Ah[(k + 1) * n + k], w.Al[(k + 1) * n + k]};
+        const dd ec = {w.Ah[(k + 1) * n + k + 1], w.Al[(k + 1) * n + k + 1]};
+        const dd det = dd_sub(dd_mul(ea, ec), dd_mul(eb, eb));
+        for (int64_t i = k + 2 + threadIdx.x; i < n; i += blockDim.x) {
+            const dd W0 = {w.Ah[k * n + i], w.Al[k * n + i]};
+            const dd W1 = {w.Ah[(k + 1) * n + i], w.Al[(k + 1) * n + i]};
+            const dd l0 = dd_div(dd_sub(dd_mul(W0, ec), dd_mul(W1, eb)), det);
+            const dd l1 = dd_div(dd_sub(dd_mul(W1, ea), dd_mul(W0, eb)), det);
+            w.Lh[i * n + k] = l0.h; w.Ll[i * n + k] = l0.l;
+            w.Lh[i * n + k + 1] = l1.h; w.Ll[i * n + k + 1] = l1.l;
+            w.v0h[i] = W0.h; w.v0l[i] = W0.l;
+            w.v1h[i] = W1.h; w.v1l[i] = W1.l;
+            w.l0h[i] = l0.h; w.l0l[i] = l0.l;
+            w.l1h[i] = l1.h; w.l1l[i] = l1.l;
+        }
+        if (threadIdx.x == 0) {
+            const int64_t q = S.nb;
+            w.bcol[q] = k;
+            w.bsz[q] = 2;
+            w.bd[3 * q] = ea;
+            w.bd[3 * q + 1] = eb;
+            w.bd[3 * q + 2] = ec;
+            w.st->nb = q + 1;
+            w.st->k = k + 2;
+            w.st->kind = 2;
+        }
+    }
+}
+
+// ---- trailing update + symmetrization + next search -----------------------
+// X = A - upd (both triangles), A <- (X + X^T) / 2 (factory.py:185-193 and
+// 213-224 with _symmetrize, 124-128).  A is exactly symmetric, so the new
+// (i, j) needs only A_ij and the pivot vectors, and equals the new (j, i)
+// bit for bit (two_sum's error term is exact, hence symmetric).
+__global__ void __launch_bounds__(UPD_THREADS) k_bp_update(int64_t n, BpWs w)
+{
+    __shared__ double tt[TB][TB + 1];  // transposed tile (hi, then lo)
+    __shared__ double rl0h[TB], rl0l[TB], rv0h[TB], rv0l[TB], rl1h[TB], rl1l[TB], rv1h[TB], rv1l[TB];
+    __shared__ double cl0h[TB], cl0l[TB], cv0h[TB], cv0l[TB], cl1h[TB], cl1l[TB], cv1h[TB], cv1l[TB];
+    const BpState S = *w.st;
+    if (S.kind == 0 || S.status != 0) return;
+    const int64_t k = S.k, m = n - k;  // the new trailing block
+    if ((int64_t)blockIdx.x >= tri_count(m)) return;
+    const bool two = S.kind == 2;
+    int I, J;
+    tri_tile(blockIdx.x, I, J);
+    const int tid = threadIdx.x, tx = tid % TB, ty = tid / TB;
+    const int64_t r0 = k + (int64_t)I * TB, c0 = k + (int64_t)J * TB;
+    if (tid < TB) {
+        const int64_t r = r0 + tid, c = c0 + tid;
+        if (r < n) {
+            rl0h[tid] = w.l0h[r]; rl0l[tid] = w.l0l[r]; rv0h[tid] = w.v0h[r]; rv0l[tid] = w.v0l[r];
+            if (two) { rl1h[tid] = w.l1h[r]; rl1l[tid] = w.l1l[r]; rv1h[tid] = w.v1h[r]; rv1l[tid] = w.v1l[r]; }
+        }
+        if (c < n) {
+            cl0h[tid] = w.l0h[c]; cl0l[tid] = w.l0l[c]; cv0h[tid] = w.v0h[c]; cv0l[tid] = w.v0l[c];
+            if (two) { cl1h[tid] = w.l1h[c]; cl1l[tid] = w.l1l[c]; cv1h[tid] = w.v1h[c]; cv1l[tid] = w.v1l[c]; }
+        }
+    }
+    __syncthreads();
+    double bo = -1.0, bd = -1.0;
+    int64_t io = 0, id = 0;
+    const int64_t c = c0 + tx;
+    constexpr int RPT = TB / (UPD_THREADS / TB);  // rows per thread
+    double nh[RPT], nl[RPT];
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) {
+        const int rr = ty + u * (UPD_THREADS / TB);
+        const int64_t r = r0 + rr;
+        nh[u] = nl[u] = 0.0;
+        if (r >= n || c >= n) continue;
+        const dd a = {w.Ah[r * n + c], w.Al[r * n + c]};
+        const dd li = {rl0h[rr], rl0l[rr]}, ci = {rv0h[rr], rv0l[rr]};
+        const dd lj = {cl0h[tx], cl0l[tx]}, cj = {cv0h[tx], cv0l[tx]};
+        dd uij, uji;
+        if (!two) {
+            uij = dd_mul(li, cj);
+            uji = dd_mul(lj, ci);
+        } else {
+            const dd li1 = {rl1h[rr], rl1l[rr]}, ci1 = {rv1h[rr], rv1l[rr]};
+            const dd lj1 = {cl1h[tx], cl1l[tx]}, cj1 = {cv1h[tx], cv1l[tx]};
+            uij = dd_add(dd_mul(li, cj), dd_mul(li1, cj1));
+            uji = dd_add(dd_mul(lj, ci), dd_mul(lj1, ci1));
+        }
+        const dd xij = dd_sub(a, uij), xji = dd_sub(a, uji);
+        const dd s = dd_mul_f(dd_add(xij, xji), 0.5);
+        w.Ah[r * n + c] = s.h;
+        w.Al[r * n + c] = s.l;
+        nh[u] = s.h;
+        nl[u] = s.l;
+        const double v = fabs(s.h);
+        const int64_t ri = r - k, cj_ = c - k;
+        if (ri < cj_) {
+            if (better(v, ri * m + cj_, bo, io)) { bo = v; io = ri * m + cj_; }
+        } else if (ri == cj_) {
+            if (better(v, ri, bd, id)) { bd = v; id = ri; }
+        }
+    }
+    if (I != J) {
+        // mirror tile: rows c0.., columns r0.. (coalesced along r), hi then lo
+        const int64_t mc = r0 + tx;
+#pragma unroll
+        for (int part = 0; part < 2; ++part) {
+            __syncthreads();
+#pragma unroll
+            for (int u = 0; u < RPT; ++u) tt[tx][ty + u * (UPD_THREADS / TB)] = part ? nl[u] : nh[u];
+            __syncthreads();
+            double *dst = part ? w.Al : w.Ah;
+            for (int cc = ty; cc < TB; cc += UPD_THREADS / TB) {
+                const int64_t mr = c0 + cc;
+                if (mr >= n || mc >= n) continue;
+                dst[mr * n + mc] = tt[cc][tx];
+            }
+        }
+    }
+    block_argmax<UPD_THREADS>(bo, io, bd, id);
+    if (tid == 0) {
+        w.poff[blockIdx.x] = Cand{bo, io};
+        w.pdiag[blockIdx.x] = Cand{bd, id};
+    }
+}
+
+// ---- post-processing: D's 2x2 blocks diagonalized (factory.py:234-255) ------
+__global__ void k_bp_blocks(BpWs w, int64_t n)
+{
+    const int64_t nb = w.st->nb;
+    const dd one = {1.0, 0.0};
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nb;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t col = w.bcol[q];
+        if (w.bsz[q] == 1) {
+            const dd d = w.bd[3 * q];
+            w.bp[4 * q] = dd_sqrt(dd_abs(d));
+            w.sg[col] = d.h > 0.0 ? 1 : -1;
+        } else {
+            const dd ea = w.bd[3 * q], eb = w.bd[3 * q + 1], ec = w.bd[3 * q + 2];
+            const dd zeta = dd_div(dd_sub(ec, ea), dd_mul_f(eb, 2.0));
+            const double sgn = zeta.h >= 0.0 ? 1.0 : -1.0;
+            const dd root = dd_sqrt(dd_add(one, dd_mul(zeta, zeta)));
+            const dd t = dd_div(dd{sgn, 0.0}, dd_add(dd_abs(zeta), root));
+            const dd cs = dd_div(one, dd_sqrt(dd_add(one, dd_mul(t, t))));
+            const dd sn = dd_mul(t, cs);
+            const dd lam1 = dd_sub(ea, dd_mul(t, eb));
+            const dd lam2 = dd_add(ec, dd_mul(t, eb));
+            w.bp[4 * q] = cs;
+            w.bp[4 * q + 1] = sn;
+            w.bp[4 * q + 2] = dd_sqrt(dd_abs(lam1));
+            w.bp[4 * q + 3] = dd_sqrt(dd_abs(lam2));
+            w.sg[col] = lam1.h > 0.0 ? 1 : -1;
+            w.sg[col + 1] = lam2.h > 0.0 ? 1 : -1;
+        }
+    }
+}
+// output column of every pivot column: +1 columns first, each class in pivot
+// order (_assemble_factor, factory.py:258-267); signs_out in output order
+__global__ void k_bp_order(BpWs w, int64_t n, int8_t *signs_out)
+{
+    if (threadIdx.x != 0) return;
+    int64_t p = 0;
+    for (int64_t c = 0; c < n; ++c) p += w.sg[c] == 1;
+    int64_t pos = 0, neg = p;
+    for (int64_t c = 0; c < n; ++c) {
+        const int64_t o = w.sg[c] == 1 ? pos++ : neg++;
+        w.ocol[c] = o;
+        signs_out[o] = w.sg[c];
+    }
+    w.st->p = p;
+}
+// G[perm[i], ocol[col]] = hi + lo of (L Q_D |Lambda_D|^{1/2})[i, col]
+__global__ void k_bp_assemble(BpWs w, const int64_t *perm, int64_t n, double *G, int64_t ldg)
+{
+    const int64_t q = blockIdx.y;
+    if (q >= w.st->nb) return;
+    const int64_t col = w.bcol[q];
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int64_t row = perm[i];
+    if (w.bsz[q] == 1) {
+        const dd g = dd_mul(dd{w.Lh[i * n + col], w.Ll[i * n + col]}, w.bp[4 * q]);
+        G[row + w.ocol[col] * ldg] = __dadd_rn(g.h, g.l);
+    } else {
+        const dd cs = w.bp[4 * q], sn = w.bp[4 * q + 1], s1 = w.bp[4 * q + 2], s2 = w.bp[4 * q + 3];
+        const dd L0 = {w.Lh[i * n + col], w.Ll[i * n + col]};
+        const dd L1 = {w.Lh[i * n + col + 1], w.Ll[i * n + col + 1]};
+        const dd u1 = dd_sub(dd_mul(L0, cs), dd_mul(L1, sn));
+        const dd u2 = dd_add(dd_mul(L0, sn), dd_mul(L1, cs));
+        const dd g1 = dd_mul(u1, s1), g2 = dd_mul(u2, s2);
+        G[row + w.ocol[col] * ldg] = __dadd_rn(g1.h, g1.l);
+        G[row + w.ocol[col + 1] * ldg] = __dadd_rn(g2.h, g2.l);
+    }
+}
+
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+// carve the workspace (sizes only when base == nullptr)
+size_t bp_carve(int64_t n, unsigned char *base, BpWs *w)
+{
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        unsigned char *p = base ? base + off : nullptr;
+        off += align256(bytes);
+        return p;
+    };
+    const size_t N = (size_t)n * n, tc = (size_t)tri_count(n);
+    BpWs x;
+    x.Ah = (double *)take(N * 8);
+    x.Al = (double *)take(N * 8);
+    x.Lh = (double *)take(N * 8);
+    x.Ll = (double *)take(N * 8);
+    x.v0h = (double *)take(n * 8); x.v0l = (double *)take(n * 8);
+    x.v1h = (double *)take(n * 8); x.v1l = (double *)take(n * 8);
+    x.l0h = (double *)take(n * 8); x.l0l = (double *)take(n * 8);
+    x.l1h = (double *)take(n * 8); x.l1l = (double *)take(n * 8);
+    x.poff = (Cand *)take(tc * sizeof(Cand));
+    x.pdiag = (Cand *)take(tc * sizeof(Cand));
+    x.bcol = (int64_t *)take(n * 8);
+    x.bsz = (int64_t *)take(n * 8);
+    x.bd = (dd *)take(3 * n * sizeof(dd));
+    x.bp = (dd *)take(4 * n * sizeof(dd));
+    x.sg = (int8_t *)take(n);
+    x.ocol = (int64_t *)take(n * 8);
+    x.st = (BpState *)take(sizeof(BpState));
+    if (w) *w = x;
+    return off;
+}
+
+}  // namespace
+}  // namespace hsvd
+
+using namespace hsvd;
+
+extern "C" {
+
+HSVD_API int hsvd_bp_workspace_size(int64_t n, size_t *bytes)
+{
+    if (n < 1 || !bytes) {
+        set_error("hsvd_bp_workspace_size: bad arguments");
+        return HSVD_ERR_ARG;
+    }
+    *bytes = bp_carve(n, nullptr, nullptr);
+    return HSVD_OK;
+}
+
+HSVD_API int hsvd_bp_factor(const double *M, int64_t n, int64_t ldm, double thresh, double *G,
+                            int64_t ldg, int8_t *signs, int64_t *perm, int64_t *p_out,
+                            int64_t *stage_out, void *ws, size_t ws_bytes, void *stream)
+{
+    if (!M || !G || !signs || !perm || !p_out || n < 1 || ldm < n || ldg < n || !ws) {
+        set_error("hsvd_bp_factor: bad arguments");
+        return HSVD_ERR_ARG;
+    }
+    if (ws_bytes < bp_carve(n, nullptr, nullptr)) {
+        set_error("hsvd_bp_factor: workspace too small");
+        return HSVD_ERR_ARG;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    BpWs w;
+    bp_carve(n, (unsigned char *)ws, &w);
+    int dev = 0;
+    HSVD_CUDA(cudaGetDevice(&dev));
+    int st_ = 0;
+    DevCtx *ctx = dev_ctx(dev, &st_);
+    if (!ctx) return st_;
+    if (ctx->host_reserve(8) != HSVD_OK) return HSVD_ERR_CUDA;
+    int64_t *hbuf = ctx->host;  // pinned
+    const double alpha = (1.0 + sqrt(17.0)) / 8.0;
+
+    k_bp_init<<<1184, 256, 0, s>>>(M, ldm, n, w);
+    k_bp_init_state<<<1, 256, 0, s>>>(n, w, perm);
+    k_bp_search<<<(unsigned)tri_count(n), UPD_THREADS, 0, s>>>(n, w);
+    HSVD_LAUNCH_CHECK("k_bp_search");
+    // pivot steps in batches; the state is read back once per batch
+    int64_t k = 0;
+    for (;;) {
+        const int64_t batch = 64;
+        for (int64_t j = 0; j < batch; ++j) {
+            // after this pivot the trailing block starts at >= k + j + 1
+            const int64_t mmax = n - (k + j + 1);
+            k_bp_pivot<<<1, PIV_THREADS, 0, s>>>(n, thresh, alpha, w, perm);
+            if (mmax > 0) k_bp_update<<<(unsigned)tri_count(mmax), UPD_THREADS, 0, s>>>(n, w);
+        }
+        HSVD_LAUNCH_CHECK("k_bp_pivot/k_bp_update");
+        HSVD_CUDA(cudaMemcpyAsync(hbuf, w.st, sizeof(BpState), cudaMemcpyDeviceToHost, s));
+        HSVD_CUDA(cudaStreamSynchronize(s));
+        BpState hs;
+        memcpy(&hs, hbuf, sizeof(hs));
+        if (hs.status != 0) {
+            if (stage_out) *stage_out = hs.stage;
+            set_error("hsvd_bp_factor: numerical singularity");
+            return HSVD_NUMERICAL_SINGULARITY;
+        }
+        k = hs.k;
+        if (k >= n) break;
+    }
+    k_bp_blocks<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(w, n);
+    k_bp_order<<<1, 32, 0, s>>>(w, n, signs);
+    HSVD_CUDA(cudaMemcpyAsync(hbuf, w.st, sizeof(BpState), cudaMemcpyDeviceToHost, s));
+    HSVD_CUDA(cudaStreamSynchronize(s));
+    BpState hs;
+    memcpy(&hs, hbuf, sizeof(hs));
+    k_bp_assemble<<<dim3((unsigned)((n + 255) / 256), (unsigned)hs.nb), 256, 0, s>>>(w, perm, n, G,
+                                                                                  ldg);
+    HSVD_LAUNCH_CHECK("k_bp_assemble");
+    *p_out = hs.p;
+    if (stage_out) *stage_out = -1;
+    return HSVD_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,60 @@
+"""Goldens of the factorization front end, made by running the REAL
+reference (hjsvd.factory.bunch_parlett_factor, factory.py:270-282) in the
+build container:
+
+    NUMBA_CACHE_DIR=/tmp/numba_cache python tests/golden/make_golden_factor.py
+
+Records SHA-256 digests of G (Fortran order), perm and signs, p and the
+number of 2x2 pivots, into tests/golden/factor.json; the inputs are seeded
+numpy matrices (tests/golden/factor_inputs.py) or reference-generated
+spectra stored in factor_inputs.npz.  Nothing on the GPU box reads
+/root/reference.
+"""
+
+import hashlib
+import json
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, HERE)
+
+import hjsvd  # noqa: E402
+from digest import digest  # noqa: E402
+from factor_inputs import make_input  # noqa: E402
+
+SPECTRA = [(16, 2), (64, 7), (128, 9)]
+CASES = [("diag", 2, 0), ("offdiag", 2, 0), ("sym", 5, 1), ("sym", 33, 3), ("sym", 200, 4),
+         ("sym", 256, 5), ("smalldiag", 100, 6), ("smalldiag", 257, 8), ("ints", 40, 10),
+         ("ints", 96, 11)] + [("spectrum", n, s) for n, s in SPECTRA]
+
+
+def main():
+    arrs = {}
+    for n, s in SPECTRA:
+        M, lam = hjsvd.generate_symmetric(hjsvd.SpectrumSpec(n, 20.0, s))
+        arrs[f"M_{n}_{s}"] = M
+        arrs[f"lam_{n}_{s}"] = lam
+    np.savez_compressed(os.path.join(HERE, "factor_inputs.npz"), **arrs)
+    out = []
+    for kind, n, seed in CASES:
+        M = make_input(kind, n, seed)
+        pair = hjsvd.bunch_parlett_factor(M)
+        out.append({
+            "kind": kind, "n": int(M.shape[0]), "seed": seed,
+            "G": digest(pair.G),
+            "perm": hashlib.sha256(np.asarray(pair.perm, "<i8").tobytes()).hexdigest(),
+            "signs": hashlib.sha256(np.asarray(pair.J.signs, "i1").tobytes()).hexdigest(),
+            "p": int(pair.J.p),
+        })
+        print(kind, n, seed, out[-1]["p"])
+    with open(os.path.join(HERE, "factor.json"), "w") as f:
+        json.dump({"reference": "hjsvd.factory.bunch_parlett_factor (factory.py:270-282)",
+                   "singular": {"kind": "ones", "n": 3}, "cases": out}, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()
