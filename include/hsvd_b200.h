@@ -271,6 +271,16 @@ HSVD_API int hsvd_bp_factor(const double *M, int64_t n, int64_t ldm, double thre
                             int64_t ldg, int8_t *signs, int64_t *perm, int64_t *p_out,
                             int64_t *stage_out, void *ws, size_t ws_bytes, void *stream);
 
+/* QR shortening of a tall factor (factory.py:300-334): G (device, n x r,
+ * column-major, n > r) = Q R; R (r x r, ldr) upper triangular with a
+ * positive diagonal, Q (n x r, ldq) orthonormal columns.  Plain fp64
+ * Householder.  HSVD_RANK_DEFICIENT (+ *bad_col) for a dependent column or a
+ * zero diagonal of R; HSVD_SHAPE_ERROR for n <= r. */
+HSVD_API int hsvd_qr_workspace_size(int64_t n, int64_t r, size_t *bytes);
+HSVD_API int hsvd_qr_shorten(const double *G, int64_t n, int64_t r, int64_t ldg, double *R,
+                             int64_t ldr, double *Q, int64_t ldq, int64_t *bad_col, void *ws,
+                             size_t ws_bytes, void *stream);
+
 /* The shard plan alone (host only, no GPU): the stepper of all slots, the
  * block placement and the per-step block moves, for tests of the exchange
  * protocol.  hsvd_plan_advance writes (block, from, from_area, to, to_area)

@@ -32,6 +32,7 @@ from .factory import (
     bunch_parlett_factor_device,
     draw_spectrum,
     eigvalsh,
+    qr_shorten,
 )
 from .matio import read_csv_matrix, read_gjh, write_csv_matrix, write_gjh
 from .rotation import (

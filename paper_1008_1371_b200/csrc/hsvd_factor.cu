@@ -628,3 +628,183 @@ HSVD_API int hsvd_bp_factor(const double *M, int64_t n, int64_t ldm, double thre
 }
 
 }  // extern "C"
+
+// ===========================================================================
+// QR shortening of a tall factor (hjsvd.factory.qr_shorten, factory.py:
+// 300-334): Householder QR, G = Q R with R's diagonal made positive.  Plain
+// fp64 (the reference's norm and dot products go through numpy's BLAS, so
+// this path is checked to the reference's tolerances, not bit for bit).
+// One step is two kernels: k_qr_reflector (one CTA: the reflector v, beta
+// and column k of R) and k_qr_apply (one CTA per remaining column: its dot
+// with v, then its rank-1 update).  Q is formed by applying the reflectors
+// to eye(n, r) in reverse order with the same column kernel.
+// ===========================================================================
+namespace hsvd {
+namespace {
+
+constexpr int QR_THREADS = 256;
+
+template <int NT>
+__device__ double block_sum(double v)
+{
+    __shared__ double sh[NT / 32];
+    __shared__ double total;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int k = 0; k < NT / 32; ++k) s += sh[k];
+        total = s;
+    }
+    __syncthreads();
+    const double r = total;
+    __syncthreads();
+    return r;
+}
+
+// A column-major n x r (ld lda); V column-major n x r holds v_k in rows k..;
+// beta[k]; status: first dependent column + 1 (0 = none)
+__global__ void __launch_bounds__(QR_THREADS) k_qr_reflector(double *A, int64_t lda, int64_t n,
+                                                             int64_t k, double *V, double *beta,
+                                                             int64_t *status)
+{
+    if (*status) return;
+    double *x = A + k * lda;
+    double s = 0.0;
+    for (int64_t i = k + threadIdx.x; i < n; i += blockDim.x) s += x[i] * x[i];
+    const double normx = sqrt(block_sum<QR_THREADS>(s));
+    if (normx == 0.0) {
+        if (threadIdx.x == 0) *status = k + 1;
+        return;
+    }
+    const double x0 = x[k];
+    const double alpha = -(x0 >= 0.0 ? 1.0 : -1.0) * normx;
+    double vv = 0.0;
+    for (int64_t i = k + threadIdx.x; i < n; i += blockDim.x) {
+        const double vi = i == k ? x0 - alpha : x[i];
+        V[k * n + i] = vi;
+        vv += vi * vi;
+    }
+    const double b = 2.0 / block_sum<QR_THREADS>(vv);
+    __syncthreads();
+    for (int64_t i = k + threadIdx.x; i < n; i += blockDim.x) x[i] = i == k ? alpha : 0.0;
+    if (threadIdx.x == 0) beta[k] = b;
+}
+
+// for every column j in [j0, j1): M[k:, j] -= beta_k v_k (v_k^T M[k:, j])
+__global__ void __launch_bounds__(QR_THREADS) k_qr_apply(double *M, int64_t ldm, int64_t n,
+                                                         int64_t k, int64_t j0, const double *V,
+                                                         const double *beta,
+                                                         const int64_t *status)
+{
+    if (*status) return;
+    const int64_t j = j0 + blockIdx.x;
+    double *col = M + j * ldm;
+    const double *v = V + k * n;
+    double s = 0.0;
+    for (int64_t i = k + threadIdx.x; i < n; i += blockDim.x) s += v[i] * col[i];
+    const double w = block_sum<QR_THREADS>(s);
+    const double bw = beta[k] * w;
+    for (int64_t i = k + threadIdx.x; i < n; i += blockDim.x) col[i] -= v[i] * bw;
+}
+
+__global__ void k_qr_eye(double *Q, int64_t n, int64_t r)
+{
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * r;
+         e += (int64_t)gridDim.x * blockDim.x)
+        Q[e] = (e % n) == (e / n) ? 1.0 : 0.0;
+}
+
+// R = triu(A[:r, :]) (column-major r x r, ldr), flipped rows/columns of
+// negative diagonal; status = r + 1 + row of a zero diagonal entry
+__global__ void k_qr_finish(const double *A, int64_t lda, int64_t n, int64_t r, double *R,
+                            int64_t ldr, double *Q, int64_t ldq, int64_t *status)
+{
+    if (*status) return;
+    const int64_t j = blockIdx.x;  // column
+    const double djj = A[j * lda + j];
+    for (int64_t i = threadIdx.x; i < r; i += blockDim.x) {
+        const double dii = A[i * lda + i];
+        const double v = i <= j ? A[j * lda + i] : 0.0;
+        R[j * ldr + i] = dii < 0.0 ? -v : v;
+    }
+    if (djj < 0.0)
+        for (int64_t i = threadIdx.x; i < n; i += blockDim.x) Q[j * ldq + i] = -Q[j * ldq + i];
+    if (threadIdx.x == 0 && djj == 0.0) atomicCAS((unsigned long long *)status, 0ull,
+                                                  (unsigned long long)(r + 1 + j));
+}
+
+}  // namespace
+}  // namespace hsvd
+
+extern "C" {
+
+HSVD_API int hsvd_qr_workspace_size(int64_t n, int64_t r, size_t *bytes)
+{
+    if (n < 1 || r < 1 || !bytes) {
+        set_error("hsvd_qr_workspace_size: bad arguments");
+        return HSVD_ERR_ARG;
+    }
+    *bytes = align256((size_t)n * r * 8) * 2 + align256((size_t)r * 8) + 256;
+    return HSVD_OK;
+}
+
+HSVD_API int hsvd_qr_shorten(const double *G, int64_t n, int64_t r, int64_t ldg, double *R,
+                             int64_t ldr, double *Q, int64_t ldq, int64_t *bad_col, void *ws,
+                             size_t ws_bytes, void *stream)
+{
+    if (!G || !R || !Q || n < 1 || r < 1 || ldg < n || ldr < r || ldq < n || !ws) {
+        set_error("hsvd_qr_shorten: bad arguments");
+        return HSVD_ERR_ARG;
+    }
+    if (n <= r) {
+        set_error("qr_shorten needs n > r");
+        return HSVD_SHAPE_ERROR;
+    }
+    size_t need = 0;
+    hsvd_qr_workspace_size(n, r, &need);
+    if (ws_bytes < need) {
+        set_error("hsvd_qr_shorten: workspace too small");
+        return HSVD_ERR_ARG;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    unsigned char *b = (unsigned char *)ws;
+    double *A = (double *)b;
+    double *V = (double *)(b + align256((size_t)n * r * 8));
+    double *beta = (double *)(b + 2 * align256((size_t)n * r * 8));
+    int64_t *status = (int64_t *)(b + 2 * align256((size_t)n * r * 8) + align256((size_t)r * 8));
+    HSVD_CUDA(cudaMemsetAsync(status, 0, 8, s));
+    HSVD_CUDA(cudaMemcpy2DAsync(A, n * 8, G, ldg * 8, n * 8, r, cudaMemcpyDeviceToDevice, s));
+    for (int64_t k = 0; k < r; ++k) {
+        k_qr_reflector<<<1, QR_THREADS, 0, s>>>(A, n, n, k, V, beta, status);
+        if (k + 1 < r) k_qr_apply<<<(unsigned)(r - k - 1), QR_THREADS, 0, s>>>(A, n, n, k, k + 1, V, beta, status);
+    }
+    HSVD_LAUNCH_CHECK("k_qr_apply");
+    k_qr_eye<<<1184, 256, 0, s>>>(Q, ldq, r);
+    // Q = H_0 ... H_{r-1} eye(n, r): reflector k touches rows k.. of the
+    // columns >= k only (the others are zero there)
+    for (int64_t k = r - 1; k >= 0; --k)
+        k_qr_apply<<<(unsigned)(r - k), QR_THREADS, 0, s>>>(Q, ldq, n, k, k, V, beta, status);
+    HSVD_LAUNCH_CHECK("k_qr_apply (Q)");
+    k_qr_finish<<<(unsigned)r, 256, 0, s>>>(A, n, n, r, R, ldr, Q, ldq, status);
+    int dev = 0;
+    HSVD_CUDA(cudaGetDevice(&dev));
+    int st_ = 0;
+    DevCtx *ctx = dev_ctx(dev, &st_);
+    if (!ctx) return st_;
+    if (ctx->host_reserve(1) != HSVD_OK) return HSVD_ERR_CUDA;
+    HSVD_CUDA(cudaMemcpyAsync(ctx->host, status, 8, cudaMemcpyDeviceToHost, s));
+    HSVD_CUDA(cudaStreamSynchronize(s));
+    const int64_t st = ctx->host[0];
+    if (st) {
+        if (bad_col) *bad_col = st <= r ? st - 1 : st - r - 1;
+        set_error(st <= r ? "qr_shorten: dependent column" : "qr_shorten: R has a zero diagonal entry");
+        return HSVD_RANK_DEFICIENT;
+    }
+    if (bad_col) *bad_col = -1;
+    return HSVD_OK;
+}
+
+}  // extern "C"

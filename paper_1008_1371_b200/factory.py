@@ -4,7 +4,9 @@ Mirrors hjsvd.factory (/root/reference/pkg/src/hjsvd/factory.py): the same
 names, dataclasses, constants and exceptions.  ``bunch_parlett_factor`` runs
 the reference's complete-pivoting Bunch-Parlett factorization in
 double-double on the device (csrc/hsvd_factor.cu, C entry hsvd_bp_factor)
-and returns the reference's factor bit for bit.  The eigenvalues of M then
+and returns the reference's factor bit for bit.  ``qr_shorten`` is the
+reference's Householder QR of a tall factor on the device (hsvd_qr_shorten;
+plain fp64, equal to the reference's to rounding).  The eigenvalues of M
 come from the HSVD of (G, J): lambda = sigma^2 * j (``eigvalsh``).
 """
 
@@ -131,3 +133,34 @@ def eigvalsh(M, cfg=None):
     pair = bunch_parlett_factor(M)
     res = drive(pair.G, pair.J, cfg)
     return np.sort(res.lam)
+
+
+def qr_shorten(G):
+    """Householder QR of a tall factor (factory.py:300-334): G = Q R with R's
+    diagonal positive, on the GPU (hsvd_qr_shorten).  The HSVD of R then
+    gives the HSVD of G after premultiplying U by Q.  Returns (R, Q)."""
+    import torch
+
+    from .linalg import as_factor
+
+    G = as_factor(G)
+    n, r = G.shape
+    if n <= r:
+        raise ShapeError("qr_shorten needs n > r")
+    require_cuda()
+    L = _lib.load()
+    size = ctypes.c_size_t(0)
+    _lib.check(L.hsvd_qr_workspace_size(n, r, ctypes.byref(size)))
+    Gt = torch.from_numpy(np.ascontiguousarray(G.T)).cuda()  # row c = column c
+    ws = torch.empty(size.value, dtype=torch.uint8, device=Gt.device)
+    Rt = torch.empty((r, r), dtype=torch.float64, device=Gt.device)
+    Qt = torch.empty((r, n), dtype=torch.float64, device=Gt.device)
+    bad = ctypes.c_int64(-1)
+    st = L.hsvd_qr_shorten(ptr(Gt), n, r, n, ptr(Rt), r, ptr(Qt), n, ctypes.byref(bad), ptr(ws),
+                           size.value, stream_handle())
+    if st == _lib.HSVD_RANK_DEFICIENT:
+        from .errors import RankDeficiencyError
+        raise RankDeficiencyError(f"column {bad.value} is dependent" if bad.value >= 0
+                                  else _lib.last_error())
+    _lib.check(st)
+    return (np.asfortranarray(Rt.cpu().numpy().T), np.asfortranarray(Qt.cpu().numpy().T))

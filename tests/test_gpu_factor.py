@@ -69,3 +69,53 @@ def test_eigen_pipeline_end_to_end(mode):
     got = H.eigvalsh(M, cfg)
     err = np.max(np.abs(got - lam) / np.abs(lam))
     assert err <= 1e-12
+
+
+# ---- qr_shorten (test_factory.py:148-177, the reference's tolerances) ------
+def test_qr_orthonormal_input():
+    Q0 = np.linalg.qr(np.random.default_rng(0).standard_normal((6, 3)))[0]
+    R, Q = H.qr_shorten(Q0)
+    np.testing.assert_allclose(R, np.eye(3), atol=1e-14)
+
+
+def test_qr_single_column():
+    R, Q = H.qr_shorten(np.array([[3.0], [4.0]]))
+    np.testing.assert_allclose(R, [[5.0]], rtol=1e-15)
+    np.testing.assert_allclose(Q, [[0.6], [0.8]], rtol=1e-15)
+
+
+@pytest.mark.parametrize("shape", [(40, 12), (300, 100), (2048, 512)])
+def test_qr_residual_and_orthogonality(shape):
+    n, r = shape
+    G = np.random.default_rng(4).standard_normal((n, r))
+    R, Q = H.qr_shorten(G)
+    assert np.linalg.norm(Q @ R - G) <= 20.0 * n * H.EPS * np.linalg.norm(G)
+    assert np.linalg.norm(Q.T @ Q - np.eye(r)) <= n * n * H.EPS
+    assert np.all(np.diag(R) > 0.0)
+    np.testing.assert_allclose(R, np.triu(R), atol=0)
+    # the reference's R to rounding (same algorithm; numpy's BLAS sums differ)
+    if n <= 300:
+        sys.path.insert(0, os.path.dirname(HERE))
+        from oracle.qr_ref import qr_shorten_numpy
+        R0, Q0 = qr_shorten_numpy(G)
+        np.testing.assert_allclose(R, R0, rtol=0, atol=1e-12 * np.abs(R0).max())
+
+
+def test_qr_errors():
+    with pytest.raises(H.ShapeError):
+        H.qr_shorten(np.eye(3))
+    G = np.zeros((4, 2))
+    G[:, 0] = 1.0
+    with pytest.raises(H.RankDeficiencyError):
+        H.qr_shorten(G)
+
+
+def test_qr_then_hsvd_tall():
+    # the HSVD of a tall G through its R factor (factory.py:300-305)
+    rng = np.random.default_rng(9)
+    G = rng.standard_normal((96, 32))
+    J = H.SignatureVector.from_p(32, 20)
+    R, Q = H.qr_shorten(G)
+    a = H.drive(G, J)
+    b = H.drive(R, J)
+    np.testing.assert_allclose(np.sort(a.lam), np.sort(b.lam), rtol=1e-12)
