@@ -267,6 +267,12 @@ HSVD_API int hsvd_drive_sharded(void *comm, int32_t nshards, int32_t nlocal,
  * remaining pivot candidate is <= thresh.  ws: device workspace of
  * hsvd_bp_workspace_size bytes (4 n^2 doubles + O(n)). */
 HSVD_API int hsvd_bp_workspace_size(int64_t n, size_t *bytes);
+/* the same on an unrounded double-double M = (M, Mlo) (generate_factor_pair,
+ * factory.py:285-297, factorizes the generator's M before rounding) */
+HSVD_API int hsvd_bp_factor_dd(const double *M, const double *Mlo, int64_t n, int64_t ldm,
+                               double thresh, double *G, int64_t ldg, int8_t *signs,
+                               int64_t *perm, int64_t *p_out, int64_t *stage_out, void *ws,
+                               size_t ws_bytes, void *stream);
 HSVD_API int hsvd_bp_factor(const double *M, int64_t n, int64_t ldm, double thresh, double *G,
                             int64_t ldg, int8_t *signs, int64_t *perm, int64_t *p_out,
                             int64_t *stage_out, void *ws, size_t ws_bytes, void *stream);
@@ -280,6 +286,18 @@ HSVD_API int hsvd_qr_workspace_size(int64_t n, int64_t r, size_t *bytes);
 HSVD_API int hsvd_qr_shorten(const double *G, int64_t n, int64_t r, int64_t ldg, double *R,
                              int64_t ldr, double *Q, int64_t ldq, int64_t *bad_col, void *ws,
                              size_t ws_bytes, void *stream);
+
+/* Test-matrix generation in double-double (factory.py:79-101), bit-identical
+ * to the reference: hsvd_gen_init sets M = diag(lam) (device lam, Mh, Ml
+ * n x n row-major), hsvd_gen_reflect applies `count` Householder reflectors
+ * (device vs, count x n row-major, the reference's standard_normal draws),
+ * hsvd_gen_finish mirrors the upper triangle (np.triu(M) + np.triu(M, 1).T).
+ * n <= 16384 (the pairwise tree of a row stays on chip). */
+HSVD_API int hsvd_gen_workspace_size(int64_t n, size_t *bytes);
+HSVD_API int hsvd_gen_init(const double *lam, int64_t n, double *Mh, double *Ml, void *stream);
+HSVD_API int hsvd_gen_reflect(double *Mh, double *Ml, int64_t n, const double *vs, int64_t count,
+                              void *ws, size_t ws_bytes, void *stream);
+HSVD_API int hsvd_gen_finish(double *Mh, double *Ml, int64_t n, void *stream);
 
 /* The shard plan alone (host only, no GPU): the stepper of all slots, the
  * block placement and the per-step block moves, for tests of the exchange

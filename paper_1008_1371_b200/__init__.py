@@ -28,10 +28,13 @@ from .factory import (
     GAP,
     FactorPair,
     SpectrumSpec,
+    TestBundle,
     bunch_parlett_factor,
     bunch_parlett_factor_device,
     draw_spectrum,
     eigvalsh,
+    generate_factor_pair,
+    generate_symmetric,
     qr_shorten,
 )
 from .matio import read_csv_matrix, read_gjh, write_csv_matrix, write_gjh

@@ -38,7 +38,9 @@ EXPORTED = (
     "hsvd_shard_columns", "hsvd_sharded_workspace_size", "hsvd_drive_sharded",
     "hsvd_plan_create", "hsvd_plan_destroy", "hsvd_plan_advance", "hsvd_plan_state",
     "hsvd_plan_redistribute", "hsvd_plan_place",
-    "hsvd_bp_workspace_size", "hsvd_bp_factor", "hsvd_qr_workspace_size", "hsvd_qr_shorten",
+    "hsvd_bp_workspace_size", "hsvd_bp_factor", "hsvd_bp_factor_dd", "hsvd_qr_workspace_size",
+    "hsvd_qr_shorten", "hsvd_gen_workspace_size", "hsvd_gen_init", "hsvd_gen_reflect",
+    "hsvd_gen_finish",
 )
 
 
@@ -141,6 +143,12 @@ _SIGS = {
     "hsvd_bp_workspace_size": (ctypes.c_int, [_I64, _P]),
     "hsvd_bp_factor": (ctypes.c_int, [_P, _I64, _I64, _D, _P, _I64, _P, _P, _P, _P, _P,
                                       ctypes.c_size_t, _P]),
+    "hsvd_bp_factor_dd": (ctypes.c_int, [_P, _P, _I64, _I64, _D, _P, _I64, _P, _P, _P, _P, _P,
+                                         ctypes.c_size_t, _P]),
+    "hsvd_gen_workspace_size": (ctypes.c_int, [_I64, _P]),
+    "hsvd_gen_init": (ctypes.c_int, [_P, _I64, _P, _P, _P]),
+    "hsvd_gen_reflect": (ctypes.c_int, [_P, _P, _I64, _P, _I64, _P, ctypes.c_size_t, _P]),
+    "hsvd_gen_finish": (ctypes.c_int, [_P, _P, _I64, _P]),
     "hsvd_qr_workspace_size": (ctypes.c_int, [_I64, _I64, _P]),
     "hsvd_qr_shorten": (ctypes.c_int, [_P, _I64, _I64, _I64, _P, _I64, _P, _I64, _P, _P,
                                        ctypes.c_size_t, _P]),

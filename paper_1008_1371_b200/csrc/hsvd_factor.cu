@@ -180,14 +180,14 @@ __device__ void block_argmax(double &v, int64_t &i, double &v2, int64_t &i2)
 }
 
 // ---- setup ---------------------------------------------------------------------
-__global__ void k_bp_init(const double *M, int64_t ldm, int64_t n, BpWs w)
+__global__ void k_bp_init(const double *M, const double *Mlo, int64_t ldm, int64_t n, BpWs w)
 {
     const int64_t N = n * n;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < N;
          e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = e / n, j = e % n;
         w.Ah[e] = M[i * ldm + j];
-        w.Al[e] = 0.0;
+        w.Al[e] = Mlo ? Mlo[i * ldm + j] : 0.0;
         w.Lh[e] = i == j ? 1.0 : 0.0;
         w.Ll[e] = 0.0;
     }
@@ -562,9 +562,10 @@ HSVD_API int hsvd_bp_workspace_size(int64_t n, size_t *bytes)
     return HSVD_OK;
 }
 
-HSVD_API int hsvd_bp_factor(const double *M, int64_t n, int64_t ldm, double thresh, double *G,
-                            int64_t ldg, int8_t *signs, int64_t *perm, int64_t *p_out,
-                            int64_t *stage_out, void *ws, size_t ws_bytes, void *stream)
+HSVD_API int hsvd_bp_factor_dd(const double *M, const double *Mlo, int64_t n, int64_t ldm,
+                               double thresh, double *G, int64_t ldg, int8_t *signs,
+                               int64_t *perm, int64_t *p_out, int64_t *stage_out, void *ws,
+                               size_t ws_bytes, void *stream)
 {
     if (!M || !G || !signs || !perm || !p_out || n < 1 || ldm < n || ldg < n || !ws) {
         set_error("hsvd_bp_factor: bad arguments");
@@ -586,7 +587,7 @@ HSVD_API int hsvd_bp_factor(const double *M, int64_t n, int64_t ldm, double thre
     int64_t *hbuf = ctx->host;  // pinned
     const double alpha = (1.0 + sqrt(17.0)) / 8.0;
 
-    k_bp_init<<<1184, 256, 0, s>>>(M, ldm, n, w);
+    k_bp_init<<<1184, 256, 0, s>>>(M, Mlo, ldm, n, w);
     k_bp_init_state<<<1, 256, 0, s>>>(n, w, perm);
     k_bp_search<<<(unsigned)tri_count(n), UPD_THREADS, 0, s>>>(n, w);
     HSVD_LAUNCH_CHECK("k_bp_search");
@@ -625,6 +626,14 @@ HSVD_API int hsvd_bp_factor(const double *M, int64_t n, int64_t ldm, double thre
     *p_out = hs.p;
     if (stage_out) *stage_out = -1;
     return HSVD_OK;
+}
+
+HSVD_API int hsvd_bp_factor(const double *M, int64_t n, int64_t ldm, double thresh, double *G,
+                            int64_t ldg, int8_t *signs, int64_t *perm, int64_t *p_out,
+                            int64_t *stage_out, void *ws, size_t ws_bytes, void *stream)
+{
+    return hsvd_bp_factor_dd(M, nullptr, n, ldm, thresh, G, ldg, signs, perm, p_out, stage_out, ws,
+                             ws_bytes, stream);
 }
 
 }  // extern "C"
@@ -804,6 +813,256 @@ HSVD_API int hsvd_qr_shorten(const double *G, int64_t n, int64_t r, int64_t ldg,
         return HSVD_RANK_DEFICIENT;
     }
     if (bad_col) *bad_col = -1;
+    return HSVD_OK;
+}
+
+}  // extern "C"
+
+// ===========================================================================
+// Test-matrix generation in double-double (hjsvd.factory._generate_dd,
+// factory.py:79-101): M = Q diag(lam) Q^T with Q a product of n - 1 random
+// Householder reflectors, every operation the reference's dd primitive, so
+// M (hi, lo) is bit-identical.  Per reflector v (drawn by the host from the
+// reference's numpy stream):
+//   beta  = 2 / tree_sum(two_prod(v, v))            k_gen_scalars (1 CTA)
+//   w_i   = tree_sum_j mul_f(M_ij, v_j)             k_gen_matvec (CTA/row)
+//   alpha = tree_sum(mul_f(w, v)), gamma = beta^2 alpha   k_gen_scalars
+//   M_ij  = (M_ij - (vw + wv)_ij beta) + two_prod(v_i, v_j) gamma
+//                                                   k_gen_update
+// tree_sum is the reference's pairwise reduction (_dd.py:96-110): pairs
+// (0,1), (2,3), ..., an odd last element carried to the end of the level.
+// ===========================================================================
+namespace hsvd {
+namespace {
+
+constexpr int GEN_THREADS = 1024;
+constexpr int GEN_MAXP = 8;  // pairs per thread per level: n <= 2 * 16 * 1024
+
+// pairwise tree over (h, l)[0, m) in shared memory (all threads of the CTA)
+__device__ dd tree_sum_smem(double *h, double *l, int m)
+{
+    while (m > 1) {
+        const int half = m >> 1;
+        dd r[GEN_MAXP];
+#pragma unroll
+        for (int k = 0; k < GEN_MAXP; ++k) {
+            const int t = threadIdx.x + k * GEN_THREADS;
+            if (t < half) r[k] = dd_add(dd{h[2 * t], l[2 * t]}, dd{h[2 * t + 1], l[2 * t + 1]});
+        }
+        dd carry = {0.0, 0.0};
+        if ((m & 1) && threadIdx.x == 0) carry = dd{h[m - 1], l[m - 1]};
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < GEN_MAXP; ++k) {
+            const int t = threadIdx.x + k * GEN_THREADS;
+            if (t < half) {
+                h[t] = r[k].h;
+                l[t] = r[k].l;
+            }
+        }
+        if ((m & 1) && threadIdx.x == 0) {
+            h[half] = carry.h;
+            l[half] = carry.l;
+        }
+        __syncthreads();
+        m = half + (m & 1);
+    }
+    return dd{h[0], l[0]};
+}
+
+// level 0 of the tree computed while loading: pair t = (x[2t], x[2t+1]);
+// returns the length of level 1 (entries in h, l)
+template <class F>
+__device__ int tree_first_level(double *h, double *l, int m, F term)
+{
+    const int half = m >> 1;
+    for (int t = threadIdx.x; t < half; t += GEN_THREADS) {
+        const dd r = dd_add(term(2 * t), term(2 * t + 1));
+        h[t] = r.h;
+        l[t] = r.l;
+    }
+    if ((m & 1) && threadIdx.x == 0) {
+        const dd c = term(m - 1);
+        h[half] = c.h;
+        l[half] = c.l;
+    }
+    __syncthreads();
+    return half + (m & 1);
+}
+
+struct GenWs {
+    double *wh, *wl;  // M v
+    dd *sc;           // beta, alpha, gamma
+};
+
+__global__ void k_gen_init(const double *lam, int64_t n, double *Mh, double *Ml)
+{
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * n;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e / n, j = e % n;
+        Mh[e] = i == j ? lam[i] : 0.0;
+        Ml[e] = 0.0;
+    }
+}
+
+// which = 0: beta = div(2, tree_sum(two_prod(v, v)));
+// which = 1: alpha = tree_sum(mul_f(w, v)), gamma = mul(mul(beta, beta), alpha)
+__global__ void __launch_bounds__(GEN_THREADS) k_gen_scalars(const double *v, int64_t n, GenWs g,
+                                                             int which)
+{
+    extern __shared__ double gsm[];
+    double *h = gsm, *l = gsm + (n + 1) / 2;
+    int m;
+    if (which == 0)
+        m = tree_first_level(h, l, (int)n, [&](int j) { return two_prod(v[j], v[j]); });
+    else
+        m = tree_first_level(h, l, (int)n,
+                             [&](int j) { return dd_mul_f(dd{g.wh[j], g.wl[j]}, v[j]); });
+    const dd s = tree_sum_smem(h, l, m);
+    if (threadIdx.x == 0) {
+        if (which == 0) {
+            g.sc[0] = dd_div(dd{2.0, 0.0}, s);
+        } else {
+            const dd beta = g.sc[0];
+            g.sc[1] = s;
+            g.sc[2] = dd_mul(dd_mul(beta, beta), s);
+        }
+    }
+}
+
+// w_i = tree_sum_j mul_f(M_ij, v_j), one CTA per row
+__global__ void __launch_bounds__(GEN_THREADS) k_gen_matvec(const double *Mh, const double *Ml,
+                                                            const double *v, int64_t n, GenWs g)
+{
+    extern __shared__ double gsm[];
+    double *h = gsm, *l = gsm + (n + 1) / 2;
+    const int64_t i = blockIdx.x;
+    const double *rh = Mh + i * n, *rl = Ml + i * n;
+    const int m = tree_first_level(h, l, (int)n, [&](int j) { return dd_mul_f(dd{rh[j], rl[j]}, v[j]); });
+    const dd s = tree_sum_smem(h, l, m);
+    if (threadIdx.x == 0) {
+        g.wh[i] = s.h;
+        g.wl[i] = s.l;
+    }
+}
+
+// M = add(sub(M, S), T), S = mul(add(vw, wv), beta), T = mul(two_prod(v_i, v_j), gamma)
+__global__ void k_gen_update(double *Mh, double *Ml, const double *v, int64_t n, GenWs g)
+{
+    const dd beta = g.sc[0], gamma = g.sc[2];
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * n;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e / n, j = e % n;
+        const double vi = v[i], vj = v[j];
+        const dd wi = {g.wh[i], g.wl[i]}, wj = {g.wh[j], g.wl[j]};
+        const dd vw = dd_mul_f(wj, vi), wv = dd_mul_f(wi, vj);
+        const dd S = dd_mul(dd_add(vw, wv), beta);
+        const dd T = dd_mul(two_prod(vi, vj), gamma);
+        const dd r = dd_add(dd_sub(dd{Mh[e], Ml[e]}, S), T);
+        Mh[e] = r.h;
+        Ml[e] = r.l;
+    }
+}
+
+// Mh = triu(Mh) + triu(Mh, 1)^T (and Ml): the upper triangle mirrored, + 0.0
+__global__ void k_gen_finish(double *Mh, double *Ml, int64_t n)
+{
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * n;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e / n, j = e % n;
+        if (i > j) {
+            Mh[e] = __dadd_rn(0.0, Mh[j * n + i]);
+            Ml[e] = __dadd_rn(0.0, Ml[j * n + i]);
+        }
+    }
+    // the upper triangle gets + 0.0 in a second pass (after every mirror read)
+}
+__global__ void k_gen_finish_upper(double *Mh, double *Ml, int64_t n)
+{
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * n;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e / n, j = e % n;
+        if (i <= j) {
+            Mh[e] = __dadd_rn(Mh[e], 0.0);
+            Ml[e] = __dadd_rn(Ml[e], 0.0);
+        }
+    }
+}
+
+}  // namespace
+}  // namespace hsvd
+
+extern "C" {
+
+HSVD_API int hsvd_gen_workspace_size(int64_t n, size_t *bytes)
+{
+    if (n < 2 || !bytes) {
+        set_error("hsvd_gen_workspace_size: bad arguments");
+        return HSVD_ERR_ARG;
+    }
+    *bytes = 2 * align256((size_t)n * 8) + align256(3 * sizeof(dd));
+    return HSVD_OK;
+}
+
+HSVD_API int hsvd_gen_init(const double *lam, int64_t n, double *Mh, double *Ml, void *stream)
+{
+    if (!lam || !Mh || !Ml || n < 2) {
+        set_error("hsvd_gen_init: bad arguments");
+        return HSVD_ERR_ARG;
+    }
+    k_gen_init<<<1184, 256, 0, (cudaStream_t)stream>>>(lam, n, Mh, Ml);
+    HSVD_LAUNCH_CHECK("k_gen_init");
+    return HSVD_OK;
+}
+
+HSVD_API int hsvd_gen_reflect(double *Mh, double *Ml, int64_t n, const double *vs, int64_t count,
+                              void *ws, size_t ws_bytes, void *stream)
+{
+    size_t need = 0;
+    if (!Mh || !Ml || !vs || !ws || n < 2 || hsvd_gen_workspace_size(n, &need) != HSVD_OK ||
+        ws_bytes < need) {
+        set_error("hsvd_gen_reflect: bad arguments");
+        return HSVD_ERR_ARG;
+    }
+    const size_t smem = 2 * (size_t)((n + 1) / 2) * 8;
+    if (n > 2 * GEN_MAXP * GEN_THREADS || smem > 200 * 1024) {
+        set_error("hsvd_gen_reflect: n too large for the on-chip pairwise tree");
+        return HSVD_ERR_UNSUPPORTED;
+    }
+    static bool attr = false;
+    if (!attr) {
+        HSVD_CUDA(cudaFuncSetAttribute(k_gen_scalars, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       200 * 1024));
+        HSVD_CUDA(cudaFuncSetAttribute(k_gen_matvec, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       200 * 1024));
+        attr = true;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    unsigned char *b = (unsigned char *)ws;
+    GenWs g;
+    g.wh = (double *)b;
+    g.wl = (double *)(b + align256((size_t)n * 8));
+    g.sc = (dd *)(b + 2 * align256((size_t)n * 8));
+    for (int64_t q = 0; q < count; ++q) {
+        const double *v = vs + q * n;
+        k_gen_scalars<<<1, GEN_THREADS, smem, s>>>(v, n, g, 0);
+        k_gen_matvec<<<(unsigned)n, GEN_THREADS, smem, s>>>(Mh, Ml, v, n, g);
+        k_gen_scalars<<<1, GEN_THREADS, smem, s>>>(v, n, g, 1);
+        k_gen_update<<<1184, 256, 0, s>>>(Mh, Ml, v, n, g);
+    }
+    HSVD_LAUNCH_CHECK("k_gen_update");
+    return HSVD_OK;
+}
+
+HSVD_API int hsvd_gen_finish(double *Mh, double *Ml, int64_t n, void *stream)
+{
+    if (!Mh || !Ml || n < 2) {
+        set_error("hsvd_gen_finish: bad arguments");
+        return HSVD_ERR_ARG;
+    }
+    k_gen_finish<<<1184, 256, 0, (cudaStream_t)stream>>>(Mh, Ml, n);
+    k_gen_finish_upper<<<1184, 256, 0, (cudaStream_t)stream>>>(Mh, Ml, n);
+    HSVD_LAUNCH_CHECK("k_gen_finish");
     return HSVD_OK;
 }
 

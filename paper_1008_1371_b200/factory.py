@@ -58,6 +58,19 @@ class FactorPair:
     perm: np.ndarray = None
 
 
+@dataclass(frozen=True)
+class TestBundle:
+    """One generated instance: matrix, exact spectrum, and its factor
+    (factory.py:60-66)."""
+
+    __test__ = False  # not a pytest class
+
+    M: np.ndarray
+    lambda_true: np.ndarray  # sorted ascending
+    factor: FactorPair
+    spec: SpectrumSpec = None
+
+
 def draw_spectrum(spec, rng):
     """Eigenvalues honoring the spectral gap (factory.py:69-76)."""
     mags = rng.uniform(spec.a * GAP, spec.a, spec.n)
@@ -164,3 +177,76 @@ def qr_shorten(G):
                                   else _lib.last_error())
     _lib.check(st)
     return (np.asfortranarray(Rt.cpu().numpy().T), np.asfortranarray(Qt.cpu().numpy().T))
+
+
+def _generate_dd_device(lam, rng, identity_q=False, chunk=64):
+    """M = Q diag(lam) Q^T in double-double on the device (factory.py:79-101):
+    the n - 1 reflector vectors are the reference's rng.standard_normal(n)
+    draws, streamed to the device in chunks.  Returns (Mh, Ml) torch (n, n)."""
+    import torch
+
+    require_cuda()
+    L = _lib.load()
+    lam = np.ascontiguousarray(lam, dtype=np.float64)
+    n = lam.shape[0]
+    dev = torch.device("cuda", torch.cuda.current_device())
+    Mh = torch.empty((n, n), dtype=torch.float64, device=dev)
+    Ml = torch.empty((n, n), dtype=torch.float64, device=dev)
+    lam_t = torch.from_numpy(lam).to(dev)
+    s = stream_handle()
+    _lib.check(L.hsvd_gen_init(ptr(lam_t), n, ptr(Mh), ptr(Ml), s))
+    if identity_q:
+        return Mh, Ml
+    size = ctypes.c_size_t(0)
+    _lib.check(L.hsvd_gen_workspace_size(n, ctypes.byref(size)))
+    ws = torch.empty(size.value, dtype=torch.uint8, device=dev)
+    left = n - 1
+    while left > 0:
+        cnt = min(chunk, left)
+        V = np.stack([rng.standard_normal(n) for _ in range(cnt)])
+        Vt = torch.from_numpy(V).to(dev)
+        _lib.check(L.hsvd_gen_reflect(ptr(Mh), ptr(Ml), n, ptr(Vt), cnt, ptr(ws), size.value, s))
+        left -= cnt
+    _lib.check(L.hsvd_gen_finish(ptr(Mh), ptr(Ml), n, s))
+    return Mh, Ml
+
+
+def generate_symmetric(spec, eigenvalues=None, identity_q=False):
+    """Generate (M, lambda_true) (factory.py:104-114): M exactly symmetric
+    with the drawn (or given) spectrum, built in double-double on the GPU
+    and rounded to float64; bit-identical to the reference."""
+    rng = np.random.default_rng(spec.seed)
+    lam = draw_spectrum(spec, rng) if eigenvalues is None else \
+        np.asarray(eigenvalues, dtype=np.float64)
+    Mh, Ml = _generate_dd_device(lam, rng, identity_q)
+    M = (Mh + Ml).cpu().numpy()
+    return M, np.sort(lam)
+
+
+def generate_factor_pair(spec, identity_q=False):
+    """Full pipeline (factory.py:285-297): spectrum -> M -> (G, J), chained in
+    double-double on the GPU (the factorization consumes the unrounded M)."""
+    rng = np.random.default_rng(spec.seed)
+    lam = draw_spectrum(spec, rng)
+    Mh, Ml = _generate_dd_device(lam, rng, identity_q)
+    n = lam.shape[0]
+    Mh_np = Mh.cpu().numpy()
+    thresh = n * EPS * np.linalg.norm(Mh_np, "fro")
+    L = _lib.load()
+    import torch
+
+    size = ctypes.c_size_t(0)
+    _lib.check(L.hsvd_bp_workspace_size(n, ctypes.byref(size)))
+    ws = torch.empty(size.value, dtype=torch.uint8, device=Mh.device)
+    Gt = torch.empty((n, n), dtype=torch.float64, device=Mh.device)
+    signs = torch.empty(n, dtype=torch.int8, device=Mh.device)
+    perm = torch.empty(n, dtype=torch.int64, device=Mh.device)
+    p = ctypes.c_int64(0)
+    stage = ctypes.c_int64(-1)
+    _lib.check(L.hsvd_bp_factor_dd(ptr(Mh), ptr(Ml), n, n, float(thresh), ptr(Gt), n,
+                                   ptr(signs), ptr(perm), ctypes.byref(p), ctypes.byref(stage),
+                                   ptr(ws), size.value, stream_handle()))
+    G = np.asfortranarray(Gt.cpu().numpy().T)
+    factor = FactorPair(G, SignatureVector.from_p(n, int(p.value)), perm.cpu().numpy())
+    M = (Mh + Ml).cpu().numpy()
+    return TestBundle(M, np.sort(lam), factor, spec)

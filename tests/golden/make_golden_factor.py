@@ -27,6 +27,8 @@ from digest import digest  # noqa: E402
 from factor_inputs import make_input  # noqa: E402
 
 SPECTRA = [(16, 2), (64, 7), (128, 9)]
+GEN = [(16, 21, None), (33, 3, None), (64, 17, 10), (100, 23, None), (128, 1, None),
+       (40, 3, 0), (24, 5, 24)]
 CASES = [("diag", 2, 0), ("offdiag", 2, 0), ("sym", 5, 1), ("sym", 33, 3), ("sym", 200, 4),
          ("sym", 256, 5), ("smalldiag", 100, 6), ("smalldiag", 257, 8), ("ints", 40, 10),
          ("ints", 96, 11)] + [("spectrum", n, s) for n, s in SPECTRA]
@@ -51,9 +53,23 @@ def main():
             "p": int(pair.J.p),
         })
         print(kind, n, seed, out[-1]["p"])
+    gen = []
+    for n, seed, pos in GEN:
+        spec = hjsvd.SpectrumSpec(n, 20.0, seed, pos)
+        M, lam = hjsvd.generate_symmetric(spec)
+        b = hjsvd.generate_factor_pair(spec)
+        gen.append({
+            "n": n, "seed": seed, "pos_count": pos, "M": digest(M), "lam": digest(lam),
+            "bundle_M": digest(b.M), "G": digest(b.factor.G),
+            "perm": hashlib.sha256(np.asarray(b.factor.perm, "<i8").tobytes()).hexdigest(),
+            "p": int(b.factor.J.p),
+        })
+        print("gen", n, seed, pos, gen[-1]["p"])
     with open(os.path.join(HERE, "factor.json"), "w") as f:
-        json.dump({"reference": "hjsvd.factory.bunch_parlett_factor (factory.py:270-282)",
-                   "singular": {"kind": "ones", "n": 3}, "cases": out}, f, indent=1)
+        json.dump({"reference": "hjsvd.factory.bunch_parlett_factor (factory.py:270-282); "
+                                "generate_symmetric / generate_factor_pair (factory.py:104-114, "
+                                "285-297)",
+                   "singular": {"kind": "ones", "n": 3}, "cases": out, "gen": gen}, f, indent=1)
 
 
 if __name__ == "__main__":

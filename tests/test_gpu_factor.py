@@ -119,3 +119,33 @@ def test_qr_then_hsvd_tall():
     a = H.drive(G, J)
     b = H.drive(R, J)
     np.testing.assert_allclose(np.sort(a.lam), np.sort(b.lam), rtol=1e-12)
+
+
+# ---- generation in double-double (factory.py:79-114, 285-297) --------------
+@pytest.mark.parametrize("case", GOLD["gen"], ids=lambda c: f"gen-{c['n']}-{c['seed']}-{c['pos_count']}")
+def test_generate_bit_exact(case):
+    spec = H.SpectrumSpec(case["n"], 20.0, case["seed"], case["pos_count"])
+    M, lam = H.generate_symmetric(spec)
+    assert digest(M) == case["M"]
+    assert digest(lam) == case["lam"]
+    b = H.generate_factor_pair(spec)
+    assert digest(b.M) == case["bundle_M"]
+    assert digest(b.factor.G) == case["G"]
+    assert hashlib.sha256(np.asarray(b.factor.perm, "<i8").tobytes()).hexdigest() == case["perm"]
+    assert b.factor.J.p == case["p"]
+
+
+def test_generate_end_to_end_eigenvalues():
+    # test_factory.py:134-139 at the reference's size
+    b = H.generate_factor_pair(H.SpectrumSpec(160, 20.0, 1))
+    res = H.drive(b.factor.G, b.factor.J)
+    err = np.max(np.abs(np.sort(res.lam) - b.lambda_true) / np.abs(b.lambda_true))
+    assert err <= 1e-12
+    assert b.factor.J.p == np.count_nonzero(b.lambda_true > 0)
+
+
+def test_generate_identity_q():
+    M, lam = H.generate_symmetric(H.SpectrumSpec(6, 20.0, 0), eigenvalues=[3.0, -1.0, 2.0, 5.0, -4.0, 1.0],
+                                  identity_q=True)
+    np.testing.assert_array_equal(M, np.diag([3.0, -1.0, 2.0, 5.0, -4.0, 1.0]))
+    np.testing.assert_array_equal(lam, np.sort([3.0, -1.0, 2.0, 5.0, -4.0, 1.0]))
