@@ -1,15 +1,14 @@
-"""Command-line front end of the solver path: ``hsvd`` and ``eig`` on a
-bundle directory, as the reference's (/root/reference/pkg/src/hjsvd/cli.py:
-107-158, 240-250), with the same files, RunRecord CSV and exit codes, plus
-the B200 flags --mode, --block-cols and --shards.
+"""Command-line front end, as the reference's (/root/reference/pkg/src/hjsvd/
+cli.py): ``gen``, ``factor``, ``hsvd``, ``eig`` and ``bench`` with the same
+files (GJH1 bundles, CSV manifests and RunRecord rows), arguments and exit
+codes, plus the B200 flags --mode, --block-cols and --shards.
 
+    python -m paper_1008_1371_b200.cli gen --n 512 --seed 1 --out BUNDLE
     python -m paper_1008_1371_b200.cli eig --in BUNDLE --out RESULT [--mode block]
 
-BUNDLE holds G.gjh (and optionally lambda_true.csv); RESULT receives
-sigma.csv, lambda.csv, U.gjh, V.gjh (unless --no-accumulate-v) and
-record.csv.  The reference's gen / factor / bench / check-strategy commands
-drive its test-matrix factory and strategy lab, which are outside this
-package's scope.
+gen/factor run the GPU factory (factory.py: double-double generator and
+Bunch-Parlett, bit-identical to the reference's).  The strategy lab
+(check-strategy) is outside this package's scope.
 """
 
 import argparse
@@ -21,6 +20,7 @@ from dataclasses import dataclass, fields
 import numpy as np
 
 from .errors import DefinitenessLostError, NumericalSingularityError, ShapeError
+from .factory import SpectrumSpec, bunch_parlett_factor, generate_factor_pair
 from .linalg import SignatureVector, orthonormality_distance
 from .matio import read_csv_matrix, read_gjh, write_csv_matrix, write_gjh
 from .solver import SolverConfig, border, drive, recover_V, strip_bordered
@@ -76,6 +76,64 @@ def read_bundle(path):
     return G, J, lam
 
 
+def write_bundle(out, bundle):
+    """Bundle directory of a generated instance (cli.py:72-82)."""
+    os.makedirs(out, exist_ok=True)
+    spec = bundle.spec
+    p = bundle.factor.J.p
+    write_gjh(os.path.join(out, "M.gjh"), bundle.M, p)
+    write_gjh(os.path.join(out, "G.gjh"), bundle.factor.G, p)
+    write_csv_matrix(os.path.join(out, "lambda_true.csv"), bundle.lambda_true[np.newaxis, :])
+    with open(os.path.join(out, "manifest.csv"), "w") as fh:
+        fh.write("seed,n,a,p\n")
+        fh.write(f"{spec.seed},{spec.n},{spec.a:.17g},{p}\n")
+
+
+def cmd_gen(args):
+    """cli.py:92-98: generate a test bundle (GPU factory)."""
+    spec = SpectrumSpec(args.n, args.a, args.seed, args.pos_count)
+    bundle = generate_factor_pair(spec)
+    write_bundle(args.out, bundle)
+    print(f"gen: wrote bundle to {args.out} (n={spec.n}, a={spec.a}, "
+          f"seed={spec.seed}, p={bundle.factor.J.p})")
+    return EXIT_OK
+
+
+def cmd_factor(args):
+    """cli.py:101-106: factor a symmetric GJH1 matrix (GPU Bunch-Parlett)."""
+    M, _ = read_gjh(args.infile)
+    pair = bunch_parlett_factor(M)
+    write_gjh(args.out, pair.G, pair.J.p)
+    print(f"factor: wrote {args.out} (n={M.shape[0]}, p={pair.J.p})")
+    return EXIT_OK
+
+
+def cmd_bench(args):
+    """cli.py:198-222: sweep/time/error table across orders, inertias and
+    sorting, on GPU-generated bundles (plus --mode)."""
+    orders = [int(x) for x in args.orders.split(",")]
+    records = []
+    for n in orders:
+        if n % 2 != 0:
+            raise ShapeError("bench orders must be even")
+        for p in (0, max(1, n // 16), n // 2):
+            bundle = generate_factor_pair(SpectrumSpec(n, args.a, args.seed, pos_count=p))
+            for sort in (True, False):
+                cfg = SolverConfig(workers=args.workers, sort=sort, mode=args.mode)
+                for _ in range(args.repeats):
+                    t0 = time.perf_counter()
+                    result = drive(bundle.factor.G, bundle.factor.J, cfg)
+                    wall = time.perf_counter() - t0
+                    lt = np.sort(bundle.lambda_true)
+                    err = float(np.max(np.abs(np.sort(result.lam) - lt) / np.abs(lt)))
+                    records.append(RunRecord(n, n, p, result.sweeps_used, result.stop_reason,
+                                             wall, err, orthonormality_distance(result.U),
+                                             result.rotations, result.skips, sort))
+    write_records(args.out, records)
+    print(f"bench: wrote {len(records)} rows to {args.out}")
+    return EXIT_OK
+
+
 def solver_config(args):
     return SolverConfig(max_sweeps=args.max_sweeps,
                         accumulate_v=not args.no_accumulate_v,
@@ -129,6 +187,26 @@ def build_parser():
     ap = argparse.ArgumentParser(prog="hsvd-b200",
                                  description="B200 hyperbolic SVD solver (hjsvd drop-in)")
     sub = ap.add_subparsers(dest="command", required=True)
+    sp = sub.add_parser("gen", help="generate a test bundle")
+    sp.add_argument("--n", type=int, required=True)
+    sp.add_argument("--a", type=float, default=20.0)
+    sp.add_argument("--seed", type=int, required=True)
+    sp.add_argument("--pos-count", dest="pos_count", type=int, default=None)
+    sp.add_argument("--out", required=True)
+    sp.set_defaults(func=cmd_gen)
+    sp = sub.add_parser("factor", help="factor a symmetric GJH1 matrix")
+    sp.add_argument("--in", dest="infile", required=True)
+    sp.add_argument("--out", required=True)
+    sp.set_defaults(func=cmd_factor)
+    sp = sub.add_parser("bench", help="sweep/time/error table across configs")
+    sp.add_argument("--orders", required=True, help="comma-separated even orders")
+    sp.add_argument("--a", type=float, default=20.0)
+    sp.add_argument("--seed", type=int, required=True)
+    sp.add_argument("--repeats", type=int, default=1)
+    sp.add_argument("--workers", type=int, default=1)
+    sp.add_argument("--mode", choices=("pointwise", "block"), default="pointwise")
+    sp.add_argument("--out", required=True)
+    sp.set_defaults(func=cmd_bench)
     for name in ("hsvd", "eig"):
         sp = sub.add_parser(name, help=f"run the {name} solver on a bundle")
         sp.add_argument("--in", dest="infile", required=True)

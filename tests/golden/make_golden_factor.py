@@ -65,11 +65,25 @@ def main():
             "p": int(b.factor.J.p),
         })
         print("gen", n, seed, pos, gen[-1]["p"])
+    # the reference's `gen` bundle files, byte for byte
+    import tempfile
+    from hjsvd.cli import main as ref_cli
+    cli = []
+    for n, seed, pos in [(48, 5, None), (30, 2, 7)]:
+        with tempfile.TemporaryDirectory() as d:
+            args = ["gen", "--n", str(n), "--seed", str(seed), "--out", d]
+            if pos is not None:
+                args += ["--pos-count", str(pos)]
+            assert ref_cli(args) == 0
+            files = {f: hashlib.sha256(open(os.path.join(d, f), "rb").read()).hexdigest()
+                     for f in sorted(os.listdir(d))}
+        cli.append({"n": n, "seed": seed, "pos_count": pos, "files": files})
     with open(os.path.join(HERE, "factor.json"), "w") as f:
         json.dump({"reference": "hjsvd.factory.bunch_parlett_factor (factory.py:270-282); "
                                 "generate_symmetric / generate_factor_pair (factory.py:104-114, "
                                 "285-297)",
-                   "singular": {"kind": "ones", "n": 3}, "cases": out, "gen": gen}, f, indent=1)
+                   "singular": {"kind": "ones", "n": 3}, "cases": out, "gen": gen, "cli_gen": cli},
+                  f, indent=1)
 
 
 if __name__ == "__main__":

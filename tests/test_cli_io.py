@@ -136,3 +136,47 @@ def test_hsvd_block_and_shards(tmp_path):
                    "--block-cols", 16, *extra) == 0
         rec = (out / "record.csv").read_text().splitlines()[1].split(",")
         assert float(rec[6]) <= 1e-10  # max_rel_eig_err against lambda_true
+
+
+# ---- gen / factor / bench (cli.py:92-106, 198-222) --------------------------
+import hashlib  # noqa: E402
+import json  # noqa: E402
+
+_GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "factor.json")))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", _GOLD["cli_gen"], ids=lambda c: f"gen-{c['n']}-{c['seed']}")
+def test_gen_bundle_byte_identical(tmp_path, case):
+    args = ["gen", "--n", case["n"], "--seed", case["seed"], "--out", tmp_path / "b"]
+    if case["pos_count"] is not None:
+        args += ["--pos-count", case["pos_count"]]
+    assert run(*args) == 0
+    for name, h in case["files"].items():
+        assert hashlib.sha256((tmp_path / "b" / name).read_bytes()).hexdigest() == h, name
+
+
+@pytest.mark.gpu
+def test_gen_factor_eig_pipeline(tmp_path):
+    assert run("gen", "--n", 64, "--seed", 3, "--out", tmp_path / "b") == 0
+    # factor M.gjh again: the same G as the bundle's (rounded M in, so the
+    # factor may differ from G.gjh in the last bits; check the eigenvalues)
+    assert run("factor", "--in", tmp_path / "b" / "M.gjh", "--out", tmp_path / "G2.gjh") == 0
+    assert run("eig", "--in", tmp_path / "b", "--out", tmp_path / "r", "--mode", "block",
+               "--block-cols", 16) == 0
+    lam = np.sort(read_csv_matrix(tmp_path / "r" / "lambda.csv").ravel())
+    lt = np.sort(read_csv_matrix(tmp_path / "b" / "lambda_true.csv").ravel())
+    assert np.max(np.abs(lam - lt) / np.abs(lt)) <= 1e-12
+
+
+@pytest.mark.gpu
+def test_bench_records(tmp_path):
+    assert run("bench", "--orders", "16,32", "--seed", 1, "--out", tmp_path / "rec.csv") == 0
+    rows = (tmp_path / "rec.csv").read_text().splitlines()
+    assert rows[0].startswith("n,r,p,sweeps") and len(rows) == 1 + 2 * 3 * 2
+
+
+@pytest.mark.gpu
+def test_factor_singular_exit_4(tmp_path):
+    write_gjh(tmp_path / "M.gjh", np.ones((3, 3)), 3)
+    assert run("factor", "--in", tmp_path / "M.gjh", "--out", tmp_path / "G.gjh") == 4
