@@ -79,6 +79,25 @@ __device__ __forceinline__ dd dd_mul(dd x, dd y)
     const dd p = two_prod(x.h, y.h);
     return quick_two_sum(p.h, __dadd_rn(p.l, __dadd_rn(__dmul_rn(x.h, y.l), __dmul_rn(x.l, y.h))));
 }
+// dd_mul with the Dekker splits of x.h and y.h supplied (the same operations:
+// the update kernel splits each row's and column's pivot vectors once)
+struct sp2 {
+    double h, l;
+};
+__device__ __forceinline__ sp2 split2(double a)
+{
+    sp2 r;
+    split(a, r.h, r.l);
+    return r;
+}
+__device__ __forceinline__ dd dd_mul_s(dd x, sp2 xs, dd y, sp2 ys)
+{
+    const double p = __dmul_rn(x.h, y.h);
+    const double e = __dadd_rn(__dadd_rn(__dadd_rn(__dsub_rn(__dmul_rn(xs.h, ys.h), p), __dmul_rn(xs.h, ys.l)),
+                                         __dmul_rn(xs.l, ys.h)),
+                               __dmul_rn(xs.l, ys.l));
+    return quick_two_sum(p, __dadd_rn(e, __dadd_rn(__dmul_rn(x.h, y.l), __dmul_rn(x.l, y.h))));
+}
 __device__ __forceinline__ dd dd_mul_f(dd x, double f)
 {
     const dd p = two_prod(x.h, f);
@@ -121,7 +140,7 @@ __device__ __forceinline__ bool better(double v, int64_t i, double bv, int64_t b
 
 constexpr int TB = 64;          // update tile
 constexpr int UPD_THREADS = 256;
-constexpr int PIV_THREADS = 1024;
+constexpr int PIV_THREADS = 512;
 
 struct BpWs {
     double *Ah, *Al, *Lh, *Ll;
@@ -228,21 +247,41 @@ __global__ void __launch_bounds__(UPD_THREADS) k_bp_search(int64_t n, BpWs w)
 
 // symmetric swap of rows/columns a and b inside the trailing block [k:]
 // (_swap_sym, factory.py:117-121) plus the rows of L left of k and perm
+// swap X[a-th and b-th elements] of cnt strided pairs, hi and lo: all loads
+// of a chunk are issued before its stores (memory-level parallelism)
+__device__ __forceinline__ void swap_pairs(double *H, double *Lo, int64_t pa, int64_t pb,
+                                           int64_t stride, int64_t cnt)
+{
+    constexpr int U = 8;
+    for (int64_t e0 = threadIdx.x; e0 < cnt; e0 += U * (int64_t)blockDim.x) {
+        double xh[U], yh[U], xl[U], yl[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t e = e0 + u * (int64_t)blockDim.x;
+            if (e < cnt) {
+                xh[u] = H[pa + e * stride]; yh[u] = H[pb + e * stride];
+                xl[u] = Lo[pa + e * stride]; yl[u] = Lo[pb + e * stride];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t e = e0 + u * (int64_t)blockDim.x;
+            if (e < cnt) {
+                H[pa + e * stride] = yh[u]; H[pb + e * stride] = xh[u];
+                Lo[pa + e * stride] = yl[u]; Lo[pb + e * stride] = xl[u];
+            }
+        }
+    }
+}
+
+// symmetric swap of rows/columns a and b inside the trailing block [k:]
+// (_swap_sym, factory.py:117-121) plus the rows of L left of k and perm
 __device__ void sym_swap(BpWs &w, int64_t *perm, int64_t n, int64_t k, int64_t a, int64_t b)
 {
-    for (int64_t c = k + threadIdx.x; c < n; c += blockDim.x) {
-        double t = w.Ah[a * n + c]; w.Ah[a * n + c] = w.Ah[b * n + c]; w.Ah[b * n + c] = t;
-        t = w.Al[a * n + c]; w.Al[a * n + c] = w.Al[b * n + c]; w.Al[b * n + c] = t;
-    }
+    swap_pairs(w.Ah, w.Al, a * n + k, b * n + k, 1, n - k);  // rows a, b over columns k:
+    swap_pairs(w.Lh, w.Ll, a * n, b * n, 1, k);              // rows of L left of k
     __syncthreads();
-    for (int64_t r = k + threadIdx.x; r < n; r += blockDim.x) {
-        double t = w.Ah[r * n + a]; w.Ah[r * n + a] = w.Ah[r * n + b]; w.Ah[r * n + b] = t;
-        t = w.Al[r * n + a]; w.Al[r * n + a] = w.Al[r * n + b]; w.Al[r * n + b] = t;
-    }
-    for (int64_t c = threadIdx.x; c < k; c += blockDim.x) {
-        double t = w.Lh[a * n + c]; w.Lh[a * n + c] = w.Lh[b * n + c]; w.Lh[b * n + c] = t;
-        t = w.Ll[a * n + c]; w.Ll[a * n + c] = w.Ll[b * n + c]; w.Ll[b * n + c] = t;
-    }
+    swap_pairs(w.Ah, w.Al, k * n + a, k * n + b, n, n - k);  // columns a, b over rows k:
     if (threadIdx.x == 0) {
         const int64_t t = perm[a];
         perm[a] = perm[b];
@@ -268,10 +307,25 @@ __global__ void __launch_bounds__(PIV_THREADS) k_bp_pivot(int64_t n, double thre
     // reduce the search partials of the trailing block
     double bo = -1.0, bd = -1.0;
     int64_t io = 0, id = 0;
-    for (int64_t e = threadIdx.x; e < cnt; e += blockDim.x) {
-        const Cand o = w.poff[e], d = w.pdiag[e];
-        if (better(o.v, o.i, bo, io)) { bo = o.v; io = o.i; }
-        if (better(d.v, d.i, bd, id)) { bd = d.v; id = d.i; }
+    {
+        constexpr int U = 8;  // loads of a chunk issued before its comparisons
+        for (int64_t e0 = threadIdx.x; e0 < cnt; e0 += U * (int64_t)blockDim.x) {
+            Cand o[U], d[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int64_t e = e0 + u * (int64_t)blockDim.x;
+                if (e < cnt) {
+                    o[u] = w.poff[e];
+                    d[u] = w.pdiag[e];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (e0 + u * (int64_t)blockDim.x >= cnt) break;
+                if (better(o[u].v, o[u].i, bo, io)) { bo = o[u].v; io = o[u].i; }
+                if (better(d[u].v, d[u].i, bd, id)) { bd = d[u].v; id = d[u].i; }
+            }
+        }
     }
     block_argmax<PIV_THREADS>(bo, io, bd, id);
     if (threadIdx.x == 0) {
@@ -295,13 +349,24 @@ __global__ void __launch_bounds__(PIV_THREADS) k_bp_pivot(int64_t n, double thre
     if (one) {
         if (sh_i0 != 0) sym_swap(w, perm, n, k, k, k + sh_i0);
         const dd d = {w.Ah[k * n + k], w.Al[k * n + k]};
-        for (int64_t i = k + 1 + threadIdx.x; i < n; i += blockDim.x) {
-            const dd c = {w.Ah[k * n + i], w.Al[k * n + i]};  // A[i][k] = A[k][i]
-            const dd l = dd_div(c, d);
-            w.Lh[i * n + k] = l.h;
-            w.Ll[i * n + k] = l.l;
-            w.v0h[i] = c.h; w.v0l[i] = c.l;
-            w.l0h[i] = l.h; w.l0l[i] = l.l;
+        constexpr int U = 4;
+        for (int64_t i0 = k + 1 + threadIdx.x; i0 < n; i0 += U * (int64_t)blockDim.x) {
+            dd c[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int64_t i = i0 + u * (int64_t)blockDim.x;
+                if (i < n) c[u] = dd{w.Ah[k * n + i], w.Al[k * n + i]};  // A[i][k] = A[k][i]
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int64_t i = i0 + u * (int64_t)blockDim.x;
+                if (i >= n) continue;
+                const dd l = dd_div(c[u], d);
+                w.Lh[i * n + k] = l.h;
+                w.Ll[i * n + k] = l.l;
+                w.v0h[i] = c[u].h; w.v0l[i] = c[u].l;
+                w.l0h[i] = l.h; w.l0l[i] = l.l;
+            }
         }
         if (threadIdx.x == 0) {
             const int64_t q = S.nb;
@@ -322,9 +387,22 @@ __global__ void __launch_bounds__(PIV_THREADS) k_bp_pivot(int64_t n, double thre
         const dd eb = {w.Ah[(k + 1) * n + k], w.Al[(k + 1) * n + k]};
         const dd ec = {w.Ah[(k + 1) * n + k + 1], w.Al[(k + 1) * n + k + 1]};
         const dd det = dd_sub(dd_mul(ea, ec), dd_mul(eb, eb));
-        for (int64_t i = k + 2 + threadIdx.x; i < n; i += blockDim.x) {
-            const dd W0 = {w.Ah[k * n + i], w.Al[k * n + i]};
-            const dd W1 = {w.Ah[(k + 1) * n + i], w.Al[(k + 1) * n + i]};
+        constexpr int U = 4;
+        for (int64_t i0 = k + 2 + threadIdx.x; i0 < n; i0 += U * (int64_t)blockDim.x) {
+          dd W0s[U], W1s[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int64_t i = i0 + u * (int64_t)blockDim.x;
+            if (i < n) {
+                W0s[u] = dd{w.Ah[k * n + i], w.Al[k * n + i]};
+                W1s[u] = dd{w.Ah[(k + 1) * n + i], w.Al[(k + 1) * n + i]};
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int64_t i = i0 + u * (int64_t)blockDim.x;
+            if (i >= n) continue;
+            const dd W0 = W0s[u], W1 = W1s[u];
             const dd l0 = dd_div(dd_sub(dd_mul(W0, ec), dd_mul(W1, eb)), det);
             const dd l1 = dd_div(dd_sub(dd_mul(W1, ea), dd_mul(W0, eb)), det);
             w.Lh[i * n + k] = l0.h; w.Ll[i * n + k] = l0.l;
@@ -333,6 +411,7 @@ __global__ void __launch_bounds__(PIV_THREADS) k_bp_pivot(int64_t n, double thre
             w.v1h[i] = W1.h; w.v1l[i] = W1.l;
             w.l0h[i] = l0.h; w.l0l[i] = l0.l;
             w.l1h[i] = l1.h; w.l1l[i] = l1.l;
+          }
         }
         if (threadIdx.x == 0) {
             const int64_t q = S.nb;
@@ -353,11 +432,12 @@ __global__ void __launch_bounds__(PIV_THREADS) k_bp_pivot(int64_t n, double thre
 // 213-224 with _symmetrize, 124-128).  A is exactly symmetric, so the new
 // (i, j) needs only A_ij and the pivot vectors, and equals the new (j, i)
 // bit for bit (two_sum's error term is exact, hence symmetric).
-__global__ void __launch_bounds__(UPD_THREADS) k_bp_update(int64_t n, BpWs w)
+__global__ void __launch_bounds__(UPD_THREADS, 2) k_bp_update(int64_t n, BpWs w)
 {
     __shared__ double tt[TB][TB + 1];  // transposed tile (hi, then lo)
     __shared__ double rl0h[TB], rl0l[TB], rv0h[TB], rv0l[TB], rl1h[TB], rl1l[TB], rv1h[TB], rv1l[TB];
     __shared__ double cl0h[TB], cl0l[TB], cv0h[TB], cv0l[TB], cl1h[TB], cl1l[TB], cv1h[TB], cv1l[TB];
+    __shared__ sp2 rsl0[TB], rsv0[TB], csl0[TB], csv0[TB];
     const BpState S = *w.st;
     if (S.kind == 0 || S.status != 0) return;
     const int64_t k = S.k, m = n - k;  // the new trailing block
@@ -371,11 +451,17 @@ __global__ void __launch_bounds__(UPD_THREADS) k_bp_update(int64_t n, BpWs w)
         const int64_t r = r0 + tid, c = c0 + tid;
         if (r < n) {
             rl0h[tid] = w.l0h[r]; rl0l[tid] = w.l0l[r]; rv0h[tid] = w.v0h[r]; rv0l[tid] = w.v0l[r];
-            if (two) { rl1h[tid] = w.l1h[r]; rl1l[tid] = w.l1l[r]; rv1h[tid] = w.v1h[r]; rv1l[tid] = w.v1l[r]; }
+            rsl0[tid] = split2(rl0h[tid]); rsv0[tid] = split2(rv0h[tid]);
+            if (two) {
+                rl1h[tid] = w.l1h[r]; rl1l[tid] = w.l1l[r]; rv1h[tid] = w.v1h[r]; rv1l[tid] = w.v1l[r];
+            }
         }
         if (c < n) {
             cl0h[tid] = w.l0h[c]; cl0l[tid] = w.l0l[c]; cv0h[tid] = w.v0h[c]; cv0l[tid] = w.v0l[c];
-            if (two) { cl1h[tid] = w.l1h[c]; cl1l[tid] = w.l1l[c]; cv1h[tid] = w.v1h[c]; cv1l[tid] = w.v1l[c]; }
+            csl0[tid] = split2(cl0h[tid]); csv0[tid] = split2(cv0h[tid]);
+            if (two) {
+                cl1h[tid] = w.l1h[c]; cl1l[tid] = w.l1l[c]; cv1h[tid] = w.v1h[c]; cv1l[tid] = w.v1l[c];
+            }
         }
     }
     __syncthreads();
@@ -384,24 +470,33 @@ __global__ void __launch_bounds__(UPD_THREADS) k_bp_update(int64_t n, BpWs w)
     const int64_t c = c0 + tx;
     constexpr int RPT = TB / (UPD_THREADS / TB);  // rows per thread
     double nh[RPT], nl[RPT];
+    // all loads of the tile first (the stores below may alias them)
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) {
+        const int64_t r = r0 + ty + u * (UPD_THREADS / TB);
+        nh[u] = nl[u] = 0.0;
+        if (r < n && c < n) {
+            nh[u] = w.Ah[r * n + c];
+            nl[u] = w.Al[r * n + c];
+        }
+    }
 #pragma unroll
     for (int u = 0; u < RPT; ++u) {
         const int rr = ty + u * (UPD_THREADS / TB);
         const int64_t r = r0 + rr;
-        nh[u] = nl[u] = 0.0;
         if (r >= n || c >= n) continue;
-        const dd a = {w.Ah[r * n + c], w.Al[r * n + c]};
+        const dd a = {nh[u], nl[u]};
         const dd li = {rl0h[rr], rl0l[rr]}, ci = {rv0h[rr], rv0l[rr]};
         const dd lj = {cl0h[tx], cl0l[tx]}, cj = {cv0h[tx], cv0l[tx]};
         dd uij, uji;
         if (!two) {
-            uij = dd_mul(li, cj);
-            uji = dd_mul(lj, ci);
+            uij = dd_mul_s(li, rsl0[rr], cj, csv0[tx]);
+            uji = dd_mul_s(lj, csl0[tx], ci, rsv0[rr]);
         } else {
             const dd li1 = {rl1h[rr], rl1l[rr]}, ci1 = {rv1h[rr], rv1l[rr]};
             const dd lj1 = {cl1h[tx], cl1l[tx]}, cj1 = {cv1h[tx], cv1l[tx]};
-            uij = dd_add(dd_mul(li, cj), dd_mul(li1, cj1));
-            uji = dd_add(dd_mul(lj, ci), dd_mul(lj1, ci1));
+            uij = dd_add(dd_mul_s(li, rsl0[rr], cj, csv0[tx]), dd_mul(li1, cj1));
+            uji = dd_add(dd_mul_s(lj, csl0[tx], ci, rsv0[rr]), dd_mul(lj1, ci1));
         }
         const dd xij = dd_sub(a, uij), xji = dd_sub(a, uji);
         const dd s = dd_mul_f(dd_add(xij, xji), 0.5);
