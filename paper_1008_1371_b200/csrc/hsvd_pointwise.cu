@@ -279,6 +279,80 @@ __device__ __forceinline__ void chunk_update(double *x, double *y, int lo, int h
     ny2 = ay;
 }
 
+// Warp-cooperative coalesced variants for chunk = 32 (lane l owns chunk l of
+// the warp's 32 consecutive chunks): the warp loads each 8-element slice of
+// its 32 chunks with 64-byte runs per chunk (every sector fully used), a
+// shared-memory transpose hands lane l its chunk's slice, and lane l runs
+// the chunk's sequential FMA chain in the reference's order.  The direct
+// per-lane loads of chunk_dot touch 32 sectors per instruction with half of
+// each used, and the second half is refetched once L1 has evicted it.
+constexpr int kSlice = 8, kSliceLd = kSlice + 1;  // padded: conflict-free lane reads
+struct WarpSlices {
+    double x[32][kSliceLd], y[32][kSliceLd];
+};
+__device__ __forceinline__ void load_slices(WarpSlices &B, const double *gx, const double *gy,
+                                            int s, int lane)
+{
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int f = u * 32 + lane, ch = f >> 2, part = f & 3;
+        const int off = ch * 32 + s * kSlice + 2 * part;
+        const double2 xv = *reinterpret_cast<const double2 *>(gx + off);
+        const double2 yv = *reinterpret_cast<const double2 *>(gy + off);
+        B.x[ch][2 * part] = xv.x;
+        B.x[ch][2 * part + 1] = xv.y;
+        B.y[ch][2 * part] = yv.x;
+        B.y[ch][2 * part + 1] = yv.y;
+    }
+    __syncwarp();
+}
+// dot of the warp's chunks: returns lane l's chunk partial
+__device__ __forceinline__ double warp_chunk_dot(WarpSlices &B, const double *gx,
+                                                 const double *gy, int lane)
+{
+    double acc = 0.0;
+#pragma unroll 1
+    for (int s = 0; s < 32 / kSlice; ++s) {
+        load_slices(B, gx, gy, s, lane);
+#pragma unroll
+        for (int e = 0; e < kSlice; ++e) acc = __fma_rn(B.x[lane][e], B.y[lane][e], acc);
+        __syncwarp();
+    }
+    return acc;
+}
+// update of the warp's chunks in place; lane l's new squared norms
+__device__ __forceinline__ void warp_chunk_update(WarpSlices &B, double *gx, double *gy, int lane,
+                                                  double t, double c, double st, double &nx2,
+                                                  double &ny2)
+{
+    double ax = 0.0, ay = 0.0;
+#pragma unroll 1
+    for (int s = 0; s < 32 / kSlice; ++s) {
+        load_slices(B, gx, gy, s, lane);
+#pragma unroll
+        for (int e = 0; e < kSlice; ++e) {
+            const double xi = B.x[lane][e], yi = B.y[lane][e];
+            const double nx = __dmul_rn(__fma_rn(st, yi, xi), c);
+            const double ny = __dmul_rn(__fma_rn(t, xi, yi), c);
+            B.x[lane][e] = nx;
+            B.y[lane][e] = ny;
+            ax = __fma_rn(nx, nx, ax);
+            ay = __fma_rn(ny, ny, ay);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int f = u * 32 + lane, ch = f >> 2, part = f & 3;
+            const int off = ch * 32 + s * kSlice + 2 * part;
+            *reinterpret_cast<double2 *>(gx + off) = make_double2(B.x[ch][2 * part], B.x[ch][2 * part + 1]);
+            *reinterpret_cast<double2 *>(gy + off) = make_double2(B.y[ch][2 * part], B.y[ch][2 * part + 1]);
+        }
+        __syncwarp();
+    }
+    nx2 = ax;
+    ny2 = ay;
+}
+
 template <int NT, int CH, bool VEC>
 __global__ void __launch_bounds__(NT) k_pointwise_stream(StepArgs a)
 {
@@ -295,9 +369,19 @@ __global__ void __launch_bounds__(NT) k_pointwise_stream(StepArgs a)
     const int n = a.n, chunk = CH > 0 ? CH : a.chunk, m = a.m;
     double *p0 = smem, *p1 = p0 + m, *p2 = p1 + m, *p3 = p2 + m;
 
-    for (int bch = threadIdx.x; bch < m; bch += NT) {
-        const int lo = bch * chunk, hi = min(lo + chunk, n);
-        p0[bch] = chunk_dot<CH, VEC>(gi, gj, lo, hi);
+    // coalesced warp path: groups of 32 full chunks (n a multiple of 1024),
+    // group g on warp g mod (NT / 32)
+    const bool wpath = CH == 32 && VEC && (n & 1023) == 0;
+    WarpSlices *WS = reinterpret_cast<WarpSlices *>(p3 + m);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (wpath) {
+        for (int g = wid; g < (m >> 5); g += NT / 32)
+            p0[g * 32 + lane] = warp_chunk_dot(WS[wid], gi + g * 1024, gj + g * 1024, lane);
+    } else {
+        for (int bch = threadIdx.x; bch < m; bch += NT) {
+            const int lo = bch * chunk, hi = min(lo + chunk, n);
+            p0[bch] = chunk_dot<CH, VEC>(gi, gj, lo, hi);
+        }
     }
     const double a_ij = tree_sum<NT>(p0, p1, m);
     if (threadIdx.x == 0) {
@@ -328,12 +412,21 @@ __global__ void __launch_bounds__(NT) k_pointwise_stream(StepArgs a)
     if (act == 2) return;
     if (act == 1) {
         const double t = s_t, c = s_c, st = __dmul_rn(s_s, s_t);
-        for (int bch = threadIdx.x; bch < m; bch += NT) {
-            const int lo = bch * chunk, hi = min(lo + chunk, n);
-            double nx2, ny2;
-            chunk_update<CH, VEC>(gi, gj, lo, hi, t, c, st, nx2, ny2);
-            p0[bch] = nx2;
-            p2[bch] = ny2;
+        if (wpath) {
+            for (int g = wid; g < (m >> 5); g += NT / 32) {
+                double nx2, ny2;
+                warp_chunk_update(WS[wid], gi + g * 1024, gj + g * 1024, lane, t, c, st, nx2, ny2);
+                p0[g * 32 + lane] = nx2;
+                p2[g * 32 + lane] = ny2;
+            }
+        } else {
+            for (int bch = threadIdx.x; bch < m; bch += NT) {
+                const int lo = bch * chunk, hi = min(lo + chunk, n);
+                double nx2, ny2;
+                chunk_update<CH, VEC>(gi, gj, lo, hi, t, c, st, nx2, ny2);
+                p0[bch] = nx2;
+                p2[bch] = ny2;
+            }
         }
         if (a.V) {
             double *vi = a.V + ci * a.ldv;
@@ -692,9 +785,10 @@ int launch_pointwise_step(double *G, int64_t n, int64_t ldg, double *V,
                            jblk, r, C, k0, eps, teps, use_skip, chunk, advance,
                            rotk, skipk, maxt, err);
     // the streaming kernel keeps only the chunk partials in shared memory
-    const size_t smem = sizeof(double) * 4 * (size_t)a.m;
     const unsigned grid = (unsigned)(k1 - k0);
     const bool vec = chunk == 32 && ldg % 2 == 0 && ((uintptr_t)G & 15) == 0;
+    const size_t smem = sizeof(double) * 4 * (size_t)a.m +
+                        (vec && n % 1024 == 0 ? sizeof(WarpSlices) * (kStepThreads / 32) : 0);
     if (vec) {
         HSVD_CUDA(cudaFuncSetAttribute(k_pointwise_stream<kStepThreads, 32, true>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
