@@ -98,6 +98,16 @@ static void half_range(int64_t nslots, int h, int64_t &lo, int64_t &hi)
     hi = h ? nslots : nslots / 2;
 }
 
+// profile mode times the kernels of this sweep (HSVD_PROFILE_SWEEP, default 0)
+static int64_t profile_sweep()
+{
+    static const int64_t v = [] {
+        const char *e = getenv("HSVD_PROFILE_SWEEP");
+        return e ? (int64_t)atoll(e) : (int64_t)0;
+    }();
+    return v;
+}
+
 static int64_t carve_block(Carve2 &c, int64_t n, int64_t r, int b, BlockWs *w)
 {
     const int64_t nb = r / b, nslots = nb / 2 > 0 ? nb / 2 : 1;
@@ -363,7 +373,7 @@ static int block_drive_t(double *G, int64_t n, int64_t r, int64_t ldg, double *V
         HSVD_CUDA(cudaEventRecord(t0, s));
         launches += (split_now ? 8 : 3) * nb + 1 + 1 + (cfg->sort ? 2 : 0);
         if (split_now || !graphs) {
-            T.on = cfg->profile && sweep == 0;
+            T.on = cfg->profile && sweep == profile_sweep();
             st = enqueue_sweep();
             if (st) return st;
             // capture the one-stream graph for the late sweeps while the
