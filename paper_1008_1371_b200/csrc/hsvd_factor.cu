@@ -9,7 +9,8 @@
 //
 // Layout in HBM (n x n, row-major; M is exactly symmetric, so the storage
 // order of the input does not matter):
-//   Ah, Al  the trailing matrix (hi, lo), kept exactly symmetric
+//   Ah, Al  the trailing matrix (hi, lo): its upper triangle (the matrix
+//           stays exactly symmetric, so the lower one is never needed)
 //   Lh, Ll  the unit lower factor, rows permuted with the pivots
 //   vectors of the current pivot (multipliers and pivot columns), the
 //   pivot-search partials, the block records and a device-side state.
@@ -18,12 +19,12 @@
 //   k_bp_pivot   (one CTA)  reduces the search partials, takes the 1x1 or
 //                2x2 decision, swaps rows/columns, forms the multipliers;
 //   k_bp_update  (upper-triangle 64x64 tiles) applies the rank-1/2 update
-//                and the symmetrization to the new trailing block, writes
-//                each tile and its mirror, and searches the updated block
-//                for the next pivot (per-tile partial maxima).
-// The trailing update is HBM-bound: 16 B read + 32 B written per element
-// pair of the upper triangle (the symmetrized value of (i, j) needs only
-// A_ij = A_ji and the pivot vectors).
+//                and the symmetrization to the new trailing block and
+//                searches the updated block for the next pivot (per-tile
+//                partial maxima).
+// The trailing update is HBM-bound: 16 B read + 16 B written per element of
+// the upper triangle (the symmetrized value of (i, j) needs only A_ij = A_ji
+// and the pivot vectors).
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -278,10 +279,39 @@ __device__ __forceinline__ void swap_pairs(double *H, double *Lo, int64_t pa, in
 // (_swap_sym, factory.py:117-121) plus the rows of L left of k and perm
 __device__ void sym_swap(BpWs &w, int64_t *perm, int64_t n, int64_t k, int64_t a, int64_t b)
 {
-    swap_pairs(w.Ah, w.Al, a * n + k, b * n + k, 1, n - k);  // rows a, b over columns k:
-    swap_pairs(w.Lh, w.Ll, a * n, b * n, 1, k);              // rows of L left of k
-    __syncthreads();
-    swap_pairs(w.Ah, w.Al, k * n + a, k * n + b, n, n - k);  // columns a, b over rows k:
+    // only the upper triangle (row <= column) of the trailing block is kept:
+    // P A P with P = (a b), a < b, moves U(r, a) <-> U(r, b) for r != a, b
+    // and U(a, a) <-> U(b, b); U(a, b) stays (the reference's row swap then
+    // column swap moves the same values)
+    constexpr int U = 8;
+    const int64_t cnt = n - k;
+    for (int64_t e0 = threadIdx.x; e0 < cnt; e0 += U * (int64_t)blockDim.x) {
+        int64_t pa[U], pb[U];
+        double xh[U], yh[U], xl[U], yl[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t r = k + e0 + u * (int64_t)blockDim.x;
+            pa[u] = -1;
+            if (r < n && r != b) {
+                if (r == a) {  // the diagonal pair
+                    pa[u] = a * n + a;
+                    pb[u] = b * n + b;
+                } else {
+                    pa[u] = r < a ? r * n + a : a * n + r;
+                    pb[u] = r < b ? r * n + b : b * n + r;
+                }
+                xh[u] = w.Ah[pa[u]]; yh[u] = w.Ah[pb[u]];
+                xl[u] = w.Al[pa[u]]; yl[u] = w.Al[pb[u]];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (pa[u] < 0) continue;
+            w.Ah[pa[u]] = yh[u]; w.Ah[pb[u]] = xh[u];
+            w.Al[pa[u]] = yl[u]; w.Al[pb[u]] = xl[u];
+        }
+    }
+    swap_pairs(w.Lh, w.Ll, a * n, b * n, 1, k);  // rows of L left of k
     if (threadIdx.x == 0) {
         const int64_t t = perm[a];
         perm[a] = perm[b];
@@ -384,7 +414,7 @@ __global__ void __launch_bounds__(PIV_THREADS) k_bp_pivot(int64_t n, double thre
         if (a != 0) sym_swap(w, perm, n, k, k, k + a);
         if (b != 1) sym_swap(w, perm, n, k, k + 1, k + b);
         const dd ea = {w.Ah[k * n + k], w.Al[k * n + k]};
-        const dd eb = {w.Ah[(k + 1) * n + k], w.Al[(k + 1) * n + k]};
+        const dd eb = {w.Ah[k * n + k + 1], w.Al[k * n + k + 1]};  // upper copy
         const dd ec = {w.Ah[(k + 1) * n + k + 1], w.Al[(k + 1) * n + k + 1]};
         const dd det = dd_sub(dd_mul(ea, ec), dd_mul(eb, eb));
         constexpr int U = 4;
@@ -434,7 +464,6 @@ __global__ void __launch_bounds__(PIV_THREADS) k_bp_pivot(int64_t n, double thre
 // bit for bit (two_sum's error term is exact, hence symmetric).
 __global__ void __launch_bounds__(UPD_THREADS, 2) k_bp_update(int64_t n, BpWs w)
 {
-    __shared__ double tt[TB][TB + 1];  // transposed tile (hi, then lo)
     __shared__ double rl0h[TB], rl0l[TB], rv0h[TB], rv0l[TB], rl1h[TB], rl1l[TB], rv1h[TB], rv1l[TB];
     __shared__ double cl0h[TB], cl0l[TB], cv0h[TB], cv0l[TB], cl1h[TB], cl1l[TB], cv1h[TB], cv1l[TB];
     __shared__ sp2 rsl0[TB], rsv0[TB], csl0[TB], csv0[TB];
@@ -475,7 +504,7 @@ __global__ void __launch_bounds__(UPD_THREADS, 2) k_bp_update(int64_t n, BpWs w)
     for (int u = 0; u < RPT; ++u) {
         const int64_t r = r0 + ty + u * (UPD_THREADS / TB);
         nh[u] = nl[u] = 0.0;
-        if (r < n && c < n) {
+        if (r < n && c < n && r <= c) {
             nh[u] = w.Ah[r * n + c];
             nl[u] = w.Al[r * n + c];
         }
@@ -484,7 +513,7 @@ __global__ void __launch_bounds__(UPD_THREADS, 2) k_bp_update(int64_t n, BpWs w)
     for (int u = 0; u < RPT; ++u) {
         const int rr = ty + u * (UPD_THREADS / TB);
         const int64_t r = r0 + rr;
-        if (r >= n || c >= n) continue;
+        if (r >= n || c >= n || r > c) continue;  // upper triangle only
         const dd a = {nh[u], nl[u]};
         const dd li = {rl0h[rr], rl0l[rr]}, ci = {rv0h[rr], rv0l[rr]};
         const dd lj = {cl0h[tx], cl0l[tx]}, cj = {cv0h[tx], cv0l[tx]};
@@ -502,31 +531,12 @@ __global__ void __launch_bounds__(UPD_THREADS, 2) k_bp_update(int64_t n, BpWs w)
         const dd s = dd_mul_f(dd_add(xij, xji), 0.5);
         w.Ah[r * n + c] = s.h;
         w.Al[r * n + c] = s.l;
-        nh[u] = s.h;
-        nl[u] = s.l;
         const double v = fabs(s.h);
         const int64_t ri = r - k, cj_ = c - k;
         if (ri < cj_) {
             if (better(v, ri * m + cj_, bo, io)) { bo = v; io = ri * m + cj_; }
         } else if (ri == cj_) {
             if (better(v, ri, bd, id)) { bd = v; id = ri; }
-        }
-    }
-    if (I != J) {
-        // mirror tile: rows c0.., columns r0.. (coalesced along r), hi then lo
-        const int64_t mc = r0 + tx;
-#pragma unroll
-        for (int part = 0; part < 2; ++part) {
-            __syncthreads();
-#pragma unroll
-            for (int u = 0; u < RPT; ++u) tt[tx][ty + u * (UPD_THREADS / TB)] = part ? nl[u] : nh[u];
-            __syncthreads();
-            double *dst = part ? w.Al : w.Ah;
-            for (int cc = ty; cc < TB; cc += UPD_THREADS / TB) {
-                const int64_t mr = c0 + cc;
-                if (mr >= n || mc >= n) continue;
-                dst[mr * n + mc] = tt[cc][tx];
-            }
         }
     }
     block_argmax<UPD_THREADS>(bo, io, bd, id);
