@@ -10,6 +10,15 @@
 #include "hsvd_internal.cuh"
 #include "hsvd_rotation.cuh"
 
+// k_gram tiling: k-tile depth, cp.async stages, resident CTAs per SM
+// (64 / 2 / 3 measured 0.5 % faster per solve than 32 / 4 / 3 on the same
+// box; 64 / 3 / 2 is 4 % slower on the Gram: occupancy 3 matters)
+#ifndef HSVD_GRAM_KT
+#define HSVD_GRAM_KT 64
+#define HSVD_GRAM_STAGES 2
+#define HSVD_GRAM_OCC 3
+#endif
+
 namespace hsvd {
 
 // ---------------------------------------------------------------------
@@ -98,7 +107,8 @@ struct GramRoles<64> {
     // super-tile (4 tiles); warps 4 and 5 add one diagonal tile each, (1,1)
     // and (3,3); warps 6 and 7 own the remaining 10 diagonal-block tiles.
     static constexpr int NACC = 5;  // accumulator tiles per warp (max)
-    __device__ static void mma(int warp, const double (*X)[GramSmem<64, 32, 4>::LD], int kk,
+    template <int LD>
+    __device__ static void mma(int warp, const double (*X)[LD], int kk,
                                int fr, int fk, double (&acc)[NACC][2])
     {
         if (warp < 6) {
@@ -164,7 +174,8 @@ struct GramRoles<32> {
         rt = (int)((0x3221110000ull >> (4 * t)) & 0xF);
         ct = (int)((0x3323213210ull >> (4 * t)) & 0xF);
     }
-    __device__ static void mma(int warp, const double (*X)[GramSmem<32, 32, 4>::LD], int kk,
+    template <int LD>
+    __device__ static void mma(int warp, const double (*X)[LD], int kk,
                                int fr, int fk, double (&acc)[NACC][2])
     {
         int rt, ct;
@@ -178,7 +189,7 @@ struct GramRoles<32> {
 };
 
 template <int B2, int KT, int STAGES>
-__global__ void __launch_bounds__(kThreads, 3) k_gram(
+__global__ void __launch_bounds__(kThreads, HSVD_GRAM_OCC) k_gram(
     const double *__restrict__ G, int64_t ldg, int n, const int64_t *__restrict__ rho,
     const int64_t *__restrict__ iblk, const int64_t *__restrict__ jblk, GramPart part,
     int maxseg, double *__restrict__ Apart, const unsigned long long *err)
@@ -869,7 +880,7 @@ inline int num_sms()
     return sms;
 }
 
-constexpr int kGramKT = 32, kGramStages = 4, kGramOcc = 3;
+constexpr int kGramKT = HSVD_GRAM_KT, kGramStages = HSVD_GRAM_STAGES, kGramOcc = HSVD_GRAM_OCC;
 
 // Static Gram partition: P = #SMs x resident CTAs, capped so that a CTA
 // spans at most GramSmem::MAXSLOTS slots and owns >= 1 k-tile.
