@@ -286,7 +286,11 @@ __device__ __forceinline__ void chunk_update(double *x, double *y, int lo, int h
 // the chunk's sequential FMA chain in the reference's order.  The direct
 // per-lane loads of chunk_dot touch 32 sectors per instruction with half of
 // each used, and the second half is refetched once L1 has evicted it.
-constexpr int kSlice = 8, kSliceLd = kSlice + 1;  // padded: conflict-free lane reads
+#ifndef HSVD_PW_SLICE  // 8: 43.1 s at n = 8192; 4 (more CTAs per SM): 45.8 s
+#define HSVD_PW_SLICE 8
+#endif
+constexpr int kSlice = HSVD_PW_SLICE, kSliceLd = kSlice + 1;  // padded: conflict-free lane reads
+constexpr int kPpc = kSlice / 2;                              // double2 per chunk per slice
 struct WarpSlices {
     double x[32][kSliceLd], y[32][kSliceLd];
 };
@@ -294,8 +298,8 @@ __device__ __forceinline__ void load_slices(WarpSlices &B, const double *gx, con
                                             int s, int lane)
 {
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-        const int f = u * 32 + lane, ch = f >> 2, part = f & 3;
+    for (int u = 0; u < kPpc; ++u) {
+        const int f = u * 32 + lane, ch = f / kPpc, part = f % kPpc;
         const int off = ch * 32 + s * kSlice + 2 * part;
         const double2 xv = *reinterpret_cast<const double2 *>(gx + off);
         const double2 yv = *reinterpret_cast<const double2 *>(gy + off);
@@ -341,8 +345,8 @@ __device__ __forceinline__ void warp_chunk_update(WarpSlices &B, double *gx, dou
         }
         __syncwarp();
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int f = u * 32 + lane, ch = f >> 2, part = f & 3;
+        for (int u = 0; u < kPpc; ++u) {
+            const int f = u * 32 + lane, ch = f / kPpc, part = f % kPpc;
             const int off = ch * 32 + s * kSlice + 2 * part;
             *reinterpret_cast<double2 *>(gx + off) = make_double2(B.x[ch][2 * part], B.x[ch][2 * part + 1]);
             *reinterpret_cast<double2 *>(gy + off) = make_double2(B.y[ch][2 * part], B.y[ch][2 * part + 1]);
