@@ -1134,13 +1134,16 @@ HSVD_API int hsvd_gen_reflect(double *Mh, double *Ml, int64_t n, const double *v
         set_error("hsvd_gen_reflect: n too large for the on-chip pairwise tree");
         return HSVD_ERR_UNSUPPORTED;
     }
-    static bool attr = false;
-    if (!attr) {
+    // the shared-memory opt-in is per device
+    static bool attr[64] = {};
+    int dev = 0;
+    HSVD_CUDA(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= 64 || !attr[dev]) {
         HSVD_CUDA(cudaFuncSetAttribute(k_gen_scalars, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        200 * 1024));
         HSVD_CUDA(cudaFuncSetAttribute(k_gen_matvec, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        200 * 1024));
-        attr = true;
+        if (dev >= 0 && dev < 64) attr[dev] = true;
     }
     cudaStream_t s = (cudaStream_t)stream;
     unsigned char *b = (unsigned char *)ws;
