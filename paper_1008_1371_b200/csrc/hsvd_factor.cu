@@ -462,7 +462,13 @@ __global__ void __launch_bounds__(PIV_THREADS) k_bp_pivot(int64_t n, double thre
 // 213-224 with _symmetrize, 124-128).  A is exactly symmetric, so the new
 // (i, j) needs only A_ij and the pivot vectors, and equals the new (j, i)
 // bit for bit (two_sum's error term is exact, hence symmetric).
-__global__ void __launch_bounds__(UPD_THREADS, 2) k_bp_update(int64_t n, BpWs w)
+// rows of a tile staged per batch and resident CTAs per SM (n = 8192:
+// 16 / 2 1.234 s, 8 / 3 1.158 s, 4 / 4 1.233 s)
+#ifndef HSVD_BP_BATCH
+#define HSVD_BP_BATCH 8
+#define HSVD_BP_OCC 3
+#endif
+__global__ void __launch_bounds__(UPD_THREADS, HSVD_BP_OCC) k_bp_update(int64_t n, BpWs w)
 {
     __shared__ double rl0h[TB], rl0l[TB], rv0h[TB], rv0l[TB], rl1h[TB], rl1l[TB], rv1h[TB], rv1l[TB];
     __shared__ double cl0h[TB], cl0l[TB], cv0h[TB], cv0l[TB], cl1h[TB], cl1l[TB], cv1h[TB], cv1l[TB];
@@ -498,11 +504,14 @@ __global__ void __launch_bounds__(UPD_THREADS, 2) k_bp_update(int64_t n, BpWs w)
     int64_t io = 0, id = 0;
     const int64_t c = c0 + tx;
     constexpr int RPT = TB / (UPD_THREADS / TB);  // rows per thread
-    double nh[RPT], nl[RPT];
-    // all loads of the tile first (the stores below may alias them)
+    constexpr int BATCH = HSVD_BP_BATCH;           // rows staged at a time
+#pragma unroll 1
+    for (int u0 = 0; u0 < RPT; u0 += BATCH) {
+    double nh[BATCH], nl[BATCH];
+    // all loads of the batch first (the stores below may alias them)
 #pragma unroll
-    for (int u = 0; u < RPT; ++u) {
-        const int64_t r = r0 + ty + u * (UPD_THREADS / TB);
+    for (int u = 0; u < BATCH; ++u) {
+        const int64_t r = r0 + ty + (u0 + u) * (UPD_THREADS / TB);
         nh[u] = nl[u] = 0.0;
         if (r < n && c < n && r <= c) {
             nh[u] = w.Ah[r * n + c];
@@ -510,8 +519,8 @@ __global__ void __launch_bounds__(UPD_THREADS, 2) k_bp_update(int64_t n, BpWs w)
         }
     }
 #pragma unroll
-    for (int u = 0; u < RPT; ++u) {
-        const int rr = ty + u * (UPD_THREADS / TB);
+    for (int u = 0; u < BATCH; ++u) {
+        const int rr = ty + (u0 + u) * (UPD_THREADS / TB);
         const int64_t r = r0 + rr;
         if (r >= n || c >= n || r > c) continue;  // upper triangle only
         const dd a = {nh[u], nl[u]};
@@ -538,6 +547,7 @@ __global__ void __launch_bounds__(UPD_THREADS, 2) k_bp_update(int64_t n, BpWs w)
         } else if (ri == cj_) {
             if (better(v, ri, bd, id)) { bd = v; id = ri; }
         }
+    }
     }
     block_argmax<UPD_THREADS>(bo, io, bd, id);
     if (tid == 0) {
