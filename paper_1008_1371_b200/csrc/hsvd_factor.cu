@@ -29,6 +29,7 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <stdlib.h>
 #include <string.h>
 
 #include "hsvd_internal.cuh"
@@ -1104,6 +1105,156 @@ __global__ void k_gen_finish_upper(double *Mh, double *Ml, int64_t n)
     }
 }
 
+// ---- power-of-two n: the same pairwise trees from warp shuffles ----------
+// For n = 2^k every level of tree_sum pairs aligned neighbours and carries
+// nothing, so a 64-element aligned segment is a subtree: lane t adds
+// elements (2t, 2t + 1) and five shuffle levels finish it; the segment sums
+// (n / 64 of them) form the remaining levels the same way.  dd_add is
+// commutative bit for bit (two_sum's error term is exact), so which lane
+// holds the left operand does not matter.
+__device__ __forceinline__ dd shfl_down_dd(dd x, int o)
+{
+    return dd{__shfl_down_sync(0xffffffffu, x.h, o), __shfl_down_sync(0xffffffffu, x.l, o)};
+}
+// tree over `cnt` (power of two <= 32) values held by lanes 0..cnt-1; lane 0 gets it
+__device__ __forceinline__ dd warp_tree(dd x, int cnt)
+{
+    for (int o = 1; o < cnt; o <<= 1) {
+        const dd y = shfl_down_dd(x, o);
+        if (((threadIdx.x & 31) & (2 * o - 1)) == 0) x = dd_add(x, y);
+    }
+    return x;
+}
+constexpr int GEN2_THREADS = 256;
+// sum over j of term(j), j < n = 2^k >= 64, pairwise tree; all threads of the
+// CTA call it; the result is returned to thread 0
+template <class F>
+__device__ dd tree_pow2(int n, F term, dd *seg)
+{
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int nseg = n >> 6;
+    for (int sg = wid; sg < nseg; sg += GEN2_THREADS / 32) {
+        const int e = sg * 64 + 2 * lane;
+        dd x = dd_add(term(e), term(e + 1));
+        x = warp_tree(x, 32);
+        if (lane == 0) seg[sg] = x;
+    }
+    __syncthreads();
+    dd r = {0.0, 0.0};
+    if (wid == 0) {
+        if (nseg >= 32) {
+            // lane t: the subtree of segments [t * per, (t + 1) * per)
+            const int per = nseg >> 5;
+            dd buf[8];  // per <= 8 (n <= 16384)
+            for (int u = 0; u < per; ++u) buf[u] = seg[lane * per + u];
+            for (int len = per; len > 1; len >>= 1)
+                for (int u = 0; u < len / 2; ++u) buf[u] = dd_add(buf[2 * u], buf[2 * u + 1]);
+            r = warp_tree(buf[0], 32);
+        } else {
+            r = warp_tree(lane < nseg ? seg[lane] : dd{0.0, 0.0}, nseg);
+        }
+    }
+    return r;
+}
+
+__global__ void __launch_bounds__(GEN2_THREADS) k_gen_scalars2(const double *v, int n, GenWs g,
+                                                                int which)
+{
+    __shared__ dd seg[256];
+    dd s;
+    if (which == 0)
+        s = tree_pow2(n, [&](int j) { return two_prod(v[j], v[j]); }, seg);
+    else
+        s = tree_pow2(n, [&](int j) { return dd_mul_f(dd{g.wh[j], g.wl[j]}, v[j]); }, seg);
+    if (threadIdx.x == 0) {
+        if (which == 0) {
+            g.sc[0] = dd_div(dd{2.0, 0.0}, s);
+        } else {
+            const dd beta = g.sc[0];
+            g.sc[1] = s;
+            g.sc[2] = dd_mul(dd_mul(beta, beta), s);
+        }
+    }
+}
+__global__ void __launch_bounds__(GEN2_THREADS) k_gen_matvec2(const double *Mh, const double *Ml,
+                                                               const double *v, int n, GenWs g)
+{
+    __shared__ dd seg[256];
+    const int64_t i = blockIdx.x;
+    const double *rh = Mh + i * n, *rl = Ml + i * n;
+    const dd s = tree_pow2(n, [&](int j) { return dd_mul_f(dd{rh[j], rl[j]}, v[j]); }, seg);
+    if (threadIdx.x == 0) {
+        g.wh[i] = s.h;
+        g.wl[i] = s.l;
+    }
+}
+
+// the rank-2 update on the upper triangle in 64x64 tiles, each written with
+// its mirror (M stays bitwise symmetric: S and T are, Dekker's two_prod
+// being exact), 16 B read + 32 B written per element pair
+__global__ void __launch_bounds__(256) k_gen_update_sym(double *Mh, double *Ml, const double *v,
+                                                         int64_t n, GenWs g)
+{
+    __shared__ double tt[64][65];
+    const int64_t tiles = (n + 63) / 64;
+    const int64_t ntri = tiles * (tiles + 1) / 2;
+    const dd beta = g.sc[0], gamma = g.sc[2];
+    const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
+    for (int64_t t = blockIdx.x; t < ntri; t += gridDim.x) {
+        int I, J;
+        {
+            int j = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+            while ((int64_t)(j + 1) * (j + 2) / 2 <= t) ++j;
+            while ((int64_t)j * (j + 1) / 2 > t) --j;
+            J = j;
+            I = (int)(t - (int64_t)j * (j + 1) / 2);
+        }
+        const int64_t r0 = (int64_t)I * 64, c0 = (int64_t)J * 64;
+        const int64_t c = c0 + tx;
+        double nh[16], nl[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            const int64_t r = r0 + ty + 4 * u;
+            nh[u] = nl[u] = 0.0;
+            if (r < n && c < n) {
+                nh[u] = Mh[r * n + c];
+                nl[u] = Ml[r * n + c];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            const int64_t r = r0 + ty + 4 * u;
+            if (r >= n || c >= n) continue;
+            const double vi = v[r], vj = v[c];
+            const dd wi = {g.wh[r], g.wl[r]}, wj = {g.wh[c], g.wl[c]};
+            const dd vw = dd_mul_f(wj, vi), wv = dd_mul_f(wi, vj);
+            const dd S = dd_mul(dd_add(vw, wv), beta);
+            const dd T = dd_mul(two_prod(vi, vj), gamma);
+            const dd res = dd_add(dd_sub(dd{nh[u], nl[u]}, S), T);
+            nh[u] = res.h;
+            nl[u] = res.l;
+            Mh[r * n + c] = res.h;
+            Ml[r * n + c] = res.l;
+        }
+        if (I != J) {
+            const int64_t mc = r0 + tx;
+#pragma unroll
+            for (int part = 0; part < 2; ++part) {
+                __syncthreads();
+#pragma unroll
+                for (int u = 0; u < 16; ++u) tt[tx][ty + 4 * u] = part ? nl[u] : nh[u];
+                __syncthreads();
+                double *dst = part ? Ml : Mh;
+                for (int cc = ty; cc < 64; cc += 4) {
+                    const int64_t mr = c0 + cc;
+                    if (mr < n && mc < n) dst[mr * n + mc] = tt[cc][tx];
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
 }  // namespace
 }  // namespace hsvd
 
@@ -1161,12 +1312,25 @@ HSVD_API int hsvd_gen_reflect(double *Mh, double *Ml, int64_t n, const double *v
     g.wh = (double *)b;
     g.wl = (double *)(b + align256((size_t)n * 8));
     g.sc = (dd *)(b + 2 * align256((size_t)n * 8));
+    // HSVD_GEN_POW2=0 keeps the generic shared-memory trees (cross-checks)
+    static const bool pow2_on = [] {
+        const char *e = getenv("HSVD_GEN_POW2");
+        return !(e && e[0] == '0');
+    }();
+    const bool pow2 = pow2_on && n >= 64 && (n & (n - 1)) == 0;
     for (int64_t q = 0; q < count; ++q) {
         const double *v = vs + q * n;
-        k_gen_scalars<<<1, GEN_THREADS, smem, s>>>(v, n, g, 0);
-        k_gen_matvec<<<(unsigned)n, GEN_THREADS, smem, s>>>(Mh, Ml, v, n, g);
-        k_gen_scalars<<<1, GEN_THREADS, smem, s>>>(v, n, g, 1);
-        k_gen_update<<<1184, 256, 0, s>>>(Mh, Ml, v, n, g);
+        if (pow2) {  // warp-shuffle trees, upper-triangle update with mirror
+            k_gen_scalars2<<<1, GEN2_THREADS, 0, s>>>(v, (int)n, g, 0);
+            k_gen_matvec2<<<(unsigned)n, GEN2_THREADS, 0, s>>>(Mh, Ml, v, (int)n, g);
+            k_gen_scalars2<<<1, GEN2_THREADS, 0, s>>>(v, (int)n, g, 1);
+            k_gen_update_sym<<<1184, 256, 0, s>>>(Mh, Ml, v, n, g);
+        } else {
+            k_gen_scalars<<<1, GEN_THREADS, smem, s>>>(v, n, g, 0);
+            k_gen_matvec<<<(unsigned)n, GEN_THREADS, smem, s>>>(Mh, Ml, v, n, g);
+            k_gen_scalars<<<1, GEN_THREADS, smem, s>>>(v, n, g, 1);
+            k_gen_update<<<1184, 256, 0, s>>>(Mh, Ml, v, n, g);
+        }
     }
     HSVD_LAUNCH_CHECK("k_gen_update");
     return HSVD_OK;

@@ -149,3 +149,24 @@ def test_generate_identity_q():
                                   identity_q=True)
     np.testing.assert_array_equal(M, np.diag([3.0, -1.0, 2.0, 5.0, -4.0, 1.0]))
     np.testing.assert_array_equal(lam, np.sort([3.0, -1.0, 2.0, 5.0, -4.0, 1.0]))
+
+
+@pytest.mark.parametrize("n", [256, 2048, 4096])
+def test_generate_pow2_path_matches_generic(n):
+    # power-of-two n takes the warp-shuffle trees and the mirrored update;
+    # the generic shared-memory path (pinned to the reference's goldens) must
+    # give the same bits
+    import subprocess
+    code = ("import sys, hashlib; sys.path.insert(0, '.'); import numpy as np; "
+            "import paper_1008_1371_b200 as H; "
+            f"M, lam = H.generate_symmetric(H.SpectrumSpec({n}, 20.0, 5)); "
+            "print(hashlib.sha256(np.ascontiguousarray(M).tobytes()).hexdigest())")
+    root = os.path.dirname(HERE)
+    out = {}
+    for flag in ("1", "0"):
+        env = dict(os.environ, HSVD_GEN_POW2=flag)
+        r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
+                           text=True, timeout=900)
+        assert r.returncode == 0, r.stderr[-1500:]
+        out[flag] = r.stdout.strip().splitlines()[-1]
+    assert out["1"] == out["0"]
