@@ -590,8 +590,11 @@ __global__ void __launch_bounds__(inner_threads<B2>()) k_inner(InnerArgs a)
                     st = hyp < 0 ? -t : t;
                 }
             }
+            if (lane < b) S.prm[par][q] = make_double4(t, c, st, 0.0);
+            const unsigned va = __ballot_sync(0xffffffffu, act), vb = __ballot_sync(0xffffffffu, bad);
+            if (lane == 0) S.flag[par] = (va ? 1 : 0) | (vb ? 2 : 0);
+            // statistics after the publication (off the round's critical path)
             if (lane < b) {
-                S.prm[par][q] = make_double4(t, c, st, 0.0);
                 if (bad) atomicMin(&S.fail, pack_err(a.slot_base + slot, slot_pos(lo, b, I, J),
                                                      slot_pos(hi, b, I, J)));
                 else if (act) {
@@ -604,8 +607,6 @@ __global__ void __launch_bounds__(inner_threads<B2>()) k_inner(InnerArgs a)
                     ++my_skip;
                 }
             }
-            const int f = (__any_sync(0xffffffffu, act) ? 1 : 0) | (__any_sync(0xffffffffu, bad) ? 2 : 0);
-            if (lane == 0) S.flag[par] = f;
         } else if (w_worker && prev_act) {
             // the previous round's W update runs beside this round's rotations
             w_update(prev_rd, par ^ 1);
