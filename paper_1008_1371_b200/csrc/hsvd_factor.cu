@@ -1192,10 +1192,12 @@ __global__ void __launch_bounds__(GEN2_THREADS) k_gen_matvec2(const double *Mh, 
 // the rank-2 update on the upper triangle in 64x64 tiles, each written with
 // its mirror (M stays bitwise symmetric: S and T are, Dekker's two_prod
 // being exact), 16 B read + 32 B written per element pair
-__global__ void __launch_bounds__(256) k_gen_update_sym(double *Mh, double *Ml, const double *v,
-                                                         int64_t n, GenWs g)
+__global__ void __launch_bounds__(256, 3) k_gen_update_sym(double *Mh, double *Ml,
+                                                            const double *v, int64_t n, GenWs g)
 {
-    __shared__ double tt[64][65];
+    extern __shared__ double gus[];  // the tile transposed (hi, lo): 2 x 64 x 65
+    double (*th)[65] = reinterpret_cast<double (*)[65]>(gus);
+    double (*tl)[65] = reinterpret_cast<double (*)[65]>(gus + 64 * 65);
     const int64_t tiles = (n + 63) / 64;
     const int64_t ntri = tiles * (tiles + 1) / 2;
     const dd beta = g.sc[0], gamma = g.sc[2];
@@ -1211,43 +1213,44 @@ __global__ void __launch_bounds__(256) k_gen_update_sym(double *Mh, double *Ml, 
         }
         const int64_t r0 = (int64_t)I * 64, c0 = (int64_t)J * 64;
         const int64_t c = c0 + tx;
-        double nh[16], nl[16];
+        // 8 rows staged at a time (registers for 3 CTAs per SM); results are
+        // kept for the mirror pass in the transposed tile
+#pragma unroll 1
+        for (int u0 = 0; u0 < 16; u0 += 8) {
+            double nh[8], nl[8];
 #pragma unroll
-        for (int u = 0; u < 16; ++u) {
-            const int64_t r = r0 + ty + 4 * u;
-            nh[u] = nl[u] = 0.0;
-            if (r < n && c < n) {
-                nh[u] = Mh[r * n + c];
-                nl[u] = Ml[r * n + c];
+            for (int u = 0; u < 8; ++u) {
+                const int64_t r = r0 + ty + 4 * (u0 + u);
+                nh[u] = nl[u] = 0.0;
+                if (r < n && c < n) {
+                    nh[u] = Mh[r * n + c];
+                    nl[u] = Ml[r * n + c];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int64_t r = r0 + ty + 4 * (u0 + u);
+                if (r >= n || c >= n) continue;
+                const double vi = v[r], vj = v[c];
+                const dd wi = {g.wh[r], g.wl[r]}, wj = {g.wh[c], g.wl[c]};
+                const dd vw = dd_mul_f(wj, vi), wv = dd_mul_f(wi, vj);
+                const dd S = dd_mul(dd_add(vw, wv), beta);
+                const dd T = dd_mul(two_prod(vi, vj), gamma);
+                const dd res = dd_add(dd_sub(dd{nh[u], nl[u]}, S), T);
+                Mh[r * n + c] = res.h;
+                Ml[r * n + c] = res.l;
+                th[tx][ty + 4 * (u0 + u)] = res.h;
+                tl[tx][ty + 4 * (u0 + u)] = res.l;
             }
         }
-#pragma unroll
-        for (int u = 0; u < 16; ++u) {
-            const int64_t r = r0 + ty + 4 * u;
-            if (r >= n || c >= n) continue;
-            const double vi = v[r], vj = v[c];
-            const dd wi = {g.wh[r], g.wl[r]}, wj = {g.wh[c], g.wl[c]};
-            const dd vw = dd_mul_f(wj, vi), wv = dd_mul_f(wi, vj);
-            const dd S = dd_mul(dd_add(vw, wv), beta);
-            const dd T = dd_mul(two_prod(vi, vj), gamma);
-            const dd res = dd_add(dd_sub(dd{nh[u], nl[u]}, S), T);
-            nh[u] = res.h;
-            nl[u] = res.l;
-            Mh[r * n + c] = res.h;
-            Ml[r * n + c] = res.l;
-        }
         if (I != J) {
+            __syncthreads();
             const int64_t mc = r0 + tx;
-#pragma unroll
-            for (int part = 0; part < 2; ++part) {
-                __syncthreads();
-#pragma unroll
-                for (int u = 0; u < 16; ++u) tt[tx][ty + 4 * u] = part ? nl[u] : nh[u];
-                __syncthreads();
-                double *dst = part ? Ml : Mh;
-                for (int cc = ty; cc < 64; cc += 4) {
-                    const int64_t mr = c0 + cc;
-                    if (mr < n && mc < n) dst[mr * n + mc] = tt[cc][tx];
+            for (int cc = ty; cc < 64; cc += 4) {
+                const int64_t mr = c0 + cc;
+                if (mr < n && mc < n) {
+                    Mh[mr * n + mc] = th[cc][tx];
+                    Ml[mr * n + mc] = tl[cc][tx];
                 }
             }
         }
@@ -1304,6 +1307,9 @@ HSVD_API int hsvd_gen_reflect(double *Mh, double *Ml, int64_t n, const double *v
                                        200 * 1024));
         HSVD_CUDA(cudaFuncSetAttribute(k_gen_matvec, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        200 * 1024));
+        HSVD_CUDA(cudaFuncSetAttribute(k_gen_update_sym,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(2 * 64 * 65 * sizeof(double))));
         if (dev >= 0 && dev < 64) attr[dev] = true;
     }
     cudaStream_t s = (cudaStream_t)stream;
@@ -1324,7 +1330,7 @@ HSVD_API int hsvd_gen_reflect(double *Mh, double *Ml, int64_t n, const double *v
             k_gen_scalars2<<<1, GEN2_THREADS, 0, s>>>(v, (int)n, g, 0);
             k_gen_matvec2<<<(unsigned)n, GEN2_THREADS, 0, s>>>(Mh, Ml, v, (int)n, g);
             k_gen_scalars2<<<1, GEN2_THREADS, 0, s>>>(v, (int)n, g, 1);
-            k_gen_update_sym<<<1184, 256, 0, s>>>(Mh, Ml, v, n, g);
+            k_gen_update_sym<<<1184, 256, 2 * 64 * 65 * sizeof(double), s>>>(Mh, Ml, v, n, g);
         } else {
             k_gen_scalars<<<1, GEN_THREADS, smem, s>>>(v, n, g, 0);
             k_gen_matvec<<<(unsigned)n, GEN_THREADS, smem, s>>>(Mh, Ml, v, n, g);
