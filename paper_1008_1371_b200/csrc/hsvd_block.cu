@@ -4,26 +4,32 @@
 // positions [I*b, I*b+b) and [J*b, J*b+b) of the sorted package order,
 // gathered through rho as the reference addresses columns, solver.py:26-43).
 // One step of the modified-modulus schedule on the r/b block indices
-// (strategies.py:41-72) processes all r/(2b) slots with three kernels:
+// (strategies.py:41-72) processes all r/(2b) slots with three kernels
+// (hsvd_block_kernels.cuh):
 //
 //   k_gram    A_P = G_P^T G_P (2b x 2b), FP64 tensor cores (mma.sync
-//             m8n8k4 -> SASS DMMA.8x8x4) fed by cp.async multi-stage smem
-//             pipelines; split-K over CTAs, upper-triangle tiles only,
-//             partials reduced in fixed order by the next kernel.
-//   k_inner   one CTA per slot: sums the split-K partials, runs one pass of
-//             2x2 rotations on (A_P, J_P) in shared memory -- each 2x2
-//             rotation is the reference's double-double rotation_tc
-//             (_kernels.py:128-173), trig or hyperbolic from the signs, with
-//             the relative-orthogonality skip (_kernels.py:211) -- and
-//             accumulates the J-orthogonal W_P; writes convergence codes and
-//             statistics, advances the stepper.
+//             m8n8k4 -> SASS DMMA.8x8x4); each slot's K range is cut into
+//             fixed segments (a function of n only) streamed over the CTAs,
+//             upper-triangle tiles only.
+//   k_inner   one CTA per slot: folds the segment partials in order, runs one
+//             pass of 2x2 rotations on (A_P, J_P) in shared memory -- trig or
+//             hyperbolic from the signs, with the relative-orthogonality skip
+//             (_kernels.py:211); "fast" plain-fp64 closed forms by default,
+//             the reference's double-double rotation_tc (_kernels.py:128-173)
+//             with block_rotation="dd" -- and accumulates the J-orthogonal
+//             W_P; writes convergence codes and statistics, advances the
+//             stepper.
 //   k_update  [G_P; V_P] <- [G_P; V_P] W_P, FP64 tensor cores, in place.
 //
-// The inner pass uses the paper's block-oriented ordering:
-// the full 2b(2b-1)/2 pairs at the first step of a sweep (each diagonal
-// block meets itself once per sweep), only the b^2 cross pairs I x J at the
-// other steps.  Per sweep the algorithm therefore applies the same pair
-// visits as the pointwise method, in blocked order.
+// The inner ordering is "full" by default (every pair of the pivot block,
+// circle method, at every step); inner_ordering="oriented" is the paper's
+// block-oriented scheme (the full triangle at the first
+// step of a sweep, only the cross pairs I x J at the other steps).
+//
+// r not a multiple of 2b: the driver appends inert zero columns (J = -1) in
+// a workspace copy and strips them afterwards (block_drive_padded): a zero
+// column has a_ij = 0 with every column, so it is never rotated, and pairs
+// that include one are not counted as visits.
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -151,10 +157,44 @@ static int64_t carve_block(Carve2 &c, int64_t n, int64_t r, int b, BlockWs *w)
     return c.off + 256;
 }
 
+// Padding to a multiple of 2b: the padded copy of G (ld even), V^{-T},
+// sigma and lam live at the front of the workspace.
+struct PadWs {
+    double *G, *V, *sigma, *lam;
+    int64_t ld, rp;
+};
+
+static int64_t pad_cols(int64_t r, int b)
+{
+    const int64_t m = 2 * (int64_t)b;
+    return (r + m - 1) / m * m - r;
+}
+
+static int64_t carve_pad(Carve2 &c, int64_t n, int64_t r, int b, bool withV, PadWs *w)
+{
+    PadWs t;
+    t.rp = r + pad_cols(r, b);
+    t.ld = n + (n & 1);
+    t.G = c.take<double>(t.rp * t.ld);
+    t.V = withV ? c.take<double>(t.rp * t.rp) : nullptr;
+    t.sigma = c.take<double>(t.rp);
+    t.lam = c.take<double>(t.rp);
+    if (w) *w = t;
+    c.off = (c.off + 255) & ~(int64_t)255;
+    return c.off;
+}
+
 int64_t block_workspace_size(int64_t n, int64_t r, const hsvd_config *cfg)
 {
+    // unsupported widths (block_drive rejects them) must not reach the
+    // carve's r / b
+    const int b = cfg->block_cols;
+    if (b != 16 && b != 32) return 256;
     Carve2 c{nullptr, 0};
-    return carve_block(c, n, r, cfg->block_cols, nullptr);
+    int64_t pre = 0;
+    if (pad_cols(r, b)) pre = carve_pad(c, n, r, b, cfg->accumulate_v != 0, nullptr);
+    Carve2 c2{nullptr, 0};
+    return pre + carve_block(c2, n, r + pad_cols(r, b), b, nullptr);
 }
 
 int launch_reduce_sweep(uint8_t *C, int64_t m, uint32_t *rotk, uint32_t *skipk,
@@ -177,7 +217,8 @@ template <int B2>
 static int block_drive_t(double *G, int64_t n, int64_t r, int64_t ldg, double *V, int64_t ldv,
                          const int8_t *signs_host, int64_t p, const hsvd_config *cfg,
                          double *sigma, double *lam, void *ws, int64_t ws_bytes,
-                         hsvd_result *res, hsvd_telemetry *tele, DevCtx &ctx)
+                         hsvd_result *res, hsvd_telemetry *tele, DevCtx &ctx,
+                         int64_t r_real)
 {
     cudaStream_t s = ctx.s;
     using K = BlockKernels<B2>;
@@ -189,6 +230,8 @@ static int block_drive_t(double *G, int64_t n, int64_t r, int64_t ldg, double *V
         set_error("workspace too small");
         return HSVD_ERR_ARG;
     }
+    // columns with rho >= r_real are padding (block_drive_padded)
+    w.sl.real_cols = w.half[0].real_cols = w.half[1].real_cols = r_real;
     int st = K::setup();
     if (st) return st;
 
@@ -218,7 +261,8 @@ static int block_drive_t(double *G, int64_t n, int64_t r, int64_t ldg, double *V
     if (st) return st;
     HSVD_CUDA(cudaMemcpyAsync(host, w.first_zero, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     HSVD_CUDA(cudaStreamSynchronize(s));
-    if ((unsigned long long)host[0] != kNoError) {
+    // the smallest zero column; padding columns (>= r_real) are zero by design
+    if ((unsigned long long)host[0] < (unsigned long long)r_real) {
         res->err[0] = host[0];
         res->err[1] = res->err[2] = -1;
         set_error("column " + std::to_string(host[0]) + " has zero norm");
@@ -442,6 +486,50 @@ static int block_drive_t(double *G, int64_t n, int64_t r, int64_t ldg, double *V
     return HSVD_OK;
 }
 
+// r not a multiple of 2b: solve the padded factor [G 0] with J = [J, -1...]
+// in a workspace copy, then copy U, V^{-T}, sigma and lam back.  The zero
+// columns are inert (never rotated, never counted), so the result is the
+// solve of G itself; sigma/lam/U of the original columns are unaffected by
+// where the padding sits in the sorted order.
+static int block_drive_padded(double *G, int64_t n, int64_t r, int64_t ldg, double *V,
+                              int64_t ldv, const int8_t *signs_host, int64_t p,
+                              const hsvd_config *cfg, double *sigma, double *lam, void *ws,
+                              int64_t ws_bytes, hsvd_result *res, hsvd_telemetry *tele,
+                              DevCtx &ctx)
+{
+    const int b = cfg->block_cols;
+    Carve2 c{(char *)ws, 0};
+    PadWs pw;
+    const int64_t pre = carve_pad(c, n, r, b, V != nullptr, &pw);
+    if (pre >= ws_bytes) {
+        set_error("workspace too small");
+        return HSVD_ERR_ARG;
+    }
+    cudaStream_t s = ctx.s;
+    const int64_t rp = pw.rp;
+    HSVD_CUDA(cudaMemcpy2DAsync(pw.G, pw.ld * sizeof(double), G, ldg * sizeof(double),
+                                n * sizeof(double), r, cudaMemcpyDeviceToDevice, s));
+    HSVD_CUDA(cudaMemsetAsync(pw.G + r * pw.ld, 0, (rp - r) * pw.ld * sizeof(double), s));
+    std::vector<int8_t> sg(signs_host, signs_host + r);
+    sg.resize(rp, (int8_t)-1);
+    int st;
+    if (b == 16)
+        st = block_drive_t<32>(pw.G, n, rp, pw.ld, pw.V, rp, sg.data(), p, cfg, pw.sigma,
+                               pw.lam, (char *)ws + pre, ws_bytes - pre, res, tele, ctx, r);
+    else
+        st = block_drive_t<64>(pw.G, n, rp, pw.ld, pw.V, rp, sg.data(), p, cfg, pw.sigma,
+                               pw.lam, (char *)ws + pre, ws_bytes - pre, res, tele, ctx, r);
+    if (st) return st;
+    HSVD_CUDA(cudaMemcpy2DAsync(G, ldg * sizeof(double), pw.G, pw.ld * sizeof(double),
+                                n * sizeof(double), r, cudaMemcpyDeviceToDevice, s));
+    if (V)
+        HSVD_CUDA(cudaMemcpy2DAsync(V, ldv * sizeof(double), pw.V, rp * sizeof(double),
+                                    r * sizeof(double), r, cudaMemcpyDeviceToDevice, s));
+    HSVD_CUDA(cudaMemcpyAsync(sigma, pw.sigma, r * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    HSVD_CUDA(cudaMemcpyAsync(lam, pw.lam, r * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    return HSVD_OK;
+}
+
 int block_drive(double *G, int64_t n, int64_t r, int64_t ldg, double *V, int64_t ldv,
                 const int8_t *signs_host, int64_t p, const hsvd_config *cfg, double *sigma,
                 double *lam, void *ws, int64_t ws_bytes, hsvd_result *res,
@@ -452,19 +540,18 @@ int block_drive(double *G, int64_t n, int64_t r, int64_t ldg, double *V, int64_t
         set_error("block mode supports block_cols 16 or 32");
         return HSVD_ERR_UNSUPPORTED;
     }
-    if (r % (2 * b) != 0) {
-        set_error("block mode needs r to be a multiple of 2*block_cols (use border())");
-        return HSVD_ERR_UNSUPPORTED;
-    }
+    if (r % (2 * b) != 0)
+        return block_drive_padded(G, n, r, ldg, V, ldv, signs_host, p, cfg, sigma, lam, ws,
+                                  ws_bytes, res, tele, ctx);
     if (ldg % 2 || (V && ldv % 2) || ((uintptr_t)G & 15) || (V && ((uintptr_t)V & 15))) {
         set_error("block mode needs 16-byte aligned columns (even leading dimensions)");
         return HSVD_ERR_UNSUPPORTED;
     }
     if (b == 16)
         return block_drive_t<32>(G, n, r, ldg, V, ldv, signs_host, p, cfg, sigma, lam, ws,
-                                 ws_bytes, res, tele, ctx);
+                                 ws_bytes, res, tele, ctx, r);
     return block_drive_t<64>(G, n, r, ldg, V, ldv, signs_host, p, cfg, sigma, lam, ws,
-                             ws_bytes, res, tele, ctx);
+                             ws_bytes, res, tele, ctx, r);
 }
 
 }  // namespace hsvd

@@ -56,29 +56,35 @@ __device__ __forceinline__ int64_t slot_pos(int c, int b, int64_t I, int64_t J)
 }
 
 // ---------------------------------------------------------------------
-// k_gram: partial Gram matrices over a static "stream-K" partition
+// k_gram: partial Gram matrices over fixed K segments, streamed over CTAs
 // ---------------------------------------------------------------------
-// The work of one step is W = nslots * T k-tiles (T = ceil(n / KT)).  The
-// grid has P = (#SMs x resident CTAs) CTAs and CTA c owns the contiguous
-// item range [c*W/P, (c+1)*W/P): every SM gets the same number of DMMAs,
-// with no wave tail.  A CTA flushes one partial Gram per slot segment it
-// covers; k_inner sums a slot's partials in segment order, so the result
-// is deterministic for a given P.
+// A slot's K range (T = ceil(n / KT) k-tiles) is cut into NSEG fixed
+// segments of L k-tiles.  L and NSEG depend on n (and KT) only, never on
+// how many slots a launch holds, how many SMs the GPU has or how the slots
+// are split over streams and shards.  Each segment's partial Gram is one
+// DMMA accumulation chain from zero over the segment's k-tiles, and k_inner
+// folds a slot's NSEG partials in segment order, so A_P is a function of
+// the slot's columns alone: block mode gives the same bits for any
+// stream split and any shard count (the reference's worker-count
+// invariance, solver.py:127-131).
+//
+// Who computes which segment is free: the NS = nslots * NSEG segments of a
+// launch are dealt to P CTAs in contiguous runs of equal length (stream-K
+// at segment granularity: a CTA streams its run through one pipeline and
+// flushes its accumulators at every segment end).
 struct GramPart {
-    int64_t W, P, T;
-    __host__ __device__ int64_t begin(int64_t c) const { return c * W / P; }
-    // CTA owning item x
-    __host__ __device__ int64_t owner(int64_t x) const
+    int64_t T, L, NSEG, NS, P;
+    __host__ __device__ int64_t seg_begin(int64_t c) const { return c * NS / P; }
+    // first k-tile item (slot * T + k-tile) of global segment s
+    __host__ __device__ int64_t item_of_seg(int64_t s) const
     {
-        int64_t c = (x * P) / W;
-        while (c + 1 < P && begin(c + 1) <= x) ++c;
-        while (c > 0 && begin(c) > x) --c;
-        return c;
+        const int64_t slot = s / NSEG, g = s % NSEG;
+        return slot * T + g * L;
     }
-    __host__ __device__ int64_t first_cta(int64_t slot) const { return owner(slot * T); }
-    __host__ __device__ int64_t nseg(int64_t slot) const
+    __host__ __device__ int64_t begin(int64_t c) const
     {
-        return owner(slot * T + T - 1) - first_cta(slot) + 1;
+        const int64_t s = seg_begin(c);
+        return s >= NS ? (NS / NSEG) * T : item_of_seg(s);
     }
 };
 
@@ -219,7 +225,7 @@ __global__ void __launch_bounds__(kThreads, HSVD_GRAM_OCC) k_gram(
     constexpr int PER_T = (CHUNKS + kThreads - 1) / kThreads;
     // the item stream (slot, k-tile) is walked with 32-bit counters: no
     // 64-bit division per k-tile
-    const int T = (int)part.T;
+    const int T = (int)part.T, Lseg = (int)part.L;
     auto load_stage = [&](int st, int si, int kt) {
         const int k0 = kt * KT;
 #pragma unroll
@@ -272,15 +278,17 @@ __global__ void __launch_bounds__(kThreads, HSVD_GRAM_OCC) k_gram(
         st_c = st_c + 1 == STAGES ? 0 : st_c + 1;
 #pragma unroll
         for (int kk = 0; kk < KT; kk += 4) Roles::mma(warp, X, kk, fr, fk, acc);
-        const bool seg_end = i + 1 == nitems || c_k == T - 1;
+        // CTA runs start and end on segment boundaries, so every segment
+        // is accumulated from zero by exactly one CTA
+        const int seg = c_k / Lseg;
+        const bool seg_end = c_k == T - 1 || c_k + 1 == (seg + 1) * Lseg;
         const int64_t slot = slot0 + c_si;
         if (++c_k == T) {
             c_k = 0;
             ++c_si;
         }
         if (seg_end) {
-            // flush this slot segment's partial (upper tiles only)
-            const int64_t seg = cta - part.first_cta(slot);
+            // flush this segment's partial (upper tiles only)
             double *out = Apart + (slot * maxseg + seg) * (B2 * B2);
 #pragma unroll
             for (int q = 0; q < Roles::NACC; ++q) {
@@ -316,6 +324,7 @@ struct InnerArgs {
     double *maxt;
     unsigned long long *err;
     int64_t nb, slot_base;
+    int64_t real_cols;  // colmap values >= real_cols are inert padding columns
     double eps, teps;
     int full, use_skip, passes;
     long long *trace;  // debug: per-round clock64 stamps of CTA 0 (NULL)
@@ -336,6 +345,7 @@ struct InnerSmem {
     double4 prm[2][B2 / 2];  // (t, c, st, -) of the round, by round parity
     int flag[2];             // bit 0: some pair rotated, bit 1: a pair failed
     int js[B2];
+    unsigned int jneg[2], padm[2];  // per-column bit masks (J = -1, padding)
     unsigned int rot, skip, big;
     unsigned long long maxt_bits;
     unsigned long long fail;
@@ -442,7 +452,7 @@ __global__ void __launch_bounds__(inner_threads<B2>()) k_inner(InnerArgs a)
     // triangle is read coalesced and mirrored); all loads of a batch of
     // segments are issued before the sums
     const double *P0 = a.Apart + (int64_t)slot * a.maxseg * (B2 * B2);
-    const int nseg = (int)a.part.nseg(slot);
+    const int nseg = (int)a.part.NSEG;
     constexpr int PER = B2 * B2 / NT;
 #pragma unroll
     for (int k = 0; k < PER; ++k) {
@@ -479,7 +489,18 @@ __global__ void __launch_bounds__(inner_threads<B2>()) k_inner(InnerArgs a)
             }
         }
     }
-    if (tid < B2) S.js[tid] = (int)a.jsign[slot_pos(tid, b, I, J)];
+    if (tid < B2) {
+        const int64_t pos = slot_pos(tid, b, I, J);
+        const int neg = a.jsign[pos] < 0;
+        const int pad = a.colmap[pos] >= a.real_cols;
+        S.js[tid] = neg ? -1 : 1;
+        const unsigned mneg = __ballot_sync(0xffffffffu, neg);
+        const unsigned mpad = __ballot_sync(0xffffffffu, pad);
+        if (lane == 0) {
+            S.jneg[warp] = mneg;
+            S.padm[warp] = mpad;
+        }
+    }
     if (tid == 0) {
         S.rot = S.skip = S.big = 0;
         S.maxt_bits = 0;
@@ -500,9 +521,12 @@ __global__ void __launch_bounds__(inner_threads<B2>()) k_inner(InnerArgs a)
     long long *tr = (a.trace && blockIdx.x == 0 && tid == 0) ? a.trace : nullptr;
 #define HSVD_STAMP(k) \
     if (tr && it < 64) tr[8 * it + (k)] = clock64();
-    // negative-sign columns as a bit mask: hyp without a shared-memory load
-    unsigned long long jneg = 0;
-    for (int c = 0; c < B2; ++c) jneg |= (unsigned long long)(S.js[c] < 0) << c;
+    // negative-sign and padding columns as bit masks (ballots above): hyp
+    // without a shared-memory load per pair
+    const unsigned long long jneg =
+        B2 == 64 ? ((unsigned long long)S.jneg[1] << 32) | S.jneg[0] : S.jneg[0];
+    const unsigned long long padm =
+        B2 == 64 ? ((unsigned long long)S.padm[1] << 32) | S.padm[0] : S.padm[0];
     // columns of pair x in round rd (circle method on B2 players, or the
     // block-oriented pairing x <-> b + (x + rd) mod b)
     auto pair_cols = [&](int x, int rd, int &ci, int &cj) {
@@ -603,8 +627,8 @@ __global__ void __launch_bounds__(inner_threads<B2>()) k_inner(InnerArgs a)
                     const double at = fabs(t);
                     my_big |= at > a.teps;
                     my_max = fmax(my_max, at);
-                } else {
-                    ++my_skip;
+                } else if (!(((padm >> i) | (padm >> j)) & 1)) {
+                    ++my_skip;  // pairs with a padding column are not visits
                 }
             }
         } else if (w_worker && prev_act) {
@@ -883,30 +907,40 @@ inline int num_sms()
 
 constexpr int kGramKT = HSVD_GRAM_KT, kGramStages = HSVD_GRAM_STAGES, kGramOcc = HSVD_GRAM_OCC;
 
-// Static Gram partition: P = #SMs x resident CTAs, capped so that a CTA
-// spans at most GramSmem::MAXSLOTS slots and owns >= 1 k-tile.
+// Target number of K segments per slot (a function of nothing but this
+// constant and n: see GramPart).  More segments balance the CTAs better
+// and cost k_inner more partials to fold.
+#ifndef HSVD_GRAM_NSEG
+#define HSVD_GRAM_NSEG 16
+#endif
+
+// Gram partition of a launch of nslots slots.  The segmentation (L, NSEG)
+// depends on n only.  The NS segments are dealt in equal runs of
+// ceil(NS / capacity) segments, capacity = #SMs x resident CTAs, so every
+// CTA has the same work and, when the runs do not fill the GPU, the spare
+// CTA slots go to the other stream's kernels.  A CTA spans at most
+// GramSmem::MAXSLOTS slots (checked by the caller through gram_slots_ok).
 inline GramPart gram_partition(int64_t n, int64_t nslots)
 {
     GramPart g;
     g.T = (n + kGramKT - 1) / kGramKT;
-    g.W = nslots * g.T;
-    g.P = (int64_t)num_sms() * kGramOcc;
-    if (g.P > g.W) g.P = g.W;
-    // items per CTA >= T / 2 keeps a CTA within 4 slots: W/P <= 2T always
-    // holds for P >= nslots/2; raise P if the slots outnumber the CTAs
-    while (g.W / g.P + 2 > 4 * g.T && g.P < g.W) g.P *= 2;
-    if (g.P > g.W) g.P = g.W;
+    if (g.T < 1) g.T = 1;
+    g.L = (g.T + HSVD_GRAM_NSEG - 1) / HSVD_GRAM_NSEG;
+    g.NSEG = (g.T + g.L - 1) / g.L;
+    g.NS = nslots * g.NSEG;
+    const int64_t cap = (int64_t)num_sms() * kGramOcc;
+    const int64_t per = (g.NS + cap - 1) / cap;
+    g.P = (g.NS + per - 1) / per;
     return g;
 }
 
-inline int gram_maxseg(const GramPart &g, int64_t nslots)
+inline int gram_maxseg(const GramPart &g, int64_t) { return (int)g.NSEG; }
+
+// every CTA's run of segments touches at most MAXSLOTS slots
+inline bool gram_slots_ok(const GramPart &g)
 {
-    int m = 1;
-    for (int64_t s = 0; s < nslots; ++s) {
-        const int k = (int)g.nseg(s);
-        if (k > m) m = k;
-    }
-    return m;
+    const int64_t per = (g.NS + g.P - 1) / g.P;
+    return (per + g.NSEG - 1) / g.NSEG + 1 <= 4;
 }
 
 // Per-slot state of one step's kernels: the whole problem on one GPU, or
@@ -923,6 +957,7 @@ struct SlotWs {
     double *Apart, *Wg;
     int64_t *colidx;
     int64_t nslots, nb, slot_base;
+    int64_t real_cols;  // colmap values >= this are padding (INT64_MAX: none)
     GramPart gp;
     int maxseg;
 };
@@ -952,6 +987,7 @@ inline void carve_slots(Carve2 &c, int64_t n, int64_t nslots, int64_t nb, int b,
     t.nslots = nslots;
     t.nb = nb;
     t.slot_base = 0;
+    t.real_cols = INT64_MAX;
     t.gp = gp;
     t.maxseg = ks;
     if (w) *w = t;
@@ -996,6 +1032,10 @@ struct BlockKernels {
     {
         const int64_t nslots = w.nslots;
         const GramPart &gp = w.gp;
+        if (!gram_slots_ok(gp)) {
+            set_error("block mode: too many slots per Gram CTA (r too large for this GPU)");
+            return HSVD_ERR_UNSUPPORTED;
+        }
         T.begin(0, s);
         {
             // Gram and inner pass are the critical path of a step: highest
@@ -1021,7 +1061,7 @@ struct BlockKernels {
         ia.Apart = w.Apart; ia.Wg = w.Wg; ia.jsign = w.js;
         ia.ip = w.ip; ia.jp = w.jp; ia.iblk = w.iblk; ia.jblk = w.jblk; ia.cur = w.cur;
         ia.C = w.C; ia.tset = w.tset; ia.colmap = w.colmap; ia.colidx = w.colidx; ia.rotk = w.rotk; ia.skipk = w.skipk; ia.maxt = w.maxt; ia.err = w.err;
-        ia.nb = w.nb; ia.slot_base = w.slot_base; ia.eps = cfg->eps; ia.teps = cfg->teps;
+        ia.nb = w.nb; ia.slot_base = w.slot_base; ia.real_cols = w.real_cols; ia.eps = cfg->eps; ia.teps = cfg->teps;
         ia.full = full; ia.use_skip = cfg->use_skip;
         ia.passes = cfg->inner_passes > 1 ? cfg->inner_passes : 1;
         ia.trace = nullptr;

@@ -1180,6 +1180,7 @@ struct ShardedDriver {
 static int64_t shard_ws_size(int64_t n, int64_t r, int nshards, int g, const hsvd_config *cfg)
 {
     ShardPlan pl;
+    if (cfg->block_cols != 16 && cfg->block_cols != 32) return -1;
     if (pl.init(r / cfg->block_cols, nshards)) return -1;
     Carve2 c{nullptr, 0};
     return carve_shard(c, pl, g, n, r, cfg->block_cols, cfg->accumulate_v != 0, nullptr);

@@ -80,6 +80,8 @@ class SolverConfig:
             raise ValueError(f"unknown mode {self.mode!r}")
         if self.inner_ordering not in ("oriented", "full"):
             raise ValueError(f"unknown inner_ordering {self.inner_ordering!r}")
+        if self.block_cols not in (16, 32):
+            raise ValueError("block_cols must be 16 or 32")
         if self.block_streams not in (1, 2):
             raise ValueError("block_streams must be 1 or 2")
         if self.inner_passes < 1:
@@ -242,7 +244,10 @@ def drive(G, J, cfg=None):
             raise ShapeError("G must be a matrix")
         if not bool(torch.isfinite(G).all()):
             raise ValueError("G contains non-finite entries")
-        Gt = G.detach().to(torch.float64).t().contiguous()
+        # always a fresh buffer: drive_device overwrites it with U, and the
+        # caller's G is never mutated (solver.py:188).  (.t().contiguous()
+        # would alias a column-major float64 G.)
+        Gt = G.detach().to(torch.float64).t().clone(memory_format=torch.contiguous_format)
         res = drive_device(Gt, J, cfg)
         res.U = res.U.t()
         if res.Vinv_t is not None:

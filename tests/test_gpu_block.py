@@ -90,10 +90,41 @@ def test_block_full_inner_ordering():
     assert sigma_class_reldiff(res.sigma, res.lam, ref.sigma, ref.lam) <= SIGMA_RTOL
 
 
-def test_block_rejects_bad_width():
-    with pytest.raises(NotImplementedError):
-        H.drive(np.eye(40), H.SignatureVector.from_p(40, 20),
-                H.SolverConfig(mode="block", block_cols=32))
+@pytest.mark.parametrize("case", [
+    # n, r, p, seed, kind, b: r not a multiple of 2b (inert zero-column padding)
+    (1000, 1000, 500, 4, "gauss", 32),
+    (520, 514, 200, 2, "gauss", 32),
+    (96, 70, 30, 1, "gauss", 16),
+    (300, 258, 258, 3, "graded12", 32),
+    (64, 62, 0, 5, "gauss", 16),
+], ids=lambda c: f"n{c[0]}r{c[1]}p{c[2]}{c[4]}b{c[5]}")
+def test_block_any_even_r(case):
+    """Block mode for r not a multiple of 2b (solver.py:289-341 purpose):
+    sigma per class within 1e-10 of the reference, residuals within the
+    same band as the aligned cases, the input never mutated."""
+    n, r, p, seed, kind, b = case
+    G = make_case_input(n, r, seed, kind)
+    G0 = G.copy()
+    signs = np.array([1] * p + [-1] * (r - p), np.int8)
+    ref = O.drive(G, signs, p)
+    res = H.drive(G, H.SignatureVector(signs, p), H.SolverConfig(mode="block", block_cols=b))
+    assert np.array_equal(G, G0)
+    assert res.U.shape == (n, r) and res.Vinv_t.shape == (r, r) and res.sigma.shape == (r,)
+    assert res.stop_reason in ("orthogonal", "quadratic")
+    assert np.all(np.isfinite(res.U)) and np.all(np.isfinite(res.Vinv_t))
+    assert sigma_class_reldiff(res.sigma, res.lam, ref.sigma, ref.lam) <= SIGMA_RTOL
+    rb, rr = residuals(G, res, signs), residuals(G, ref, signs)
+    for k in rb:
+        assert rb[k] <= RESID_FACTOR * rr[k] + 1e-15, (k, rb[k], rr[k])
+    # pairs with a padding column are not counted as visits
+    assert res.rotations + res.skips <= res.sweeps_used * r * (r - 1)
+
+
+def test_block_padding_identity_diag():
+    G = np.asfortranarray(np.diag(np.arange(40, 0, -1, dtype=np.float64)))
+    res = H.drive(G, H.SignatureVector.from_p(40, 20), H.SolverConfig(mode="block", block_cols=32))
+    assert res.stop_reason == "orthogonal" and res.rotations == 0
+    assert np.array_equal(np.sort(res.sigma), np.arange(1.0, 41.0))
 
 
 def test_block_config3_n4096_p3072_against_pointwise():
@@ -112,3 +143,33 @@ def test_block_config3_n4096_p3072_against_pointwise():
     for k in rb:
         assert rb[k] <= 2.0 * rr[k], (k, rb[k], rr[k])
     assert res.sweeps_used <= ref.sweeps_used
+
+
+def _definiteness_case(n=64, p=32):
+    """Columns p-1 (J = +1) and p (J = -1) identical, every other column a
+    unit vector orthogonal to them: the hyperbolic pair has |theta| = 1 and
+    no other rotation can change it first (the reference raises
+    DefinitenessLostError on it, _kernels.py:163-171)."""
+    G = np.eye(n)
+    G[:, p - 1] = 0.0
+    G[:, p] = 0.0
+    G[p - 1, p - 1] = G[p, p - 1] = 1.0
+    G[p - 1, p] = G[p, p] = 1.0
+    return np.asfortranarray(G), H.SignatureVector.from_p(n, p)
+
+
+@pytest.mark.parametrize("rot", ["fast", "dd"])
+def test_block_definiteness_lost_raises(rot):
+    G, J = _definiteness_case()
+    with pytest.raises(RuntimeError) as ei:
+        O.drive(G, J.signs, J.p)  # the reference's behaviour on this input
+    assert ei.value.args[0] == 1   # status 1: definiteness lost
+    with pytest.raises(H.DefinitenessLostError):
+        H.drive(G, J, H.SolverConfig(mode="block", block_cols=16, block_rotation=rot))
+
+
+@pytest.mark.parametrize("N", [1, 2])
+def test_sharded_definiteness_lost_raises(N):
+    G, J = _definiteness_case()
+    with pytest.raises(H.DefinitenessLostError):
+        H.drive_local_shards(G, J, H.SolverConfig(mode="block", block_cols=16), nshards=N)

@@ -66,6 +66,23 @@ def test_input_not_mutated():
     assert np.array_equal(G, G0)
 
 
+def test_cuda_input_not_mutated():
+    """A column-major float64 CUDA G (whose transpose is already contiguous)
+    must be copied, not overwritten by U (the reference copies G,
+    solver.py:188)."""
+    G = make_case_input(64, 64, 2, "gauss")
+    Gd = torch.from_numpy(np.asfortranarray(G)).cuda()   # strides (1, 64)
+    Gd = torch.as_strided(Gd.t().contiguous(), (64, 64), (1, 64))
+    G0 = Gd.clone()
+    res = H.drive(Gd, H.SignatureVector.from_p(64, 32))
+    assert torch.equal(Gd, G0)
+    assert res.U.data_ptr() != Gd.data_ptr()
+    for mode in ("pointwise", "block"):
+        res = H.drive(Gd, H.SignatureVector.from_p(64, 32),
+                      H.SolverConfig(mode=mode, block_cols=16))
+        assert torch.equal(Gd, G0), mode
+
+
 def test_rotation_kernel_bit_exact(golden):
     rows = golden["rotation"]
     a = np.array([unhex(r[0]) for r in rows])

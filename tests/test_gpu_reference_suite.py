@@ -1,0 +1,65 @@
+"""The reference's OWN test files, run against this build on the GPU.
+
+tests/ref_shim.py rebinds the names this package shares with ``hjsvd`` to
+the GPU build, then pytest runs the reference's test modules from the
+staged copy in baseline/_ref/ref_tests (see the plugin's docstring; staged
+by __graft_entry__.build() where /root/reference exists, git-ignored, and
+shipped to the GPU box with the snapshot).  The files are run unmodified:
+
+* test_solver.py -- TestPrecompute, TestSortDiagonal, TestCheckConvergence,
+  TestJacobiStep, TestDrive (incl. worker invariance, row-cyclic, no-sort,
+  max_sweeps, telemetry), TestRecoverV, TestBorder (test_solver.py:33-273);
+* test_acceptance.py -- criteria 1-11 (the strategy-lab criteria 3-4 run
+  the reference's own lab, which is out of scope);
+* test_linalg.py, test_rotation.py, test_strategies.py, test_io.py,
+  test_cli.py, test_factory.py;
+* test_acceptance.py criteria 5-7 again with block mode as drive()'s
+  default (HSVD_SHIM_MODE=block).
+"""
+
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
+STAGED = os.path.join(ROOT, "baseline", "_ref", "ref_tests")
+FILES = ["test_solver.py", "test_acceptance.py", "test_linalg.py", "test_rotation.py",
+         "test_strategies.py", "test_io.py", "test_cli.py", "test_factory.py"]
+
+
+def _run(files, mode="pointwise", k=None, tag=""):
+    if not os.path.isdir(STAGED) or not os.path.isdir(os.path.join(ROOT, "baseline", "_ref", "hjsvd")):
+        pytest.skip("reference tests not staged (run __graft_entry__.build() where "
+                    "/root/reference exists)")
+    env = dict(os.environ, HSVD_SHIM_MODE=mode,
+               NUMBA_CACHE_DIR=os.environ.get("NUMBA_CACHE_DIR", "/tmp/numba_cache_ref"),
+               PYTHONPATH=ROOT)
+    cmd = [sys.executable, "-m", "pytest", "-p", "tests.ref_shim", "-q", "-rA",
+           "-p", "no:cacheprovider", "--rootdir", STAGED]
+    if k:
+        cmd += ["-k", k]
+    cmd += [os.path.join(STAGED, f) for f in files]
+    out = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=1500)
+    log = os.path.join(ROOT, "gpurun_out", f"reference_suite{tag}.log")
+    os.makedirs(os.path.dirname(log), exist_ok=True)
+    with open(log, "w") as f:
+        f.write(out.stdout + out.stderr)
+    tail = "\n".join((out.stdout + out.stderr).splitlines()[-40:])
+    assert out.returncode == 0, tail
+    assert "hjsvd shim: mode=" + mode in out.stdout, tail
+    return out.stdout
+
+
+def test_reference_suite_pointwise():
+    txt = _run(FILES, tag="_pointwise")
+    assert " passed" in txt and " failed" not in txt
+
+
+def test_reference_acceptance_block_mode():
+    txt = _run(["test_acceptance.py"], mode="block",
+               k="criterion_05 or criterion_06 or criterion_07", tag="_block")
+    assert "3 passed" in txt

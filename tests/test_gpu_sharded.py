@@ -24,6 +24,14 @@ pytestmark = pytest.mark.gpu
 SIGMA_RTOL = 1e-10
 
 
+def _assert_same(a, b):
+    assert (a.sweeps_used, a.stop_reason) == (b.sweeps_used, b.stop_reason)
+    assert (a.rotations, a.skips) == (b.rotations, b.skips)
+    for f in ("sigma", "lam", "U", "Vinv_t"):
+        x, y = getattr(a, f), getattr(b, f)
+        assert (x is None and y is None) or np.array_equal(x, y), f
+
+
 def _case(n, r, p, seed, kind="gauss"):
     G = make_case_input(n, r, seed, kind)
     signs = np.array([1] * p + [-1] * (r - p), np.int8)
@@ -63,21 +71,42 @@ def test_sharded_matches_reference(case):
     s = H.drive_local_shards(G, J, cfg, nshards=N)
     assert s.stop_reason in ("orthogonal", "quadratic")
     assert sigma_class_reldiff(s.sigma, s.lam, ref.sigma, ref.lam) <= SIGMA_RTOL
-    rs, r1 = residuals(G, s, signs), residuals(G, one, signs)
-    for k in rs:
-        assert rs[k] <= 4.0 * r1[k] + 1e-15, (k, rs[k], r1[k])
-    assert abs(s.sweeps_used - one.sweeps_used) <= 1, (s.sweeps_used, one.sweeps_used)
+    # worker-count invariance (solver.py:127-131, test_solver.py:167-173):
+    # the Gram's K segmentation depends on n only, so N shards give the
+    # one-GPU solver's bits, sweeps and statistics
+    _assert_same(s, one)
 
 
 @pytest.mark.parametrize("N", [1, 2])
 def test_sharded_split_matches_one_stream(N):
     """Split-stream steps (two slot halves + overlapped exchange per shard)
-    against the one-stream sharded solver: same tolerance to each other."""
+    against the one-stream sharded solver and the one-GPU solver: bit for
+    bit."""
     G, signs, J = _case(1024, 1024, 512, 7)
     a = H.drive_local_shards(G, J, H.SolverConfig(mode="block", block_streams=1), nshards=N)
     b = H.drive_local_shards(G, J, H.SolverConfig(mode="block", block_streams=2), nshards=N)
-    assert sigma_class_reldiff(a.sigma, a.lam, b.sigma, b.lam) <= 1e-12
-    assert abs(a.sweeps_used - b.sweeps_used) <= 1
+    one = H.drive(G, J, H.SolverConfig(mode="block", block_streams=1))
+    _assert_same(a, b)
+    _assert_same(a, one)
+
+
+@pytest.mark.parametrize("streams", [1, 2])
+@pytest.mark.parametrize("graph", [False, True])
+def test_one_gpu_stream_split_invariance(streams, graph):
+    """One GPU: one stream vs two slot halves, eager vs graph replay: the
+    same bits (the Gram's segmentation does not follow the launch)."""
+    G, signs, J = _case(2048, 2048, 1024, 0)
+    ref = H.drive(G, J, H.SolverConfig(mode="block", block_streams=2))
+    x = H.drive(G, J, H.SolverConfig(mode="block", block_streams=streams, use_graph=graph))
+    _assert_same(x, ref)
+
+
+def test_sharded_n8_large_bit_identical():
+    """8 local shards at n = 2048 (8 slots per shard, split steps): the
+    one-GPU solver's bits."""
+    G, signs, J = _case(2048, 2048, 1024, 0)
+    cfg = H.SolverConfig(mode="block")
+    _assert_same(H.drive_local_shards(G, J, cfg, nshards=8), H.drive(G, J, cfg))
 
 
 def test_sharded_is_deterministic():

@@ -55,6 +55,19 @@ def test_solverconfig_defaults_mirror_reference():
         H.SolverConfig(workers=0)
 
 
+def test_block_cols_validated():
+    """block_cols outside {16, 32} is rejected on the host, and the
+    workspace query never divides by it (no SIGFPE through the C ABI)."""
+    for b in (0, -1, 8, 64):
+        with pytest.raises(ValueError):
+            H.SolverConfig(mode="block", block_cols=b)
+    L = _lib.load()
+    c = H.SolverConfig(mode="block").to_c()
+    c.block_cols = 0
+    assert L.hsvd_drive_workspace_size(256, 256, c) > 0
+    assert L.hsvd_sharded_workspace_size(256, 256, 2, 0, c) == -1
+
+
 def test_struct_sizes():
     """The ctypes mirrors have the C layouts (sizes reported by the library)."""
     out = (ctypes.c_int64 * 3)()
