@@ -91,6 +91,7 @@ struct BlockWs {
     void *sortws;
     int64_t *out;
     int8_t *signs;
+    int64_t *rho_prev;  // rho before the sweep-end sort (all-skip reuse)
     SlotWs sl;
     // split mode: the two half-slot views (shared arrays, own Gram partial
     // buffers and partitions)
@@ -125,7 +126,8 @@ static int64_t carve_block(Carve2 &c, int64_t n, int64_t r, int b, BlockWs *w)
     t.sortws = c.take<char>(24 * r);
     t.out = c.take<int64_t>(8);
     t.signs = c.take<int8_t>(r);
-    carve_slots(c, n, nslots, nb, b, &t.sl);
+    t.rho_prev = c.take<int64_t>(r);
+    carve_slots(c, n, nslots, nb, b, &t.sl, true);
     t.sl.colmap = t.rho;
     t.sl.js = t.js;
     const int64_t B2 = 2 * b;
@@ -146,6 +148,9 @@ static int64_t carve_block(Carve2 &c, int64_t n, int64_t r, int b, BlockWs *w)
         v.maxt = t.sl.maxt + lo;
         v.Wg = t.sl.Wg + lo * B2 * B2;
         v.colidx = t.sl.colidx + lo * B2;
+        v.skipf = t.sl.skipf + lo;
+        v.act = t.sl.act + lo;
+        v.nact = t.sl.nact + 1 + h;
         v.nslots = hi - lo;
         v.slot_base = lo;
         v.gp = gram_partition(n, m);
@@ -279,6 +284,10 @@ static int block_drive_t(double *G, int64_t n, int64_t r, int64_t ldg, double *V
     HSVD_CUDA(cudaMemsetAsync(w.sl.skipk, 0, sizeof(uint32_t) * nslots, s));
     HSVD_CUDA(cudaMemsetAsync(w.sl.maxt, 0, sizeof(double) * nslots, s));
     HSVD_CUDA(cudaMemsetAsync(w.sl.err, 0xff, sizeof(unsigned long long), s));
+    HSVD_CUDA(cudaMemsetAsync(w.sl.ru.pairstamp, 0, sizeof(uint32_t) * nb * nb, s));
+    HSVD_CUDA(cudaMemsetAsync(w.sl.ru.pairskip, 0, sizeof(uint32_t) * nb * nb, s));
+    HSVD_CUDA(cudaMemsetAsync(w.sl.ru.blkmod, 0, sizeof(uint32_t) * nb, s));
+    HSVD_CUDA(cudaMemsetAsync(w.sl.ru.dsweep, 0, sizeof(int32_t), s));
 
     KernelTimer T;
     // Split mode: the two slot halves run on two streams.  A block only
@@ -318,6 +327,13 @@ static int block_drive_t(double *G, int64_t n, int64_t r, int64_t ldg, double *V
         tl.push_back({what, e});
         return HSVD_OK;
     };
+    // replay recorded all-skip visits (k_plan) in the graphed late sweeps;
+    // the eager split sweeps only record them (HSVD_REUSE=0: never)
+    const bool reuse_ok = [] {
+        const char *e = getenv("HSVD_REUSE");
+        return !(e && e[0] == '0');
+    }();
+    bool plan_now = false;
     auto enqueue_steps_split = [&]() -> int {
         cudaStream_t ss[2] = {s, s2};
         if (tl_on) {
@@ -340,7 +356,7 @@ static int block_drive_t(double *G, int64_t n, int64_t r, int64_t ldg, double *V
                 const std::string tag = std::string(h ? "B" : "A") + std::to_string(step);
                 int e = mark(tag + " start", ss[h]);
                 if (e) return e;
-                e = K::gram_inner(G, ldg, (int)n, hw, full, cfg, ss[h], T);
+                e = K::gram_inner(G, ldg, (int)n, hw, full, cfg, ss[h], T, (int)step, plan_now);
                 if (e) return e;
                 if (step == 0 && h == 0) HSVD_CUDA(cudaEventRecord(ev_stagger, ss[h]));
                 if ((e = mark(tag + " gram+inner done", ss[h]))) return e;
@@ -368,7 +384,8 @@ static int block_drive_t(double *G, int64_t n, int64_t r, int64_t ldg, double *V
         } else {
             for (int64_t step = 0; step < nb; ++step) {
                 const int full = cfg->inner_full || step == 0;
-                int e = K::step(G, ldg, (int)n, V, ldv, (int)r, w.sl, full, cfg, s, T);
+                int e = K::step(G, ldg, (int)n, V, ldv, (int)r, w.sl, full, cfg, s, T, (int)step,
+                                plan_now);
                 if (e) return e;
             }
         }
@@ -379,9 +396,16 @@ static int block_drive_t(double *G, int64_t n, int64_t r, int64_t ldg, double *V
                                 w.sl.err, 1, s);
         if (e) return e;
         if (cfg->sort) {
+            HSVD_CUDA(cudaMemcpyAsync(w.rho_prev, w.rho, sizeof(int64_t) * r,
+                                      cudaMemcpyDeviceToDevice, s));
             e = hsvd_sort_diagonal(w.d, w.rho, w.js, r, p, w.sortws, s);
             if (e) return e;
+            k_reuse_sweep_end<<<(unsigned)((r + 255) / 256), 256, 0, s>>>(w.rho, w.rho_prev, r, b,
+                                                                         nb, w.sl.ru);
+            HSVD_LAUNCH_CHECK("k_reuse_sweep_end");
         }
+        k_reuse_next_sweep<<<1, 1, 0, s>>>(w.sl.ru.dsweep);
+        HSVD_LAUNCH_CHECK("k_reuse_next_sweep");
         T.end(s);
         HSVD_CUDA(cudaMemcpyAsync(host, w.out, 5 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
         return HSVD_OK;
@@ -395,10 +419,12 @@ static int block_drive_t(double *G, int64_t n, int64_t r, int64_t ldg, double *V
     auto capture = [&]() -> int {
         const bool keep = split_now;
         split_now = false;
+        plan_now = reuse_ok;
         HSVD_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
         int e = enqueue_sweep();
         cudaError_t ce = cudaStreamEndCapture(s, &graph);
         split_now = keep;
+        plan_now = false;
         if (e) return e;
         if (ce != cudaSuccess) return cuda_fail(ce, "cudaStreamEndCapture");
         HSVD_CUDA(cudaGraphInstantiate(&exec, graph, 0));
@@ -415,7 +441,8 @@ static int block_drive_t(double *G, int64_t n, int64_t r, int64_t ldg, double *V
     res->setup_ms = t_loop0;  // absolute for now; hsvd_drive makes it relative
     for (int64_t sweep = 0; sweep < cfg->max_sweeps; ++sweep) {
         HSVD_CUDA(cudaEventRecord(t0, s));
-        launches += (split_now ? 8 : 3) * nb + 1 + 1 + (cfg->sort ? 2 : 0);
+        launches += (split_now ? 8 : (reuse_ok && graphs ? 4 : 3)) * nb + 1 + 1 +
+                    (cfg->sort ? 3 : 0) + 1;
         if (split_now || !graphs) {
             T.on = cfg->profile && sweep == profile_sweep();
             st = enqueue_sweep();

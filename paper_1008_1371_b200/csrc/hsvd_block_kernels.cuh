@@ -88,6 +88,36 @@ struct GramPart {
     }
 };
 
+// ---------------------------------------------------------------------
+// Exact reuse of all-skip visits (the late sweeps)
+// ---------------------------------------------------------------------
+// A slot visit's outcome (rotations, W_P, code, statistics) is a function
+// of its 2b columns alone: which columns sit at its positions, their bits
+// and J signs, and the inner ordering.  When a visit of the block pair
+// (I, J) skipped every pair (no rotation: _kernels.py:210-213 applied to
+// every pair of the pass) and since then no column of blocks I and J was
+// rewritten and no sort moved another column into them, the next visit of
+// (I, J) reads the same bits and must skip every pair again: its Gram,
+// inner pass and update are not run, and its statistics are those of the
+// recorded visit.  Same bits in, same decision out, so the result is bit
+// for bit the one without reuse.
+//
+// Stamps order events: step k of sweep s is s*(nb+1) + k + 1, the sort at
+// the end of sweep s is s*(nb+1) + nb + 1.  blkmod[K] is the stamp of the
+// last event that changed block K's columns (a rotation touching one of
+// them, written by k_inner, or a sort moving another column in);
+// pairstamp[I*nb+J] is the stamp of the last all-skip visit of (I, J)
+// (bit 31: it was a full-ordering pass), pairskip its skip count.
+struct ReuseWs {
+    uint32_t *pairstamp, *pairskip, *blkmod;
+    int32_t *dsweep;  // sweeps completed (device)
+};
+
+__device__ __forceinline__ uint32_t reuse_stamp(const int32_t *dsweep, int64_t nb, int step)
+{
+    return (uint32_t)(*(volatile const int32_t *)dsweep) * (uint32_t)(nb + 1) + (uint32_t)step + 1u;
+}
+
 template <int B2, int KT, int STAGES>
 struct GramSmem {
     static constexpr int LD = KT + 4;  // == 4 mod 16: conflict-free fragments
@@ -198,7 +228,8 @@ template <int B2, int KT, int STAGES>
 __global__ void __launch_bounds__(kThreads, HSVD_GRAM_OCC) k_gram(
     const double *__restrict__ G, int64_t ldg, int n, const int64_t *__restrict__ rho,
     const int64_t *__restrict__ iblk, const int64_t *__restrict__ jblk, GramPart part,
-    int maxseg, double *__restrict__ Apart, const unsigned long long *err)
+    int maxseg, double *__restrict__ Apart, const unsigned long long *err,
+    const int32_t *__restrict__ act, const int32_t *__restrict__ nact)
 {
     using Sm = GramSmem<B2, KT, STAGES>;
     using Roles = GramRoles<B2>;
@@ -206,6 +237,16 @@ __global__ void __launch_bounds__(kThreads, HSVD_GRAM_OCC) k_gram(
     auto &S = *reinterpret_cast<Sm *>(gsm_raw);
     if (*(volatile const unsigned long long *)err != kNoError) return;
     constexpr int b = B2 / 2;
+    // reuse (k_plan): only the active slots act[0..nact) are computed; the
+    // segments of the active slots are re-dealt over the grid in equal runs
+    if (act) {
+        const int64_t na = *nact;
+        part.NS = na * part.NSEG;
+        if (part.NS == 0) return;
+        const int64_t per = (part.NS + part.P - 1) / part.P;
+        part.P = (part.NS + per - 1) / per;
+        if ((int64_t)blockIdx.x >= part.P) return;
+    }
     const int64_t cta = blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t it0 = part.begin(cta), it1 = part.begin(cta + 1);
@@ -214,7 +255,7 @@ __global__ void __launch_bounds__(kThreads, HSVD_GRAM_OCC) k_gram(
     const int nsl = (int)((it1 - 1) / part.T - slot0 + 1);  // <= MAXSLOTS (host-checked)
     for (int q = tid; q < nsl * B2; q += kThreads) {
         const int si = q / B2, c = q % B2;
-        const int64_t slot = slot0 + si;
+        const int64_t slot = act ? act[slot0 + si] : slot0 + si;
         int64_t I = iblk[slot], J = jblk[slot];
         if (I > J) { int64_t t = I; I = J; J = t; }
         S.col[si][c] = G + rho[slot_pos(c, b, I, J)] * ldg;
@@ -282,7 +323,7 @@ __global__ void __launch_bounds__(kThreads, HSVD_GRAM_OCC) k_gram(
         // is accumulated from zero by exactly one CTA
         const int seg = c_k / Lseg;
         const bool seg_end = c_k == T - 1 || c_k + 1 == (seg + 1) * Lseg;
-        const int64_t slot = slot0 + c_si;
+        const int64_t slot = act ? act[slot0 + c_si] : slot0 + c_si;
         if (++c_k == T) {
             c_k = 0;
             ++c_si;
@@ -325,6 +366,9 @@ struct InnerArgs {
     unsigned long long *err;
     int64_t nb, slot_base;
     int64_t real_cols;  // colmap values >= real_cols are inert padding columns
+    ReuseWs ru;         // all-skip reuse bookkeeping (pairstamp NULL: off)
+    const uint8_t *skipf;  // per slot: 1 = reused all-skip visit (k_plan)
+    int step;
     double eps, teps;
     int full, use_skip, passes;
     long long *trace;  // debug: per-round clock64 stamps of CTA 0 (NULL)
@@ -436,6 +480,97 @@ constexpr int kInnerThreads = HSVD_INNER_THREADS;
 template <int B2>
 __host__ __device__ constexpr int inner_threads() { return B2 == 64 ? kInnerThreads : 256; }
 
+// cur = the visited pair; advance_stepper (_kernels.py:238-251) on the
+// block indices
+__device__ __forceinline__ void inner_advance(const InnerArgs &a, int slot, int64_t I, int64_t J)
+{
+    a.cur[2 * slot] = I;
+    a.cur[2 * slot + 1] = J;
+    const int64_t r = a.nb, half = r / 2;
+    int64_t ip = a.ip[slot], jp = a.jp[slot];
+    if (ip + jp >= r - 1) {
+        ip += 1;
+        if (ip == jp) {
+            ip -= half;
+            jp = ip;
+        }
+        a.ip[slot] = ip;
+        a.jp[slot] = jp;
+        a.iblk[slot] = ip;
+    } else {
+        jp += 1;
+        a.jp[slot] = jp;
+        a.jblk[slot] = jp;
+    }
+}
+
+// k_plan: which slots of this step replay a recorded all-skip visit, and
+// the ordered list of the others (one CTA, one thread per slot: three loads
+// decide a slot, then a block-wide ordered compaction)
+constexpr int kPlanThreads = 1024;
+static __global__ void __launch_bounds__(kPlanThreads) k_plan(const int64_t *__restrict__ iblk,
+                                                       const int64_t *__restrict__ jblk,
+                                                       int64_t nslots, int64_t nb, ReuseWs ru,
+                                                       int step, int full,
+                                                       uint8_t *__restrict__ skipf,
+                                                       int32_t *__restrict__ act,
+                                                       int32_t *__restrict__ nact,
+                                                       const unsigned long long *err)
+{
+    __shared__ int wcnt[kPlanThreads / 32];
+    __shared__ int base;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t stamp = reuse_stamp(ru.dsweep, nb, step);
+    const bool failed = *(volatile const unsigned long long *)err != kNoError;
+    if (tid == 0) base = 0;
+    for (int64_t s0 = 0; s0 < nslots; s0 += kPlanThreads) {
+        const int64_t slot = s0 + tid;
+        int sk = 0;
+        if (slot < nslots && !failed) {
+            int64_t I = iblk[slot], J = jblk[slot];
+            if (I > J) { int64_t t = I; I = J; J = t; }
+            const uint32_t ps = ru.pairstamp[I * nb + J];
+            const uint32_t m = max(ru.blkmod[I], ru.blkmod[J]);
+            const uint32_t at = ps & 0x7fffffffu;
+            sk = ps != 0u && (int)(ps >> 31) >= (full != 0) && m < at && at < stamp;
+        }
+        if (slot < nslots) skipf[slot] = (uint8_t)sk;
+        const int live = slot < nslots && !sk;
+        const unsigned bal = __ballot_sync(0xffffffffu, live);
+        if (lane == 0) wcnt[warp] = __popc(bal);
+        __syncthreads();
+        if (warp == 0) {
+            // exclusive scan of the warp counts
+            const int v = wcnt[lane];
+            int x = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            wcnt[lane] = x - v;
+        }
+        __syncthreads();
+        if (live) act[base + wcnt[warp] + __popc(bal & ((1u << lane) - 1u))] = (int32_t)slot;
+        __syncthreads();
+        if (tid == kPlanThreads - 1) base += wcnt[warp] + __popc(bal);
+        __syncthreads();
+    }
+    if (tid == 0) *nact = base;
+}
+
+// sweep end: blocks whose positions received another column in the sort
+// are stamped, then the sweep counter advances (one CTA per 256 positions)
+static __global__ void k_reuse_sweep_end(const int64_t *__restrict__ rho,
+                                  const int64_t *__restrict__ rho_prev, int64_t r, int b,
+                                  int64_t nb, ReuseWs ru)
+{
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const uint32_t stamp = reuse_stamp(ru.dsweep, nb, (int)nb);
+    if (k < r && rho[k] != rho_prev[k]) ru.blkmod[k / b] = stamp;
+}
+static __global__ void k_reuse_next_sweep(int32_t *dsweep) { *dsweep += 1; }
+
 template <int B2, bool FAST>
 __global__ void __launch_bounds__(inner_threads<B2>()) k_inner(InnerArgs a)
 {
@@ -447,6 +582,16 @@ __global__ void __launch_bounds__(inner_threads<B2>()) k_inner(InnerArgs a)
     const int slot = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     int64_t I = a.iblk[slot], J = a.jblk[slot];
     if (I > J) { int64_t t = I; I = J; J = t; }
+    if (a.skipf && a.skipf[slot]) {
+        // reused all-skip visit: the recorded statistics, no rotation, no
+        // update (empty touched set), stepper advanced as usual
+        if (tid == 0) {
+            a.tset[(int64_t)slot * kTsetStride] = 0;
+            a.skipk[slot] += a.ru.pairskip[I * a.nb + J];
+            inner_advance(a, slot, I, J);
+        }
+        return;
+    }
 
     // A = sum of the slot's partial segments in segment order (the upper
     // triangle is read coalesced and mirrored); all loads of a batch of
@@ -726,25 +871,19 @@ __global__ void __launch_bounds__(inner_threads<B2>()) k_inner(InnerArgs a)
         a.skipk[slot] += S.skip;
         const double mt = __longlong_as_double((long long)S.maxt_bits);
         if (mt > a.maxt[slot]) a.maxt[slot] = mt;
-        a.cur[2 * slot] = I;
-        a.cur[2 * slot + 1] = J;
-        // advance_stepper (_kernels.py:238-251) on the block indices
-        const int64_t r = a.nb, half = r / 2;
-        int64_t ip = a.ip[slot], jp = a.jp[slot];
-        if (ip + jp >= r - 1) {
-            ip += 1;
-            if (ip == jp) {
-                ip -= half;
-                jp = ip;
+        if (a.ru.pairstamp) {
+            const uint32_t stamp = reuse_stamp(a.ru.dsweep, a.nb, a.step);
+            if (S.touched) {
+                // the blocks' columns are rewritten by this step's update
+                a.ru.blkmod[I] = stamp;
+                a.ru.blkmod[J] = stamp;
+            } else if (!S.rot) {
+                // an all-skip visit: recorded for reuse
+                a.ru.pairstamp[I * a.nb + J] = stamp | ((uint32_t)(a.full != 0) << 31);
+                a.ru.pairskip[I * a.nb + J] = S.skip;
             }
-            a.ip[slot] = ip;
-            a.jp[slot] = jp;
-            a.iblk[slot] = ip;
-        } else {
-            jp += 1;
-            a.jp[slot] = jp;
-            a.jblk[slot] = jp;
         }
+        inner_advance(a, slot, I, J);
     }
 }
 
@@ -960,10 +1099,17 @@ struct SlotWs {
     int64_t real_cols;  // colmap values >= this are padding (INT64_MAX: none)
     GramPart gp;
     int maxseg;
+    // all-skip reuse (ru.pairstamp NULL: off): per-slot flags, the active
+    // slot list of the launch and its length
+    ReuseWs ru;
+    uint8_t *skipf;
+    int32_t *act, *nact;
 };
 
-// Carve the per-slot arrays for nslots slots of a problem with nb blocks.
-inline void carve_slots(Carve2 &c, int64_t n, int64_t nslots, int64_t nb, int b, SlotWs *w)
+// Carve the per-slot arrays for nslots slots of a problem with nb blocks
+// (with the all-skip reuse bookkeeping when reuse is set).
+inline void carve_slots(Carve2 &c, int64_t n, int64_t nslots, int64_t nb, int b, SlotWs *w,
+                        bool reuse = false)
 {
     const int64_t B2 = 2 * b;
     const GramPart gp = gram_partition(n, nslots);
@@ -984,6 +1130,17 @@ inline void carve_slots(Carve2 &c, int64_t n, int64_t nslots, int64_t nb, int b,
     t.Apart = c.take<double>(nslots * ks * B2 * B2);
     t.Wg = c.take<double>(nslots * B2 * B2);
     t.colidx = c.take<int64_t>(nslots * B2);
+    t.skipf = c.take<uint8_t>(nslots);
+    t.act = c.take<int32_t>(nslots);
+    t.nact = c.take<int32_t>(4);
+    t.ru.pairstamp = t.ru.pairskip = t.ru.blkmod = nullptr;
+    t.ru.dsweep = nullptr;
+    if (reuse) {
+        t.ru.pairstamp = c.take<uint32_t>(nb * nb);
+        t.ru.pairskip = c.take<uint32_t>(nb * nb);
+        t.ru.blkmod = c.take<uint32_t>(nb);
+        t.ru.dsweep = c.take<int32_t>(1);
+    }
     t.nslots = nslots;
     t.nb = nb;
     t.slot_base = 0;
@@ -1027,8 +1184,11 @@ struct BlockKernels {
         return HSVD_OK;
     }
     // Gram -> inner pass of one step
+    // Gram -> inner pass of step `step`; plan: replay recorded all-skip
+    // visits (k_plan) instead of recomputing them
     static int gram_inner(double *G, int64_t ldg, int n, const SlotWs &w, int full,
-                          const hsvd_config *cfg, cudaStream_t s, KernelTimer &T)
+                          const hsvd_config *cfg, cudaStream_t s, KernelTimer &T, int step,
+                          bool plan)
     {
         const int64_t nslots = w.nslots;
         const GramPart &gp = w.gp;
@@ -1036,7 +1196,13 @@ struct BlockKernels {
             set_error("block mode: too many slots per Gram CTA (r too large for this GPU)");
             return HSVD_ERR_UNSUPPORTED;
         }
+        plan = plan && w.ru.pairstamp != nullptr;
         T.begin(0, s);
+        if (plan) {
+            k_plan<<<1, kPlanThreads, 0, s>>>(w.iblk, w.jblk, nslots, w.nb, w.ru, step, full,
+                                              w.skipf, w.act, w.nact, w.err);
+            HSVD_LAUNCH_CHECK("k_plan");
+        }
         {
             // Gram and inner pass are the critical path of a step: highest
             // priority (split mode runs a bulk update on another stream)
@@ -1052,7 +1218,9 @@ struct BlockKernels {
             lc.numAttrs = 1;
             HSVD_CUDA(cudaLaunchKernelEx(&lc, k_gram<B2, KT, STAGES>, G, ldg, n, w.colmap,
                                          (const int64_t *)w.iblk, (const int64_t *)w.jblk, gp,
-                                         w.maxseg, w.Apart, (const unsigned long long *)w.err));
+                                         w.maxseg, w.Apart, (const unsigned long long *)w.err,
+                                         (const int32_t *)(plan ? w.act : nullptr),
+                                         (const int32_t *)w.nact));
         }
         T.end(s);
         HSVD_LAUNCH_CHECK("k_gram");
@@ -1065,6 +1233,9 @@ struct BlockKernels {
         ia.full = full; ia.use_skip = cfg->use_skip;
         ia.passes = cfg->inner_passes > 1 ? cfg->inner_passes : 1;
         ia.trace = nullptr;
+        ia.ru = w.ru;
+        ia.skipf = plan ? w.skipf : nullptr;
+        ia.step = step;
         T.begin(1, s);
         {
             // the inner pass is latency bound on few SMs: launched at the
@@ -1120,9 +1291,9 @@ struct BlockKernels {
     // one step: Gram -> inner pass -> update
     static int step(double *G, int64_t ldg, int n, double *V, int64_t ldv, int rv,
                     const SlotWs &w, int full, const hsvd_config *cfg, cudaStream_t s,
-                    KernelTimer &T)
+                    KernelTimer &T, int stepno, bool plan)
     {
-        int e = gram_inner(G, ldg, n, w, full, cfg, s, T);
+        int e = gram_inner(G, ldg, n, w, full, cfg, s, T, stepno, plan);
         if (e) return e;
         return update(G, ldg, n, V, ldv, rv, w, 0, w.nslots, s, T);
     }

@@ -860,7 +860,7 @@ struct ShardedDriver {
                         HSVD_CUDA(cudaStreamWaitEvent(ss[h], x.e_stag, 0));
                     }
                     double *V = withV ? x.w.Vs : nullptr;
-                    HSVD_CUDA_OK(K::gram_inner(x.w.Gs, n, (int)n, hw, full, cfg, ss[h], Toff));
+                    HSVD_CUDA_OK(K::gram_inner(x.w.Gs, n, (int)n, hw, full, cfg, ss[h], Toff, (int)step, false));
                     if (step == 0 && h == 0) HSVD_CUDA(cudaEventRecord(x.e_stag, ss[h]));
                     HSVD_CUDA_OK(K::update(x.w.Gs, n, (int)n, V, r, (int)r, hw, 0, 1, ss[h], Toff,
                                            true));
@@ -1088,7 +1088,7 @@ struct ShardedDriver {
                         HSVD_CUDA(cudaSetDevice(x.dev));
                         HSVD_CUDA_OK(K::step(x.w.Gs, n, (int)n, withV ? x.w.Vs : nullptr, r,
                                              (int)r, x.w.sl, full, cfg, x.s,
-                                             &x == &sh[0] ? T : Toff));
+                                             &x == &sh[0] ? T : Toff, (int)step, false));
                         launches += 3;
                     }
                     HSVD_CUDA_OK(pl.advance(mv));

@@ -15,7 +15,14 @@ from tests.golden.inputs import make_case_input
 pytestmark = pytest.mark.gpu
 
 SIGMA_RTOL = 1e-10     # north star: "singular values within ~1e-10"
-RESID_FACTOR = 4.0     # block residuals vs the reference's own (reported)
+# block residuals at or below the reference's own (north star) with the
+# default "fast" rotation; measured ratios for every case are in
+# profiles/r02_block_residual_ratios.md (worst: dU 0.96, VtJV 0.37, recon
+# 0.30).  The "dd" variant (the reference's double-double rotation_tc inside
+# the block inner pass, a cross-check, not the default or benchmarked path)
+# measures up to 1.6x on recon / VtJV (same table): band 2.0.
+RESID_FACTOR = 1.0
+RESID_FACTOR_ROT = {"fast": 1.0, "dd": 2.0}
 
 CASES = [
     # n, r, p, seed, kind, b
@@ -45,11 +52,11 @@ def test_block_matches_reference(case, rot):
     assert d <= SIGMA_RTOL, d
     rb, rr = residuals(G, res, signs), residuals(G, ref, signs)
     for k in rb:
-        assert rb[k] <= RESID_FACTOR * rr[k] + 1e-15, (k, rb[k], rr[k])
+        assert rb[k] <= RESID_FACTOR_ROT[rot] * rr[k], (k, rb[k], rr[k])
     # block sweeps: the full inner ordering (default) rotates every pair of
-    # the pivot block at every step, so it never needs more sweeps than the
-    # reference (up to a small band) and often needs fewer
-    assert res.sweeps_used <= ref.sweeps_used + 3, (res.sweeps_used, ref.sweeps_used)
+    # the pivot block at every step; it never needs more sweeps than the
+    # reference in any measured case (7-11 vs 8-14)
+    assert res.sweeps_used <= ref.sweeps_used, (res.sweeps_used, ref.sweeps_used)
 
 
 def test_block_big_golden(golden_big):
@@ -69,7 +76,7 @@ def test_block_big_golden(golden_big):
         assert rb["dU"] <= RESID_FACTOR * c["dU"], (c["name"], rb, c["dU"])
         assert rb["vjv"] <= RESID_FACTOR * c["VtJV"], (c["name"], rb, c["VtJV"])
         assert rb["recon"] <= RESID_FACTOR * c["recon"], (c["name"], rb, c["recon"])
-        assert res.sweeps_used <= c["sweeps_used"] + 3
+        assert res.sweeps_used <= c["sweeps_used"]
 
 
 def test_block_deterministic():
@@ -115,16 +122,17 @@ def test_block_any_even_r(case):
     assert sigma_class_reldiff(res.sigma, res.lam, ref.sigma, ref.lam) <= SIGMA_RTOL
     rb, rr = residuals(G, res, signs), residuals(G, ref, signs)
     for k in rb:
-        assert rb[k] <= RESID_FACTOR * rr[k] + 1e-15, (k, rb[k], rr[k])
-    # pairs with a padding column are not counted as visits
-    assert res.rotations + res.skips <= res.sweeps_used * r * (r - 1)
+        assert rb[k] <= RESID_FACTOR * rr[k], (k, rb[k], rr[k])
 
 
 def test_block_padding_identity_diag():
     G = np.asfortranarray(np.diag(np.arange(40, 0, -1, dtype=np.float64)))
     res = H.drive(G, H.SignatureVector.from_p(40, 20), H.SolverConfig(mode="block", block_cols=32))
-    assert res.stop_reason == "orthogonal" and res.rotations == 0
+    assert res.stop_reason == "orthogonal" and res.rotations == 0 and res.sweeps_used == 1
     assert np.array_equal(np.sort(res.sigma), np.arange(1.0, 41.0))
+    # pairs with a padding column are not visits: r_pad = 64, one slot, two
+    # steps of the full ordering, 40 * 39 / 2 real pairs each
+    assert res.skips == 2 * (40 * 39 // 2)
 
 
 def test_block_config3_n4096_p3072_against_pointwise():
@@ -141,7 +149,7 @@ def test_block_config3_n4096_p3072_against_pointwise():
     assert sigma_class_reldiff(res.sigma, res.lam, ref.sigma, ref.lam) <= SIGMA_RTOL
     rb, rr = residuals(G, res, signs), residuals(G, ref, signs)
     for k in rb:
-        assert rb[k] <= 2.0 * rr[k], (k, rb[k], rr[k])
+        assert rb[k] <= rr[k], (k, rb[k], rr[k])
     assert res.sweeps_used <= ref.sweeps_used
 
 
@@ -173,3 +181,23 @@ def test_sharded_definiteness_lost_raises(N):
     G, J = _definiteness_case()
     with pytest.raises(H.DefinitenessLostError):
         H.drive_local_shards(G, J, H.SolverConfig(mode="block", block_cols=16), nshards=N)
+
+
+@pytest.mark.parametrize("streams", [1, 2])
+def test_block_allskip_reuse_is_exact(streams, monkeypatch):
+    """Replaying recorded all-skip visits (k_plan, the late sweeps) gives the
+    bits, sweeps and statistics of recomputing them (_kernels.py:210-213:
+    the skip decision is a function of the pair's columns alone)."""
+    for kind, n, p in (("gauss", 1024, 512), ("graded12", 512, 256)):
+        G = make_case_input(n, n, 3, kind)
+        J = H.SignatureVector.from_p(n, p)
+        cfg = H.SolverConfig(mode="block", block_streams=streams)
+        monkeypatch.setenv("HSVD_REUSE", "0")
+        a = H.drive(G, J, cfg)
+        monkeypatch.setenv("HSVD_REUSE", "1")
+        b = H.drive(G, J, cfg)
+        assert (a.sweeps_used, a.stop_reason, a.rotations, a.skips) == \
+            (b.sweeps_used, b.stop_reason, b.rotations, b.skips)
+        assert a.telemetry == b.telemetry
+        for f in ("sigma", "lam", "U", "Vinv_t"):
+            assert np.array_equal(getattr(a, f), getattr(b, f)), f

@@ -4,6 +4,7 @@ rotations, skips, telemetry).  Calls go through the C ABI via the host
 package, exactly the path drive() uses."""
 
 import numpy as np
+import torch
 import pytest
 
 import paper_1008_1371_b200 as H
