@@ -127,6 +127,52 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+# ---------------------------------------------------------------- FP64 peak
+
+
+def measure_fp64_peak(dev, n=8192, sustain_s=4.0):
+    """The FP64 roofline denominators on THIS box, before the timed region:
+    cuBLAS DGEMM n^3 (torch.matmul float64; the library's DMMA GEMM is the
+    reference ceiling for k_update / k_gram).  burst = best single call of
+    10 after warm-up; sustained = back-to-back calls for >= sustain_s
+    seconds (the solve runs for seconds, so its kernels are compared with
+    the sustained figure), with nvidia-smi clocks sampled during that loop."""
+    import torch
+    a = torch.randn(n, n, dtype=torch.float64, device=dev)
+    b = torch.randn(n, n, dtype=torch.float64, device=dev)
+    for _ in range(3):
+        c = a @ b
+    torch.cuda.synchronize()
+    best = 1e9
+    for _ in range(10):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        c = a @ b
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    flop = 2.0 * n ** 3
+    clk = ClockSampler(dev.index if dev.index is not None else 0)
+    clk.start()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    calls = max(8, int(sustain_s / (best / 1e3)))
+    e0.record()
+    for _ in range(calls):
+        c = a @ b
+    e1.record()
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    sus_ms = e0.elapsed_time(e1)
+    del a, b, c
+    torch.cuda.empty_cache()
+    return {"burst_tflops": flop / (best / 1e3) / 1e12,
+            "sustained_tflops": flop * calls / (sus_ms / 1e3) / 1e12,
+            "sustained_s": sus_ms / 1e3, "dgemm_n": n, "clocks_sustained": clocks,
+            "source": "cuBLAS DGEMM (torch.matmul float64) measured in this bench run"}
+
+
 # ---------------------------------------------------------------- CPU legs
 
 
@@ -137,10 +183,32 @@ def cpu_threads():
         return os.cpu_count() or 1
 
 
+XL_GOLDEN = os.path.join(ROOT, "tests", "golden", "golden_xl.json")
+
+
+def load_measured_reference(n, p):
+    """The reference algorithm run to COMPLETION on the build host for this
+    input (tests/golden/make_golden_xl.py: the oracle, bit-exact with
+    hjsvd): telemetry, wall time and thread count, or None."""
+    if not os.path.exists(XL_GOLDEN):
+        return None
+    with open(XL_GOLDEN) as f:
+        for c in json.load(f)["cases"]:
+            if c["n"] == n and c["r"] == n and c["p"] == p and c["kind"] == "gauss":
+                return c
+    return None
+
+
 def load_reference_telemetry(n, p):
-    """Per-sweep (rotations, skips) of the reference on this exact input.
-    The pointwise GPU mode is bit-exact with the reference, so its telemetry
-    IS the reference's; bench.py records it in profiles/ when it runs."""
+    """Per-sweep (rotations, skips) of the reference on this exact input:
+    from the full reference run (golden_xl.json) when there is one, else
+    from profiles/reference_telemetry.json (the pointwise GPU mode, which is
+    bit-exact with the reference)."""
+    c = load_measured_reference(n, p)
+    if c is not None:
+        return {"sweeps": c["sweeps_used"], "rotations": c["rotations"], "skips": c["skips"],
+                "per_sweep": [[t[1], t[2]] for t in c["telemetry"]],
+                "source": "full reference run on the build host (tests/golden/golden_xl.json)"}
     if os.path.exists(TELEMETRY_FILE):
         with open(TELEMETRY_FILE) as f:
             data = json.load(f)
@@ -191,18 +259,33 @@ def cpu_reference_estimate(G, signs, p, budget_s, threads, telemetry):
         rot = telemetry["rotations"]
         skip = telemetry["skips"]
         sweeps = telemetry["sweeps"]
-        how = "exact per-sweep rotation/skip counts of this input"
+        how = ("exact rotation/skip counts of this input ("
+               + telemetry.get("source", "pointwise GPU mode") + ")")
     else:  # no telemetry yet: every visit of 14 sweeps rotates (upper bound)
         sweeps = 14
         rot, skip = sweeps * r * half, 0
         how = "assumed 14 sweeps, every visit rotating (upper bound)"
     est = rot * c_rot + skip * c_skip
-    sample = (f"oracle C restatement (bit-exact with hjsvd), {threads} threads: "
+    sample = (f"EXTRAPOLATED: oracle C restatement (bit-exact with hjsvd), {threads} threads: "
               f"{steps_a} steps of sweep 0 on G ({ta:.1f} s) + {steps_b} all-skip steps "
               f"on I ({tb:.1f} s) -> c_rot={c_rot*1e6:.2f} us, c_skip={c_skip*1e6:.2f} us "
               f"per pair visit; extrapolated with {how}: {rot} rotations + {skip} skips "
               f"over {sweeps} sweeps")
     return est, sample
+
+
+def measured_full(n, p):
+    """The measured full reference solve of this input (build host), reported
+    beside the per-run extrapolation."""
+    c = load_measured_reference(n, p)
+    if c is None:
+        return None
+    out = {"wall_s": c["wall_s"], "threads": c["threads"], "sweeps": c["sweeps_used"],
+           "solver": c["solver"], "host": "build container (8-core x86; not the GPU box)",
+           "source": "tests/golden/golden_xl.json"}
+    if "hjsvd" in c:
+        out["stock_hjsvd"] = c["hjsvd"]
+    return out
 
 
 def run_reference(a, rank, world):
@@ -230,7 +313,8 @@ def run_reference(a, rank, world):
         "config": {"workload": f"n={a.n} p={a.p} full HSVD with V^-T (SURVEY.md §8(d) cfg 5)",
                    "n": a.n, "p": a.p},
         "cpu_baseline": {"value": v, "unit": "s", "cores": threads, "kind": "port",
-                         "sample": sample},
+                         "sample": sample,
+                         "measured_full_solve": measured_full(a.n, a.p)},
         "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -301,6 +385,8 @@ def run_ours(a, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    # FP64 roofline denominators on this box (before the timed region)
+    fp64 = measure_fp64_peak(dev) if a.mode == "block" else {}
     res = None
     for _ in range(a.warmup):
         res = solve()
@@ -367,11 +453,8 @@ def run_ours(a, rank, world, local_rank):
               "update": 2.0 * (n + r) * b2 * b2 * nslots}  # [G_P; V_P] W_P per slot
         dom = max(("gram", "update"), key=lambda k: kp[k]["ms"])
         avg_s = kp[dom]["ms"] / kp[dom]["launches"] / 1e3
-        fp64 = {}
-        pk = os.path.join(ROOT, "profiles", "r01_fp64_dgemm_peak.json")
-        if os.path.exists(pk):
-            fp64 = json.load(open(pk))
-        peak = float(fp64.get("fp64_tflops", 37.0))
+        # k_update runs inside a seconds-long solve: sustained denominator
+        peak = float(fp64["sustained_tflops"])
         achieved = fl[dom] / avg_s / 1e12
         tot_ms = sum(v["ms"] for v in kp.values())
         solve_tflops = res.sweeps_used * 12.0 * n ** 3 / value / 1e12
@@ -382,9 +465,12 @@ def run_ours(a, rank, world, local_rank):
                     "traffic": tr["bytes_per_launch"] if isinstance(tr, dict) else tr,
                     "kernel": f"k_{dom}", "launch_avg_ms": avg_s * 1e3,
                     "alg_flop_per_launch": fl[dom],
-                    "peak_source": ("cuBLAS DGEMM 8192^3 measured on this pool "
-                                    "(profiles/r01_fp64_dgemm_peak.json); DMMA microbench 37.1 "
-                                    "(profiles/r01_fp64_micro.jsonl)") if fp64 else "nominal 37",
+                    "peak_source": ("sustained cuBLAS DGEMM 8192^3 on this box in this run "
+                                    f"({fp64['sustained_s']:.1f} s loop); burst "
+                                    f"{fp64['burst_tflops']:.2f} TFLOP/s"),
+                    "peak_burst": fp64["burst_tflops"],
+                    "frac_burst": achieved / fp64["burst_tflops"],
+                    "fp64_peak_measurement": fp64,
                     "kernel_share_sweep0": {k: round(v["ms"] / tot_ms, 4) for k, v in kp.items()},
                     "kernel_ms_sweep0": {k: round(v["ms"], 3) for k, v in kp.items()},
                     "gram_tflops": fl["gram"] / (kp["gram"]["ms"] / kp["gram"]["launches"] / 1e3) / 1e12,
@@ -456,7 +542,7 @@ def run_ours(a, rank, world, local_rank):
         est, sample = cpu_reference_estimate(G, signs, a.p, a.cpu_sample_s,
                                              cpu_threads(), tel)
         cpu = {"value": est, "unit": "s", "cores": cpu_threads(), "kind": "port",
-               "sample": sample}
+               "sample": sample, "measured_full_solve": measured_full(a.n, a.p)}
     if comm is not None:
         comm.close()
 

@@ -73,6 +73,34 @@ __global__ void k_block_norms(const double *__restrict__ G, int64_t ldg, int n,
     }
 }
 
+typedef CUresult (*TensorMapEncodeFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                      const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                      const cuuint32_t *, CUtensorMapInterleave,
+                                      CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                      CUtensorMapFloatOOBfill);
+
+int make_gram_tensor_map(CUtensorMap *tm, const double *G, int64_t ld, int64_t n, int64_t ncols)
+{
+    static TensorMapEncodeFn enc = [] {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+                cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            fn = nullptr;
+        return (TensorMapEncodeFn)fn;
+    }();
+    if (!enc || (ld * 8) % 16 || ((uintptr_t)G & 15)) return 1;
+    const cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)ncols};
+    const cuuint64_t strides[1] = {(cuuint64_t)ld * 8};
+    const cuuint32_t box[2] = {16, 1};
+    const cuuint32_t es[2] = {1, 1};
+    const CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void *)G, dims, strides, box,
+                           es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? 0 : 1;
+}
+
 int launch_block_norms(const double *G, int64_t ldg, int64_t n, const int64_t *rho, int64_t r,
                        double *d, unsigned long long *first_zero, cudaStream_t s)
 {
@@ -237,6 +265,12 @@ static int block_drive_t(double *G, int64_t n, int64_t r, int64_t ldg, double *V
     }
     // columns with rho >= r_real are padding (block_drive_padded)
     w.sl.real_cols = w.half[0].real_cols = w.half[1].real_cols = r_real;
+    // the Gram's TMA view of G (HSVD_GRAM_TMA=0 in the environment: cp.async)
+    alignas(64) CUtensorMap gmap;
+    const char *tma_env = getenv("HSVD_GRAM_TMA");
+    if (HSVD_GRAM_TMA && !(tma_env && tma_env[0] == '0') &&
+        make_gram_tensor_map(&gmap, G, ldg, n, r) == 0)
+        w.sl.gmap = w.half[0].gmap = w.half[1].gmap = &gmap;
     int st = K::setup();
     if (st) return st;
 

@@ -3,6 +3,7 @@
 // driver (hsvd_block.cu) and the sharded multi-GPU driver (hsvd_sharded.cu).
 #pragma once
 
+#include <cuda.h>  // CUtensorMap (the encoder is fetched at run time: no libcuda link)
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -17,6 +18,15 @@
 #define HSVD_GRAM_KT 64
 #define HSVD_GRAM_STAGES 2
 #define HSVD_GRAM_OCC 3
+#endif
+// k_gram operand pipeline: 1 = TMA (cp.async.bulk.tensor gather4 through
+// rho) + mbarrier ring with a producer warp; 0 = the cp.async kernel
+#ifndef HSVD_GRAM_TMA
+#define HSVD_GRAM_TMA 1
+#endif
+#ifndef HSVD_GRAM_TMA_STAGES
+#define HSVD_GRAM_TMA_STAGES 3
+#define HSVD_GRAM_TMA_OCC 2
 #endif
 
 namespace hsvd {
@@ -33,6 +43,41 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *gmem, int src
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// mbarrier + TMA (sm_90+ PTX; gather4 is sm_100a)
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned bar)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity)
+{
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "HSVD_MBW_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra HSVD_MBW_%=;\n}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+// 4 arbitrary columns (dim-1 coordinates c0..c3) x 16 consecutive rows from
+// row k0 of the column-major factor, into 4 x 128 swizzled bytes at dst
+__device__ __forceinline__ void tma_gather4(unsigned dst, const CUtensorMap *tm, int k0, int c0,
+                                            int c1, int c2, int c3, unsigned bar)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n" ::"r"(dst),
+        "l"(tm), "r"(k0), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
+        : "memory");
+}
 
 // D(8x8) += A(8x4, row) * B(4x8, col), FP64 tensor core.
 // a = A[lane>>2][lane&3], b = B[lane&3][lane>>2],
@@ -136,6 +181,8 @@ struct GramSmem {
 template <int B2>
 struct GramRoles;
 
+// ld(R) returns this lane's fragment element of row R + (lane >> 2) at the
+// current k-step (column k + (lane & 3)); R is a multiple of 8.
 template <>
 struct GramRoles<64> {
     // 36 upper 8x8 tiles over 8 warps, 9 per SM sub-partition (warps w and
@@ -143,29 +190,27 @@ struct GramRoles<64> {
     // super-tile (4 tiles); warps 4 and 5 add one diagonal tile each, (1,1)
     // and (3,3); warps 6 and 7 own the remaining 10 diagonal-block tiles.
     static constexpr int NACC = 5;  // accumulator tiles per warp (max)
-    template <int LD>
-    __device__ static void mma(int warp, const double (*X)[LD], int kk,
-                               int fr, int fk, double (&acc)[NACC][2])
+    template <class LD>
+    __device__ static void mma(int warp, LD &&ld, double (&acc)[NACC][2])
     {
         if (warp < 6) {
             const int R = warp < 3 ? 0 : (warp < 5 ? 1 : 2);
             const int C = warp < 3 ? warp + 1 : (warp < 5 ? warp - 1 : 3);
-            const double a0 = X[16 * R + fr][kk + fk], a1 = X[16 * R + 8 + fr][kk + fk];
-            const double b0 = X[16 * C + fr][kk + fk], b1 = X[16 * C + 8 + fr][kk + fk];
+            const double a0 = ld(16 * R), a1 = ld(16 * R + 8);
+            const double b0 = ld(16 * C), b1 = ld(16 * C + 8);
             dmma(acc[0][0], acc[0][1], a0, b0);
             dmma(acc[1][0], acc[1][1], a0, b1);
             dmma(acc[2][0], acc[2][1], a1, b0);
             dmma(acc[3][0], acc[3][1], a1, b1);
             if (warp >= 4) {  // tile (1,1) (warp 4) or (3,3) (warp 5)
-                const double e = X[8 * (2 * warp - 7) + fr][kk + fk];
+                const double e = ld(8 * (2 * warp - 7));
                 dmma(acc[4][0], acc[4][1], e, e);
             }
         } else {
             // warp 6: (0,0) (0,1) (4,4) (4,5) (5,5); warp 7: (2,2) (2,3) (6,6) (6,7) (7,7)
             const int d = warp - 6;  // diagonal super-tiles d and d + 2
-            const double f0 = X[16 * d + fr][kk + fk], f1 = X[16 * d + 8 + fr][kk + fk];
-            const double g0 = X[16 * (d + 2) + fr][kk + fk];
-            const double g1 = X[16 * (d + 2) + 8 + fr][kk + fk];
+            const double f0 = ld(16 * d), f1 = ld(16 * d + 8);
+            const double g0 = ld(16 * (d + 2)), g1 = ld(16 * (d + 2) + 8);
             dmma(acc[0][0], acc[0][1], f0, f0);
             dmma(acc[1][0], acc[1][1], f0, f1);
             dmma(acc[2][0], acc[2][1], g0, g0);
@@ -210,16 +255,15 @@ struct GramRoles<32> {
         rt = (int)((0x3221110000ull >> (4 * t)) & 0xF);
         ct = (int)((0x3323213210ull >> (4 * t)) & 0xF);
     }
-    template <int LD>
-    __device__ static void mma(int warp, const double (*X)[LD], int kk,
-                               int fr, int fk, double (&acc)[NACC][2])
+    template <class LD>
+    __device__ static void mma(int warp, LD &&ld, double (&acc)[NACC][2])
     {
         int rt, ct;
         tile(warp, 0, rt, ct);
-        dmma(acc[0][0], acc[0][1], X[8 * rt + fr][kk + fk], X[8 * ct + fr][kk + fk]);
+        dmma(acc[0][0], acc[0][1], ld(8 * rt), ld(8 * ct));
         if (warp < 2) {
             tile(warp, 1, rt, ct);
-            dmma(acc[1][0], acc[1][1], X[8 * rt + fr][kk + fk], X[8 * ct + fr][kk + fk]);
+            dmma(acc[1][0], acc[1][1], ld(8 * rt), ld(8 * ct));
         }
     }
 };
@@ -318,7 +362,8 @@ __global__ void __launch_bounds__(kThreads, HSVD_GRAM_OCC) k_gram(
         const auto X = S.x[st_c];
         st_c = st_c + 1 == STAGES ? 0 : st_c + 1;
 #pragma unroll
-        for (int kk = 0; kk < KT; kk += 4) Roles::mma(warp, X, kk, fr, fk, acc);
+        for (int kk = 0; kk < KT; kk += 4)
+            Roles::mma(warp, [&](int R) { return X[R + fr][kk + fk]; }, acc);
         // CTA runs start and end on segment boundaries, so every segment
         // is accumulated from zero by exactly one CTA
         const int seg = c_k / Lseg;
@@ -346,6 +391,156 @@ __global__ void __launch_bounds__(kThreads, HSVD_GRAM_OCC) k_gram(
     }
     cp_async_wait<0>();
 }
+
+// ---------------------------------------------------------------------
+// k_gram_tma: the same partial Grams (same segments, same DMMA sequence,
+// hence the same bits), operands brought in by TMA
+// ---------------------------------------------------------------------
+// A stage is KT rows of the CTA's B2 columns, stored as KT/16 sub-tiles of
+// B2 x 128 bytes (16 doubles of one column per 128-byte line) with the
+// 128-byte swizzle: the 16-byte chunk j of line c sits at chunk j ^ (c & 7),
+// so the 8 lines x 4 k of a DMMA fragment hit 16 distinct chunks (two
+// wavefronts, no conflict) without padding.  One producer warp issues the
+// gather4 copies (4 columns through rho x 16 rows each; 64 per stage at
+// b = 32) into a STAGES-deep ring of full/empty mbarriers; the 8 consumer
+// warps keep the cp.async kernel's DMMA roles and accumulation order.
+template <int B2, int KT, int STAGES>
+struct GramTmaSmem {
+    static constexpr int SUB = KT / 16;
+    static constexpr int STAGE_BYTES = SUB * B2 * 128;
+    static constexpr int MAXSLOTS = 4;
+    alignas(1024) unsigned char x[STAGES][STAGE_BYTES];
+    unsigned long long full[STAGES], empty[STAGES];
+    int cidx[MAXSLOTS][B2];
+};
+
+template <int B2, int KT, int STAGES>
+__global__ void __launch_bounds__(kThreads + 32, HSVD_GRAM_TMA_OCC) k_gram_tma(
+    const __grid_constant__ CUtensorMap gmap, int n, const int64_t *__restrict__ rho,
+    const int64_t *__restrict__ iblk, const int64_t *__restrict__ jblk, GramPart part,
+    int maxseg, double *__restrict__ Apart, const unsigned long long *err,
+    const int32_t *__restrict__ act, const int32_t *__restrict__ nact)
+{
+    using Sm = GramTmaSmem<B2, KT, STAGES>;
+    using Roles = GramRoles<B2>;
+    extern __shared__ __align__(1024) unsigned char gtm_raw[];
+    // dynamic shared memory is only 16-byte aligned by contract: align up
+    auto &S = *reinterpret_cast<Sm *>(
+        gtm_raw + ((1024 - ((unsigned)__cvta_generic_to_shared(gtm_raw) & 1023)) & 1023));
+    if (*(volatile const unsigned long long *)err != kNoError) return;
+    constexpr int b = B2 / 2;
+    if (act) {
+        const int64_t na = *nact;
+        part.NS = na * part.NSEG;
+        if (part.NS == 0) return;
+        const int64_t per = (part.NS + part.P - 1) / part.P;
+        part.P = (part.NS + per - 1) / per;
+        if ((int64_t)blockIdx.x >= part.P) return;
+    }
+    const int64_t cta = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t it0 = part.begin(cta), it1 = part.begin(cta + 1);
+    if (it1 <= it0) return;
+    const int64_t slot0 = it0 / part.T;
+    const int nsl = (int)((it1 - 1) / part.T - slot0 + 1);  // <= MAXSLOTS (gram_slots_ok)
+    for (int q = tid; q < nsl * B2; q += kThreads + 32) {
+        const int si = q / B2, c = q % B2;
+        const int64_t slot = act ? act[slot0 + si] : slot0 + si;
+        int64_t I = iblk[slot], J = jblk[slot];
+        if (I > J) { int64_t t = I; I = J; J = t; }
+        S.cidx[si][c] = (int)rho[slot_pos(c, b, I, J)];
+    }
+    const unsigned full0 = (unsigned)__cvta_generic_to_shared(&S.full[0]);
+    const unsigned empty0 = (unsigned)__cvta_generic_to_shared(&S.empty[0]);
+    if (tid == 0) {
+        for (int st = 0; st < STAGES; ++st) {
+            mbar_init(full0 + 8 * st, 1);
+            mbar_init(empty0 + 8 * st, kThreads / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    const int T = (int)part.T, Lseg = (int)part.L;
+    const int nitems = (int)(it1 - it0);
+    const int kt0 = (int)(it0 - slot0 * part.T);
+    const unsigned x0 = (unsigned)__cvta_generic_to_shared(&S.x[0][0]);
+
+    if (warp == kThreads / 32) {
+        // ---- producer warp
+        int si = 0, k = kt0;
+        for (int i = 0; i < nitems; ++i) {
+            const int st = i % STAGES;
+            const unsigned ph = (unsigned)(i / STAGES) & 1u;
+            if (i >= STAGES) mbar_wait(empty0 + 8 * st, ph ^ 1u);
+            if (lane == 0) mbar_expect_tx(full0 + 8 * st, Sm::STAGE_BYTES);
+            __syncwarp();
+            constexpr int GROUPS = B2 / 4, OPS = Sm::SUB * GROUPS;
+#pragma unroll
+            for (int op = lane; op < OPS; op += 32) {
+                const int q = op / GROUPS, g = op % GROUPS;
+                const int *cc = &S.cidx[si][4 * g];
+                tma_gather4(x0 + st * Sm::STAGE_BYTES + q * (B2 * 128) + g * 512, &gmap,
+                            k * KT + q * 16, cc[0], cc[1], cc[2], cc[3], full0 + 8 * st);
+            }
+            if (++k == T) {
+                k = 0;
+                ++si;
+            }
+        }
+        return;
+    }
+
+    // ---- consumer warps: fragment offsets of this lane in a sub-tile
+    const int fr = lane >> 2, fk = lane & 3;
+    const int lp = (fk >> 1) ^ fr;
+    unsigned off[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) off[a] = (unsigned)((((2 * a) ^ lp) << 4) + (fk & 1) * 8 + fr * 128);
+    double acc[Roles::NACC][2];
+#pragma unroll
+    for (int q = 0; q < Roles::NACC; ++q) acc[q][0] = acc[q][1] = 0.0;
+    int c_si = 0, c_k = kt0;
+    for (int i = 0; i < nitems; ++i) {
+        const int st = i % STAGES;
+        const unsigned ph = (unsigned)(i / STAGES) & 1u;
+        mbar_wait(full0 + 8 * st, ph);
+        const unsigned char *xs = S.x[st];
+#pragma unroll
+        for (int kk = 0; kk < KT; kk += 4) {
+            const unsigned char *xq = xs + (kk >> 4) * (B2 * 128) + off[(kk >> 2) & 3];
+            Roles::mma(warp, [&](int R) { return *(const double *)(xq + R * 128); }, acc);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty0 + 8 * st);
+        const int seg = c_k / Lseg;
+        const bool seg_end = c_k == T - 1 || c_k + 1 == (seg + 1) * Lseg;
+        const int64_t slot = act ? act[slot0 + c_si] : slot0 + c_si;
+        if (++c_k == T) {
+            c_k = 0;
+            ++c_si;
+        }
+        if (seg_end) {
+            double *out = Apart + (slot * maxseg + seg) * (B2 * B2);
+#pragma unroll
+            for (int q = 0; q < Roles::NACC; ++q) {
+                int rt, ct;
+                Roles::tile(warp, q, rt, ct);
+                if (rt >= 0) {
+                    const int row = 8 * rt + fr, col = 8 * ct + 2 * fk;
+                    out[row * B2 + col] = acc[q][0];
+                    out[row * B2 + col + 1] = acc[q][1];
+                }
+                acc[q][0] = acc[q][1] = 0.0;
+            }
+        }
+    }
+}
+
+// The factor's storage as a 2D tensor for k_gram_tma: dim 0 = rows (n,
+// contiguous), dim 1 = storage columns (ld doubles apart); box 16 x 1 with
+// the 128-byte swizzle (gather4 takes 4 dim-1 coordinates per copy).
+// Rows >= n read as zero.  Returns 0 on success.
+int make_gram_tensor_map(CUtensorMap *tm, const double *G, int64_t ld, int64_t n, int64_t ncols);
 
 // ---------------------------------------------------------------------
 // k_inner: one pass of 2x2 rotations on the 2b x 2b pivot Gram
@@ -1044,7 +1239,8 @@ inline int num_sms()
     return sms;
 }
 
-constexpr int kGramKT = HSVD_GRAM_KT, kGramStages = HSVD_GRAM_STAGES, kGramOcc = HSVD_GRAM_OCC;
+constexpr int kGramKT = HSVD_GRAM_KT, kGramStages = HSVD_GRAM_STAGES,
+              kGramOcc = HSVD_GRAM_TMA ? HSVD_GRAM_TMA_OCC : HSVD_GRAM_OCC;
 
 // Target number of K segments per slot (a function of nothing but this
 // constant and n: see GramPart).  More segments balance the CTAs better
@@ -1104,6 +1300,9 @@ struct SlotWs {
     ReuseWs ru;
     uint8_t *skipf;
     int32_t *act, *nact;
+    // k_gram_tma: tensor map of the storage colmap indexes (NULL: cp.async
+    // k_gram)
+    const CUtensorMap *gmap;
 };
 
 // Carve the per-slot arrays for nslots slots of a problem with nb blocks
@@ -1133,6 +1332,7 @@ inline void carve_slots(Carve2 &c, int64_t n, int64_t nslots, int64_t nb, int b,
     t.skipf = c.take<uint8_t>(nslots);
     t.act = c.take<int32_t>(nslots);
     t.nact = c.take<int32_t>(4);
+    t.gmap = nullptr;
     t.ru.pairstamp = t.ru.pairskip = t.ru.blkmod = nullptr;
     t.ru.dsweep = nullptr;
     if (reuse) {
@@ -1164,7 +1364,9 @@ inline int inner_priority()
 template <int B2>
 struct BlockKernels {
     static constexpr int KT = kGramKT, STAGES = kGramStages, MT = 128;
+    static constexpr int TSTAGES = HSVD_GRAM_TMA_STAGES;
     static size_t gram_smem() { return sizeof(GramSmem<B2, KT, STAGES>); }
+    static size_t gram_tma_smem() { return sizeof(GramTmaSmem<B2, KT, TSTAGES>) + 1024; }
     static size_t inner_smem() { return sizeof(InnerSmem<B2>); }
     static size_t upd_smem() { return sizeof(UpdSmem<B2, MT>); }
     static int setup()
@@ -1172,6 +1374,9 @@ struct BlockKernels {
         HSVD_CUDA(cudaFuncSetAttribute(k_gram<B2, KT, STAGES>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)gram_smem()));
+        HSVD_CUDA(cudaFuncSetAttribute(k_gram_tma<B2, KT, TSTAGES>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)gram_tma_smem()));
         HSVD_CUDA(cudaFuncSetAttribute(k_inner<B2, true>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)inner_smem()));
@@ -1207,20 +1412,32 @@ struct BlockKernels {
             // Gram and inner pass are the critical path of a step: highest
             // priority (split mode runs a bulk update on another stream)
             cudaLaunchConfig_t lc = {};
-            lc.gridDim = dim3((unsigned)gp.P);
-            lc.blockDim = dim3(kThreads);
-            lc.dynamicSmemBytes = gram_smem();
-            lc.stream = s;
             cudaLaunchAttribute at[1];
             at[0].id = cudaLaunchAttributePriority;
             at[0].val.priority = inner_priority();
             lc.attrs = at;
             lc.numAttrs = 1;
-            HSVD_CUDA(cudaLaunchKernelEx(&lc, k_gram<B2, KT, STAGES>, G, ldg, n, w.colmap,
-                                         (const int64_t *)w.iblk, (const int64_t *)w.jblk, gp,
-                                         w.maxseg, w.Apart, (const unsigned long long *)w.err,
-                                         (const int32_t *)(plan ? w.act : nullptr),
-                                         (const int32_t *)w.nact));
+            lc.stream = s;
+            const int32_t *actp = plan ? w.act : nullptr;
+            if (w.gmap) {
+                lc.gridDim = dim3((unsigned)gp.P);
+                lc.blockDim = dim3(kThreads + 32);
+                lc.dynamicSmemBytes = gram_tma_smem();
+                HSVD_CUDA(cudaLaunchKernelEx(&lc, k_gram_tma<B2, KT, TSTAGES>, *w.gmap, n,
+                                             w.colmap, (const int64_t *)w.iblk,
+                                             (const int64_t *)w.jblk, gp, w.maxseg, w.Apart,
+                                             (const unsigned long long *)w.err, actp,
+                                             (const int32_t *)w.nact));
+            } else {
+                lc.gridDim = dim3((unsigned)gp.P);
+                lc.blockDim = dim3(kThreads);
+                lc.dynamicSmemBytes = gram_smem();
+                HSVD_CUDA(cudaLaunchKernelEx(&lc, k_gram<B2, KT, STAGES>, G, ldg, n, w.colmap,
+                                             (const int64_t *)w.iblk, (const int64_t *)w.jblk,
+                                             gp, w.maxseg, w.Apart,
+                                             (const unsigned long long *)w.err, actp,
+                                             (const int32_t *)w.nact));
+            }
         }
         T.end(s);
         HSVD_LAUNCH_CHECK("k_gram");

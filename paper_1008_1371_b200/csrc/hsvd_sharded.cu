@@ -469,6 +469,7 @@ struct Shard {
     cudaEvent_t ev = nullptr, t0 = nullptr, t1 = nullptr;
     const double *G = nullptr;  // the caller's full factor on this device
     ShardWs w;
+    alignas(64) CUtensorMap gmap;  // k_gram_tma's view of the shard's storage
     // split mode: half B's stream, the (high-priority) exchange stream and
     // their events: edge updates per half and step parity, exchange per
     // step parity, sweep fork / join, first-step stagger
@@ -1221,6 +1222,10 @@ static int sharded_drive_t(Comm *comm, int nshards, int nlocal, const int *shard
             set_error("sharded: workspace too small");
             return HSVD_ERR_ARG;
         }
+        const char *tma_env = getenv("HSVD_GRAM_TMA");
+        if (HSVD_GRAM_TMA && !(tma_env && tma_env[0] == '0') &&
+            make_gram_tensor_map(&x.gmap, x.w.Gs, n, n, pl.areas(x.g) * (B2 / 2)) == 0)
+            x.w.sl.gmap = x.w.half[0].gmap = x.w.half[1].gmap = &x.gmap;
     }
     return D.run(signs_host, U_out, V_out, cols_host, sigma_out, lam_out, res, tele);
 }

@@ -201,3 +201,26 @@ def test_block_allskip_reuse_is_exact(streams, monkeypatch):
         assert a.telemetry == b.telemetry
         for f in ("sigma", "lam", "U", "Vinv_t"):
             assert np.array_equal(getattr(a, f), getattr(b, f)), f
+
+
+@pytest.mark.parametrize("case", [
+    (1024, 1024, 512, 0, "gauss", 32),
+    (520, 512, 200, 2, "gauss", 32),     # n not a multiple of the k-tile
+    (1000, 1000, 500, 4, "gauss", 32),   # padded r, ragged n
+    (256, 256, 100, 3, "graded12", 16),
+], ids=lambda c: f"n{c[0]}r{c[1]}p{c[2]}{c[4]}b{c[5]}")
+def test_gram_tma_bit_identical_to_cp_async(case, monkeypatch):
+    """k_gram_tma (TMA gather4 + mbarrier ring) issues the cp.async
+    kernel's DMMA sequence on the same segments: the whole solve is bit for
+    bit the same (rows beyond n come in as TMA zero fill)."""
+    n, r, p, seed, kind, b = case
+    G = make_case_input(n, r, seed, kind)
+    J = H.SignatureVector.from_p(r, p)
+    cfg = H.SolverConfig(mode="block", block_cols=b)
+    monkeypatch.setenv("HSVD_GRAM_TMA", "0")
+    a = H.drive(G, J, cfg)
+    monkeypatch.setenv("HSVD_GRAM_TMA", "1")
+    t = H.drive(G, J, cfg)
+    assert (a.sweeps_used, a.rotations, a.skips) == (t.sweeps_used, t.rotations, t.skips)
+    for f in ("sigma", "lam", "U", "Vinv_t"):
+        assert np.array_equal(getattr(a, f), getattr(t, f)), f
