@@ -322,6 +322,7 @@ static int block_drive_t(double *G, int64_t n, int64_t r, int64_t ldg, double *V
     HSVD_CUDA(cudaMemsetAsync(w.sl.ru.pairskip, 0, sizeof(uint32_t) * nb * nb, s));
     HSVD_CUDA(cudaMemsetAsync(w.sl.ru.blkmod, 0, sizeof(uint32_t) * nb, s));
     HSVD_CUDA(cudaMemsetAsync(w.sl.ru.dsweep, 0, sizeof(int32_t), s));
+    HSVD_CUDA(cudaMemsetAsync(w.sl.ru.dstamp, 0, sizeof(uint32_t) * nb, s));
 
     KernelTimer T;
     // Split mode: the two slot halves run on two streams.  A block only

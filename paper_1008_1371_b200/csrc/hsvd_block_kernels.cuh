@@ -156,7 +156,17 @@ struct GramPart {
 struct ReuseWs {
     uint32_t *pairstamp, *pairskip, *blkmod;
     int32_t *dsweep;  // sweeps completed (device)
+    // Diagonal-block cache: dcache[K] (b x b) is block K's own Gram
+    // G_K^T G_K as folded by the visit at stamp dstamp[K].  While no event
+    // has changed block K since (blkmod[K] < dstamp[K]) the same segments
+    // would produce the same bits, so a visit whose two blocks are both
+    // cached computes only the cross block G_I^T G_J ("cross" class).
+    double *dcache;
+    uint32_t *dstamp;
 };
+
+// slot classes of a planned step (k_plan -> skipf)
+constexpr uint8_t kSlotFull = 0, kSlotReused = 1, kSlotCross = 2;
 
 __device__ __forceinline__ uint32_t reuse_stamp(const int32_t *dsweep, int64_t nb, int step)
 {
@@ -268,12 +278,47 @@ struct GramRoles<32> {
     }
 };
 
+// Cross-block roles (kSlotCross): only the b x b block G_I^T G_J (8x8 tile
+// rows 0..T-1, columns T..2T-1, T = b / 8).  B2 = 64: 16 tiles, two per
+// warp (one A fragment, two B fragments); B2 = 32: 4 tiles on warps 0-3.
+template <int B2>
+struct GramRolesX {
+    static constexpr int TT = B2 / 16;  // tiles per block side
+    __device__ static void tile(int warp, int q, int &rt, int &ct)
+    {
+        rt = ct = -1;
+        if (B2 == 64) {
+            if (q < 2) {
+                rt = warp >> 1;
+                ct = TT + 2 * (warp & 1) + q;
+            }
+        } else if (q == 0 && warp < 4) {
+            rt = warp >> 1;
+            ct = TT + (warp & 1);
+        }
+    }
+    template <class LD, int NACC>
+    __device__ static void mma(int warp, LD &&ld, double (&acc)[NACC][2])
+    {
+        if (B2 == 64) {
+            const double a = ld(8 * (warp >> 1));
+            const int c0 = TT + 2 * (warp & 1);
+            const double b0 = ld(8 * c0), b1 = ld(8 * (c0 + 1));
+            dmma(acc[0][0], acc[0][1], a, b0);
+            dmma(acc[1][0], acc[1][1], a, b1);
+        } else if (warp < 4) {
+            dmma(acc[0][0], acc[0][1], ld(8 * (warp >> 1)), ld(8 * (TT + (warp & 1))));
+        }
+    }
+};
+
 template <int B2, int KT, int STAGES>
 __global__ void __launch_bounds__(kThreads, HSVD_GRAM_OCC) k_gram(
     const double *__restrict__ G, int64_t ldg, int n, const int64_t *__restrict__ rho,
     const int64_t *__restrict__ iblk, const int64_t *__restrict__ jblk, GramPart part,
     int maxseg, double *__restrict__ Apart, const unsigned long long *err,
-    const int32_t *__restrict__ act, const int32_t *__restrict__ nact)
+    const int32_t *__restrict__ act, const int32_t *__restrict__ nact,
+    const uint8_t *__restrict__ skipf)
 {
     using Sm = GramSmem<B2, KT, STAGES>;
     using Roles = GramRoles<B2>;
@@ -361,14 +406,22 @@ __global__ void __launch_bounds__(kThreads, HSVD_GRAM_OCC) k_gram(
         st_l = st_l + 1 == STAGES ? 0 : st_l + 1;
         const auto X = S.x[st_c];
         st_c = st_c + 1 == STAGES ? 0 : st_c + 1;
+        const int64_t cslot = act ? act[slot0 + c_si] : slot0 + c_si;
+        const bool cross = act && skipf[cslot] == kSlotCross;
+        if (cross) {
 #pragma unroll
-        for (int kk = 0; kk < KT; kk += 4)
-            Roles::mma(warp, [&](int R) { return X[R + fr][kk + fk]; }, acc);
+            for (int kk = 0; kk < KT; kk += 4)
+                GramRolesX<B2>::mma(warp, [&](int R) { return X[R + fr][kk + fk]; }, acc);
+        } else {
+#pragma unroll
+            for (int kk = 0; kk < KT; kk += 4)
+                Roles::mma(warp, [&](int R) { return X[R + fr][kk + fk]; }, acc);
+        }
         // CTA runs start and end on segment boundaries, so every segment
         // is accumulated from zero by exactly one CTA
         const int seg = c_k / Lseg;
         const bool seg_end = c_k == T - 1 || c_k + 1 == (seg + 1) * Lseg;
-        const int64_t slot = act ? act[slot0 + c_si] : slot0 + c_si;
+        const int64_t slot = cslot;
         if (++c_k == T) {
             c_k = 0;
             ++c_si;
@@ -379,7 +432,8 @@ __global__ void __launch_bounds__(kThreads, HSVD_GRAM_OCC) k_gram(
 #pragma unroll
             for (int q = 0; q < Roles::NACC; ++q) {
                 int rt, ct;
-                Roles::tile(warp, q, rt, ct);
+                if (cross) GramRolesX<B2>::tile(warp, q, rt, ct);
+                else Roles::tile(warp, q, rt, ct);
                 if (rt >= 0) {
                     const int row = 8 * rt + fr, col = 8 * ct + 2 * fk;
                     out[row * B2 + col] = acc[q][0];
@@ -398,9 +452,9 @@ __global__ void __launch_bounds__(kThreads, HSVD_GRAM_OCC) k_gram(
 // ---------------------------------------------------------------------
 // A stage is KT rows of the CTA's B2 columns, stored as KT/16 sub-tiles of
 // B2 x 128 bytes (16 doubles of one column per 128-byte line) with the
-// 128-byte swizzle: the 16-byte chunk j of line c sits at chunk j ^ (c & 7),
-// so the 8 lines x 4 k of a DMMA fragment hit 16 distinct chunks (two
-// wavefronts, no conflict) without padding.  One producer warp issues the
+// 128-byte swizzle: the 16-byte chunk j of line L sits at chunk j ^ (L & 7).
+// Columns are interleaved within each 8-line atom (consumer comment) so a
+// DMMA fragment load is conflict-free without padding.  One producer warp issues the
 // gather4 copies (4 columns through rho x 16 rows each; 64 per stage at
 // b = 32) into a STAGES-deep ring of full/empty mbarriers; the 8 consumer
 // warps keep the cp.async kernel's DMMA roles and accumulation order.
@@ -419,7 +473,8 @@ __global__ void __launch_bounds__(kThreads + 32, HSVD_GRAM_TMA_OCC) k_gram_tma(
     const __grid_constant__ CUtensorMap gmap, int n, const int64_t *__restrict__ rho,
     const int64_t *__restrict__ iblk, const int64_t *__restrict__ jblk, GramPart part,
     int maxseg, double *__restrict__ Apart, const unsigned long long *err,
-    const int32_t *__restrict__ act, const int32_t *__restrict__ nact)
+    const int32_t *__restrict__ act, const int32_t *__restrict__ nact,
+    const uint8_t *__restrict__ skipf)
 {
     using Sm = GramTmaSmem<B2, KT, STAGES>;
     using Roles = GramRoles<B2>;
@@ -478,9 +533,12 @@ __global__ void __launch_bounds__(kThreads + 32, HSVD_GRAM_TMA_OCC) k_gram_tma(
 #pragma unroll
             for (int op = lane; op < OPS; op += 32) {
                 const int q = op / GROUPS, g = op % GROUPS;
-                const int *cc = &S.cidx[si][4 * g];
+                // lines 4h..4h+3 of the 8-line atom of columns 8a..8a+7 hold
+                // columns {0,4,1,5} (h = 0) / {2,6,3,7} (h = 1): line 2f + f/4
+                // for column f (see the consumer's offsets)
+                const int *cc = &S.cidx[si][8 * (g >> 1) + 2 * (g & 1)];
                 tma_gather4(x0 + st * Sm::STAGE_BYTES + q * (B2 * 128) + g * 512, &gmap,
-                            k * KT + q * 16, cc[0], cc[1], cc[2], cc[3], full0 + 8 * st);
+                            k * KT + q * 16, cc[0], cc[4], cc[1], cc[5], full0 + 8 * st);
             }
             if (++k == T) {
                 k = 0;
@@ -490,12 +548,17 @@ __global__ void __launch_bounds__(kThreads + 32, HSVD_GRAM_TMA_OCC) k_gram_tma(
         return;
     }
 
-    // ---- consumer warps: fragment offsets of this lane in a sub-tile
+    // ---- consumer warps: fragment offsets of this lane in a sub-tile.
+    // Fragment row f of an 8-row group sits on line p = 2 (f & 3) + (f >> 2)
+    // of its 1024-byte atom, so the 16 lanes of a half-warp (f = 0..3 or
+    // 4..7, two k-chunks each) read 8 distinct swizzled chunks x 2 halves:
+    // one wavefront per half-warp, no bank conflict.
     const int fr = lane >> 2, fk = lane & 3;
-    const int lp = (fk >> 1) ^ fr;
+    const int lp = 2 * (fr & 3) + (fr >> 2);
     unsigned off[4];
 #pragma unroll
-    for (int a = 0; a < 4; ++a) off[a] = (unsigned)((((2 * a) ^ lp) << 4) + (fk & 1) * 8 + fr * 128);
+    for (int a = 0; a < 4; ++a)
+        off[a] = (unsigned)(lp * 128 + ((((2 * a) | (fk >> 1)) ^ lp) << 4) + (fk & 1) * 8);
     double acc[Roles::NACC][2];
 #pragma unroll
     for (int q = 0; q < Roles::NACC; ++q) acc[q][0] = acc[q][1] = 0.0;
@@ -503,18 +566,28 @@ __global__ void __launch_bounds__(kThreads + 32, HSVD_GRAM_TMA_OCC) k_gram_tma(
     for (int i = 0; i < nitems; ++i) {
         const int st = i % STAGES;
         const unsigned ph = (unsigned)(i / STAGES) & 1u;
+        const int64_t slot = act ? act[slot0 + c_si] : slot0 + c_si;
+        const bool cross = act && skipf[slot] == kSlotCross;
         mbar_wait(full0 + 8 * st, ph);
         const unsigned char *xs = S.x[st];
+        if (cross) {
 #pragma unroll
-        for (int kk = 0; kk < KT; kk += 4) {
-            const unsigned char *xq = xs + (kk >> 4) * (B2 * 128) + off[(kk >> 2) & 3];
-            Roles::mma(warp, [&](int R) { return *(const double *)(xq + R * 128); }, acc);
+            for (int kk = 0; kk < KT; kk += 4) {
+                const unsigned char *xq = xs + (kk >> 4) * (B2 * 128) + off[(kk >> 2) & 3];
+                GramRolesX<B2>::mma(warp, [&](int R) { return *(const double *)(xq + R * 128); },
+                                    acc);
+            }
+        } else {
+#pragma unroll
+            for (int kk = 0; kk < KT; kk += 4) {
+                const unsigned char *xq = xs + (kk >> 4) * (B2 * 128) + off[(kk >> 2) & 3];
+                Roles::mma(warp, [&](int R) { return *(const double *)(xq + R * 128); }, acc);
+            }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(empty0 + 8 * st);
         const int seg = c_k / Lseg;
         const bool seg_end = c_k == T - 1 || c_k + 1 == (seg + 1) * Lseg;
-        const int64_t slot = act ? act[slot0 + c_si] : slot0 + c_si;
         if (++c_k == T) {
             c_k = 0;
             ++c_si;
@@ -524,7 +597,8 @@ __global__ void __launch_bounds__(kThreads + 32, HSVD_GRAM_TMA_OCC) k_gram_tma(
 #pragma unroll
             for (int q = 0; q < Roles::NACC; ++q) {
                 int rt, ct;
-                Roles::tile(warp, q, rt, ct);
+                if (cross) GramRolesX<B2>::tile(warp, q, rt, ct);
+                else Roles::tile(warp, q, rt, ct);
                 if (rt >= 0) {
                     const int row = 8 * rt + fr, col = 8 * ct + 2 * fk;
                     out[row * B2 + col] = acc[q][0];
@@ -721,6 +795,7 @@ static __global__ void __launch_bounds__(kPlanThreads) k_plan(const int64_t *__r
     for (int64_t s0 = 0; s0 < nslots; s0 += kPlanThreads) {
         const int64_t slot = s0 + tid;
         int sk = 0;
+        uint8_t cls = kSlotFull;
         if (slot < nslots && !failed) {
             int64_t I = iblk[slot], J = jblk[slot];
             if (I > J) { int64_t t = I; I = J; J = t; }
@@ -728,8 +803,13 @@ static __global__ void __launch_bounds__(kPlanThreads) k_plan(const int64_t *__r
             const uint32_t m = max(ru.blkmod[I], ru.blkmod[J]);
             const uint32_t at = ps & 0x7fffffffu;
             sk = ps != 0u && (int)(ps >> 31) >= (full != 0) && m < at && at < stamp;
+            if (!sk && ru.dcache) {
+                const uint32_t dI = ru.dstamp[I], dJ = ru.dstamp[J];
+                cls = dI != 0u && dJ != 0u && ru.blkmod[I] < dI && ru.blkmod[J] < dJ
+                          ? kSlotCross : kSlotFull;
+            }
         }
-        if (slot < nslots) skipf[slot] = (uint8_t)sk;
+        if (slot < nslots) skipf[slot] = sk ? kSlotReused : cls;
         const int live = slot < nslots && !sk;
         const unsigned bal = __ballot_sync(0xffffffffu, live);
         if (lane == 0) wcnt[warp] = __popc(bal);
@@ -777,7 +857,7 @@ __global__ void __launch_bounds__(inner_threads<B2>()) k_inner(InnerArgs a)
     const int slot = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     int64_t I = a.iblk[slot], J = a.jblk[slot];
     if (I > J) { int64_t t = I; I = J; J = t; }
-    if (a.skipf && a.skipf[slot]) {
+    if (a.skipf && a.skipf[slot] == kSlotReused) {
         // reused all-skip visit: the recorded statistics, no rotation, no
         // update (empty touched set), stepper advanced as usual
         if (tid == 0) {
@@ -800,6 +880,10 @@ __global__ void __launch_bounds__(inner_threads<B2>()) k_inner(InnerArgs a)
         S.W[i][j] = i == j ? 1.0 : 0.0;
     }
     {
+        // cross class: the two diagonal blocks come from the cache, only the
+        // cross block from the partials (the same segment folds as a fresh
+        // visit, so the same bits)
+        const bool cross = a.skipf && a.skipf[slot] == kSlotCross;
         double v[PER];
 #pragma unroll
         for (int k = 0; k < PER; ++k) v[k] = 0.0;
@@ -810,8 +894,8 @@ __global__ void __launch_bounds__(inner_threads<B2>()) k_inner(InnerArgs a)
             for (int u = 0; u < BATCH; ++u)
 #pragma unroll
                 for (int k = 0; k < PER; ++k) {
-                    const int e = tid + k * NT;
-                    x[u][k] = (s0 + u < nseg && e / B2 <= e % B2)
+                    const int e = tid + k * NT, i = e / B2, j = e % B2;
+                    x[u][k] = (s0 + u < nseg && i <= j && (!cross || (i < b && j >= b)))
                                   ? P0[(int64_t)(s0 + u) * B2 * B2 + e] : 0.0;
                 }
 #pragma unroll
@@ -820,10 +904,19 @@ __global__ void __launch_bounds__(inner_threads<B2>()) k_inner(InnerArgs a)
                 for (int k = 0; k < PER; ++k)
                     if (s0 + u < nseg) v[k] += x[u][k];
         }
+        const bool cache = a.ru.dcache != nullptr;
 #pragma unroll
         for (int k = 0; k < PER; ++k) {
             const int e = tid + k * NT, i = e / B2, j = e % B2;
             if (i <= j) {
+                const bool dI = j < b, dJ = i >= b;  // inside a diagonal block
+                if (cross && (dI || dJ)) {
+                    v[k] = dI ? a.ru.dcache[(I * b + i) * b + j]
+                              : a.ru.dcache[(J * b + (i - b)) * b + (j - b)];
+                } else if (cache && !cross && (dI || dJ)) {
+                    if (dI) a.ru.dcache[(I * b + i) * b + j] = v[k];
+                    else a.ru.dcache[(J * b + (i - b)) * b + (j - b)] = v[k];
+                }
                 S.A[i][j] = v[k];
                 S.A[j][i] = v[k];
             }
@@ -1068,6 +1161,11 @@ __global__ void __launch_bounds__(inner_threads<B2>()) k_inner(InnerArgs a)
         if (mt > a.maxt[slot]) a.maxt[slot] = mt;
         if (a.ru.pairstamp) {
             const uint32_t stamp = reuse_stamp(a.ru.dsweep, a.nb, a.step);
+            if (a.ru.dcache && !(a.skipf && a.skipf[slot] == kSlotCross)) {
+                // this visit folded both diagonal blocks fresh: cached as of now
+                a.ru.dstamp[I] = stamp;
+                a.ru.dstamp[J] = stamp;
+            }
             if (S.touched) {
                 // the blocks' columns are rewritten by this step's update
                 a.ru.blkmod[I] = stamp;
@@ -1335,11 +1433,15 @@ inline void carve_slots(Carve2 &c, int64_t n, int64_t nslots, int64_t nb, int b,
     t.gmap = nullptr;
     t.ru.pairstamp = t.ru.pairskip = t.ru.blkmod = nullptr;
     t.ru.dsweep = nullptr;
+    t.ru.dcache = nullptr;
+    t.ru.dstamp = nullptr;
     if (reuse) {
         t.ru.pairstamp = c.take<uint32_t>(nb * nb);
         t.ru.pairskip = c.take<uint32_t>(nb * nb);
         t.ru.blkmod = c.take<uint32_t>(nb);
         t.ru.dsweep = c.take<int32_t>(1);
+        t.ru.dcache = c.take<double>(nb * b * b);
+        t.ru.dstamp = c.take<uint32_t>(nb);
     }
     t.nslots = nslots;
     t.nb = nb;
@@ -1427,7 +1529,8 @@ struct BlockKernels {
                                              w.colmap, (const int64_t *)w.iblk,
                                              (const int64_t *)w.jblk, gp, w.maxseg, w.Apart,
                                              (const unsigned long long *)w.err, actp,
-                                             (const int32_t *)w.nact));
+                                             (const int32_t *)w.nact,
+                                             (const uint8_t *)w.skipf));
             } else {
                 lc.gridDim = dim3((unsigned)gp.P);
                 lc.blockDim = dim3(kThreads);
@@ -1436,7 +1539,8 @@ struct BlockKernels {
                                              (const int64_t *)w.iblk, (const int64_t *)w.jblk,
                                              gp, w.maxseg, w.Apart,
                                              (const unsigned long long *)w.err, actp,
-                                             (const int32_t *)w.nact));
+                                             (const int32_t *)w.nact,
+                                             (const uint8_t *)w.skipf));
             }
         }
         T.end(s);
