@@ -79,7 +79,8 @@ typedef CUresult (*TensorMapEncodeFn)(CUtensorMap *, CUtensorMapDataType, cuuint
                                       CUtensorMapSwizzle, CUtensorMapL2promotion,
                                       CUtensorMapFloatOOBfill);
 
-int make_gram_tensor_map(CUtensorMap *tm, const double *G, int64_t ld, int64_t n, int64_t ncols)
+int make_gram_tensor_map(CUtensorMap *tm, const double *G, int64_t ld, int64_t n, int64_t ncols,
+                         int box_cols)
 {
     static TensorMapEncodeFn enc = [] {
         void *fn = nullptr;
@@ -93,7 +94,7 @@ int make_gram_tensor_map(CUtensorMap *tm, const double *G, int64_t ld, int64_t n
     if (!enc || (ld * 8) % 16 || ((uintptr_t)G & 15)) return 1;
     const cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)ncols};
     const cuuint64_t strides[1] = {(cuuint64_t)ld * 8};
-    const cuuint32_t box[2] = {16, 1};
+    const cuuint32_t box[2] = {16, (cuuint32_t)box_cols};
     const cuuint32_t es[2] = {1, 1};
     const CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void *)G, dims, strides, box,
                            es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -110,6 +111,57 @@ int launch_block_norms(const double *G, int64_t ldg, int64_t n, const int64_t *r
 }
 
 // ---------------------------------------------------------------------
+// position-ordered storage (one GPU): column moves
+// ---------------------------------------------------------------------
+// The one-GPU driver keeps G and V^{-T} with storage column = POSITION of
+// the sorted package order, so block K is the contiguous columns
+// [K b, K b + b) and the Gram reads a block's k-tile as one TMA box.  After
+// each sort the columns move to their new positions: position q takes the
+// column of original index tgt[q], which sat at position inv_old[tgt[q]].
+// Two passes through a scratch buffer, touching only moved columns.
+
+__global__ void k_iota(int64_t *x, int64_t r)
+{
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k < r) x[k] = k;
+}
+
+__global__ void k_inverse(const int64_t *__restrict__ rho, int64_t *__restrict__ inv, int64_t r)
+{
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k < r) inv[rho[k]] = k;
+}
+
+// phase 0: S[:, q] = W[:, src(q)]; phase 1: W[:, q] = S[:, q] (moved q only)
+__global__ void k_move_cols(double *__restrict__ W, int64_t ldw, double *__restrict__ S,
+                            int64_t lds, int64_t rows, const int64_t *__restrict__ tgt,
+                            const int64_t *__restrict__ inv_old, int phase)
+{
+    const int64_t q = blockIdx.y;
+    const int64_t src = inv_old[tgt[q]];
+    if (src == q) return;
+    const double2 *from = (const double2 *)(phase ? S + q * lds : W + src * ldw);
+    double2 *to = (double2 *)(phase ? W + q * ldw : S + q * lds);
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < rows / 2;
+         e += (int64_t)gridDim.x * blockDim.x)
+        to[e] = from[e];
+    if ((rows & 1) && blockIdx.x == 0 && threadIdx.x == 0)
+        (phase ? W + q * ldw : S + q * lds)[rows - 1] = (phase ? S + q * lds : W + src * ldw)[rows - 1];
+}
+
+static int move_cols(double *W, int64_t ldw, double *S, int64_t lds, int64_t rows, int64_t r,
+                     const int64_t *tgt, const int64_t *inv_old, cudaStream_t s)
+{
+    unsigned gx = (unsigned)((rows / 2 + 255) / 256);
+    if (gx > 16) gx = 16;
+    for (int ph = 0; ph < 2; ++ph) {
+        k_move_cols<<<dim3(gx, (unsigned)r), 256, 0, s>>>(W, ldw, S, lds, rows, tgt, inv_old, ph);
+        HSVD_LAUNCH_CHECK("k_move_cols");
+    }
+    return HSVD_OK;
+}
+
+// ---------------------------------------------------------------------
 // one-GPU driver
 // ---------------------------------------------------------------------
 struct BlockWs {
@@ -120,6 +172,10 @@ struct BlockWs {
     int64_t *out;
     int8_t *signs;
     int64_t *rho_prev;  // rho before the sweep-end sort (all-skip reuse)
+    int64_t *ident;     // 0..r-1 (storage = position)
+    int64_t *inv;       // original column -> position (before a sort)
+    double *Gs, *Vs;    // scratch columns for the moves (ld lds / r)
+    int64_t lds;
     SlotWs sl;
     // split mode: the two half-slot views (shared arrays, own Gram partial
     // buffers and partitions)
@@ -143,7 +199,7 @@ static int64_t profile_sweep()
     return v;
 }
 
-static int64_t carve_block(Carve2 &c, int64_t n, int64_t r, int b, BlockWs *w)
+static int64_t carve_block(Carve2 &c, int64_t n, int64_t r, int b, BlockWs *w, bool withV = true)
 {
     const int64_t nb = r / b, nslots = nb / 2 > 0 ? nb / 2 : 1;
     BlockWs t;
@@ -155,8 +211,14 @@ static int64_t carve_block(Carve2 &c, int64_t n, int64_t r, int b, BlockWs *w)
     t.out = c.take<int64_t>(8);
     t.signs = c.take<int8_t>(r);
     t.rho_prev = c.take<int64_t>(r);
+    t.ident = c.take<int64_t>(r);
+    t.inv = c.take<int64_t>(r);
+    t.lds = n + (n & 1);
+    t.Gs = c.take<double>(t.lds * r);
+    t.Vs = withV ? c.take<double>(r * r) : nullptr;
     carve_slots(c, n, nslots, nb, b, &t.sl, true);
-    t.sl.colmap = t.rho;
+    t.sl.colmap = t.ident;  // storage column = position
+    t.sl.orig = t.rho;
     t.sl.js = t.js;
     const int64_t B2 = 2 * b;
     for (int h = 0; h < 2; ++h) {
@@ -227,7 +289,7 @@ int64_t block_workspace_size(int64_t n, int64_t r, const hsvd_config *cfg)
     int64_t pre = 0;
     if (pad_cols(r, b)) pre = carve_pad(c, n, r, b, cfg->accumulate_v != 0, nullptr);
     Carve2 c2{nullptr, 0};
-    return pre + carve_block(c2, n, r + pad_cols(r, b), b, nullptr);
+    return pre + carve_block(c2, n, r + pad_cols(r, b), b, nullptr, cfg->accumulate_v != 0);
 }
 
 int launch_reduce_sweep(uint8_t *C, int64_t m, uint32_t *rotk, uint32_t *skipk,
@@ -237,10 +299,12 @@ int launch_init_packages(const int8_t *signs, int64_t r, int64_t *rho,
                          int64_t *jsign, cudaStream_t s);
 int launch_identity(double *V, int64_t r, int64_t ldv, cudaStream_t s);
 
+// d[k] = ||G[:, map[k]]||^2 (map = the identity once storage is in
+// position order)
 static int block_norms(double *G, int64_t ldg, int64_t n, const BlockWs &w, int64_t r,
-                       unsigned long long *first_zero, cudaStream_t s)
+                       unsigned long long *first_zero, cudaStream_t s, const int64_t *map)
 {
-    k_block_norms<<<(unsigned)((r + 7) / 8), 256, 0, s>>>(G, ldg, (int)n, w.rho, r, w.d,
+    k_block_norms<<<(unsigned)((r + 7) / 8), 256, 0, s>>>(G, ldg, (int)n, map, r, w.d,
                                                           first_zero);
     HSVD_LAUNCH_CHECK("k_block_norms");
     return HSVD_OK;
@@ -259,7 +323,7 @@ static int block_drive_t(double *G, int64_t n, int64_t r, int64_t ldg, double *V
     const int64_t nb = r / b, nslots = nb / 2;
     Carve2 c{(char *)ws, 0};
     BlockWs w;
-    if (carve_block(c, n, r, b, &w) > ws_bytes) {
+    if (carve_block(c, n, r, b, &w, V != nullptr) > ws_bytes) {
         set_error("workspace too small");
         return HSVD_ERR_ARG;
     }
@@ -269,8 +333,10 @@ static int block_drive_t(double *G, int64_t n, int64_t r, int64_t ldg, double *V
     alignas(64) CUtensorMap gmap;
     const char *tma_env = getenv("HSVD_GRAM_TMA");
     if (HSVD_GRAM_TMA && !(tma_env && tma_env[0] == '0') &&
-        make_gram_tensor_map(&gmap, G, ldg, n, r) == 0)
+        make_gram_tensor_map(&gmap, G, ldg, n, r, b) == 0) {
         w.sl.gmap = w.half[0].gmap = w.half[1].gmap = &gmap;
+        w.sl.tile = w.half[0].tile = w.half[1].tile = true;
+    }
     int st = K::setup();
     if (st) return st;
 
@@ -295,8 +361,10 @@ static int block_drive_t(double *G, int64_t n, int64_t r, int64_t ldg, double *V
     HSVD_CUDA(cudaMemcpyAsync(w.signs, signs_host, (size_t)r, cudaMemcpyHostToDevice, s));
     st = launch_init_packages(w.signs, r, w.rho, w.js, s);
     if (st) return st;
+    k_iota<<<(unsigned)((r + 255) / 256), 256, 0, s>>>(w.ident, r);
+    HSVD_LAUNCH_CHECK("k_iota");
     HSVD_CUDA(cudaMemsetAsync(w.first_zero, 0xff, sizeof(unsigned long long), s));
-    st = block_norms(G, ldg, n, w, r, w.first_zero, s);
+    st = block_norms(G, ldg, n, w, r, w.first_zero, s, w.ident);
     if (st) return st;
     HSVD_CUDA(cudaMemcpyAsync(host, w.first_zero, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     HSVD_CUDA(cudaStreamSynchronize(s));
@@ -311,6 +379,10 @@ static int block_drive_t(double *G, int64_t n, int64_t r, int64_t ldg, double *V
         st = hsvd_sort_diagonal(w.d, w.rho, w.js, r, p, w.sortws, s);
         if (st) return st;
     }
+    // storage into position order (it is in original order: inv = identity)
+    st = move_cols(G, ldg, w.Gs, w.lds, n, r, w.rho, w.ident, s);
+    if (!st && V) st = move_cols(V, ldv, w.Vs, r, r, r, w.rho, w.ident, s);
+    if (st) return st;
     st = hsvd_stepper_init(w.sl.ip, w.sl.jp, w.sl.iblk, w.sl.jblk, nb, s);
     if (st) return st;
     HSVD_CUDA(cudaMemsetAsync(w.sl.C, 0, (size_t)nslots, s));
@@ -323,6 +395,7 @@ static int block_drive_t(double *G, int64_t n, int64_t r, int64_t ldg, double *V
     HSVD_CUDA(cudaMemsetAsync(w.sl.ru.blkmod, 0, sizeof(uint32_t) * nb, s));
     HSVD_CUDA(cudaMemsetAsync(w.sl.ru.dsweep, 0, sizeof(int32_t), s));
     HSVD_CUDA(cudaMemsetAsync(w.sl.ru.dstamp, 0, sizeof(uint32_t) * nb, s));
+    HSVD_CUDA(cudaMemsetAsync(w.sl.ru.planstat, 0, sizeof(unsigned long long) * 4, s));
 
     KernelTimer T;
     // Split mode: the two slot halves run on two streams.  A block only
@@ -425,7 +498,7 @@ static int block_drive_t(double *G, int64_t n, int64_t r, int64_t ldg, double *V
             }
         }
         T.begin(3, s);
-        int e = block_norms(G, ldg, n, w, r, nullptr, s);
+        int e = block_norms(G, ldg, n, w, r, nullptr, s, w.ident);
         if (e) return e;
         e = launch_reduce_sweep(w.sl.C, nslots, w.sl.rotk, w.sl.skipk, w.sl.maxt, nslots, w.out,
                                 w.sl.err, 1, s);
@@ -438,6 +511,12 @@ static int block_drive_t(double *G, int64_t n, int64_t r, int64_t ldg, double *V
             k_reuse_sweep_end<<<(unsigned)((r + 255) / 256), 256, 0, s>>>(w.rho, w.rho_prev, r, b,
                                                                          nb, w.sl.ru);
             HSVD_LAUNCH_CHECK("k_reuse_sweep_end");
+            // the columns follow their packages to the new positions
+            k_inverse<<<(unsigned)((r + 255) / 256), 256, 0, s>>>(w.rho_prev, w.inv, r);
+            HSVD_LAUNCH_CHECK("k_inverse");
+            e = move_cols(G, ldg, w.Gs, w.lds, n, r, w.rho, w.inv, s);
+            if (!e && V) e = move_cols(V, ldv, w.Vs, r, r, r, w.rho, w.inv, s);
+            if (e) return e;
         }
         k_reuse_next_sweep<<<1, 1, 0, s>>>(w.sl.ru.dsweep);
         HSVD_LAUNCH_CHECK("k_reuse_next_sweep");
@@ -451,9 +530,15 @@ static int block_drive_t(double *G, int64_t n, int64_t r, int64_t ldg, double *V
     // rotates few pairs (most updates are skipped and launch overhead
     // dominates) the remaining sweeps run as one-stream graph replays.
     const bool graphs = cfg->use_graph && !cfg->profile && !tl_on;
+    // the late-sweep graph keeps the two-half schedule (one half's inner pass
+    // beside the other half's Gram) unless HSVD_LATE_SPLIT=0
+    const bool late_split = split && [] {
+        const char *e = getenv("HSVD_LATE_SPLIT");
+        return !(e && e[0] == '0');
+    }();
     auto capture = [&]() -> int {
         const bool keep = split_now;
-        split_now = false;
+        split_now = late_split;
         plan_now = reuse_ok;
         HSVD_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
         int e = enqueue_sweep();
@@ -469,15 +554,22 @@ static int block_drive_t(double *G, int64_t n, int64_t r, int64_t ldg, double *V
         st = capture();
         if (st) return st;
     }
-    int64_t launches = (V ? 1 : 0) + 1 + 1 + (cfg->sort ? 2 : 0) + 1 + 2;
+    const int64_t mv = V ? 4 : 2;  // k_move_cols launches per column move
+    int64_t launches = (V ? 1 : 0) + 1 + 1 + 1 + (cfg->sort ? 2 : 0) + 1 + 2 + mv + 1 + mv;
     int64_t sweeps_used = 0, total_rot = 0, total_skip = 0;
     int stop = 2;
     const double t_loop0 = wall_ms();
     res->setup_ms = t_loop0;  // absolute for now; hsvd_drive makes it relative
     for (int64_t sweep = 0; sweep < cfg->max_sweeps; ++sweep) {
         HSVD_CUDA(cudaEventRecord(t0, s));
-        launches += (split_now ? 8 : (reuse_ok && graphs ? 4 : 3)) * nb + 1 + 1 +
-                    (cfg->sort ? 3 : 0) + 1;
+        {
+            // kernels per step: split = 2 x (gram, inner, 3 updates), one
+            // stream = gram, inner, update; graphed sweeps add k_plan per launch
+            const bool graphed = graphs && !split_now;
+            const int64_t per_step = (split_now || (graphed && late_split)) ? 10 : 3;
+            const int64_t plans = graphed && reuse_ok ? (late_split ? 2 : 1) : 0;
+            launches += (per_step + plans) * nb + 1 + 1 + (cfg->sort ? 4 + mv : 0) + 1;
+        }
         if (split_now || !graphs) {
             T.on = cfg->profile && sweep == profile_sweep();
             st = enqueue_sweep();
@@ -537,7 +629,19 @@ static int block_drive_t(double *G, int64_t n, int64_t r, int64_t ldg, double *V
         if (code == 1) { stop = 1; break; }
     }
     res->sweeps_ms = wall_ms() - t_loop0;
-    // d was refreshed from G at the end of the last sweep (then sorted)
+    if (getenv("HSVD_PLAN_STATS")) {
+        unsigned long long ps[3] = {0, 0, 0};
+        cudaMemcpy(ps, w.sl.ru.planstat, sizeof(ps), cudaMemcpyDeviceToHost);
+        fprintf(stderr, "plan stats: full %llu reused %llu cross %llu (planned slot visits)\n",
+                ps[0], ps[1], ps[2]);
+    }
+    // storage back to the original column order, then the extraction
+    // (d was refreshed from G at the end of the last sweep, then sorted)
+    k_inverse<<<(unsigned)((r + 255) / 256), 256, 0, s>>>(w.rho, w.inv, r);
+    HSVD_LAUNCH_CHECK("k_inverse");
+    st = move_cols(G, ldg, w.Gs, w.lds, n, r, w.ident, w.inv, s);
+    if (!st && V) st = move_cols(V, ldv, w.Vs, r, r, r, w.ident, w.inv, s);
+    if (st) return st;
     st = hsvd_extract(G, n, ldg, w.d, w.rho, w.js, r, sigma, lam, s);
     if (st) return st;
     res->sweeps_used = sweeps_used;

@@ -24,6 +24,9 @@
 #ifndef HSVD_GRAM_TMA
 #define HSVD_GRAM_TMA 1
 #endif
+#ifndef HSVD_GRAM_TMA_GMAJOR
+#define HSVD_GRAM_TMA_GMAJOR 1
+#endif
 #ifndef HSVD_GRAM_TMA_STAGES
 #define HSVD_GRAM_TMA_STAGES 3
 #define HSVD_GRAM_TMA_OCC 2
@@ -163,6 +166,7 @@ struct ReuseWs {
     // cached computes only the cross block G_I^T G_J ("cross" class).
     double *dcache;
     uint32_t *dstamp;
+    unsigned long long *planstat;  // [full, reused, cross] slot counts of planned steps
 };
 
 // slot classes of a planned step (k_plan -> skipf)
@@ -468,7 +472,10 @@ struct GramTmaSmem {
     int cidx[MAXSLOTS][B2];
 };
 
-template <int B2, int KT, int STAGES>
+// fragment row f of an 8-row group <-> line p(f) of the 8-line swizzle atom
+__host__ __device__ constexpr int frag_line(int f) { return 2 * (f & 3) + (f >> 2); }
+
+template <int B2, int KT, int STAGES, bool TILE>
 __global__ void __launch_bounds__(kThreads + 32, HSVD_GRAM_TMA_OCC) k_gram_tma(
     const __grid_constant__ CUtensorMap gmap, int n, const int64_t *__restrict__ rho,
     const int64_t *__restrict__ iblk, const int64_t *__restrict__ jblk, GramPart part,
@@ -529,10 +536,35 @@ __global__ void __launch_bounds__(kThreads + 32, HSVD_GRAM_TMA_OCC) k_gram_tma(
             if (i >= STAGES) mbar_wait(empty0 + 8 * st, ph ^ 1u);
             if (lane == 0) mbar_expect_tx(full0 + 8 * st, Sm::STAGE_BYTES);
             __syncwarp();
+            if (TILE) {
+                // position-ordered storage: block I (J) of the slot is the
+                // box {16 rows, b columns} at column I*b (J*b): 2 x SUB boxes
+                if (lane < 2 * Sm::SUB) {
+                    const int q = lane % Sm::SUB, h = lane / Sm::SUB;
+                    const int col0 = S.cidx[si][h * b];
+                    const unsigned dst = x0 + st * Sm::STAGE_BYTES + q * (B2 * 128) + h * (b * 128);
+                    asm volatile(
+                        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                        " [%0], [%1, {%2, %3}], [%4];\n" ::"r"(dst),
+                        "l"(&gmap), "r"(k * KT + q * 16), "r"(col0), "r"(full0 + 8 * st)
+                        : "memory");
+                }
+                if (++k == T) {
+                    k = 0;
+                    ++si;
+                }
+                continue;
+            }
             constexpr int GROUPS = B2 / 4, OPS = Sm::SUB * GROUPS;
 #pragma unroll
             for (int op = lane; op < OPS; op += 32) {
+#if HSVD_GRAM_TMA_GMAJOR
+                // consecutive ops walk one column group's k sub-tiles: each
+                // column's KT*8 contiguous bytes are requested together
+                const int g = op / Sm::SUB, q = op % Sm::SUB;
+#else
                 const int q = op / GROUPS, g = op % GROUPS;
+#endif
                 // lines 4h..4h+3 of the 8-line atom of columns 8a..8a+7 hold
                 // columns {0,4,1,5} (h = 0) / {2,6,3,7} (h = 1): line 2f + f/4
                 // for column f (see the consumer's offsets)
@@ -600,9 +632,17 @@ __global__ void __launch_bounds__(kThreads + 32, HSVD_GRAM_TMA_OCC) k_gram_tma(
                 if (cross) GramRolesX<B2>::tile(warp, q, rt, ct);
                 else Roles::tile(warp, q, rt, ct);
                 if (rt >= 0) {
-                    const int row = 8 * rt + fr, col = 8 * ct + 2 * fk;
-                    out[row * B2 + col] = acc[q][0];
-                    out[row * B2 + col + 1] = acc[q][1];
+                    if (TILE) {
+                        // fragment row f read column 8t + p(f) (natural
+                        // line order in shared memory)
+                        const int row = 8 * rt + frag_line(fr);
+                        out[row * B2 + 8 * ct + frag_line(2 * fk)] = acc[q][0];
+                        out[row * B2 + 8 * ct + frag_line(2 * fk + 1)] = acc[q][1];
+                    } else {
+                        const int row = 8 * rt + fr, col = 8 * ct + 2 * fk;
+                        out[row * B2 + col] = acc[q][0];
+                        out[row * B2 + col + 1] = acc[q][1];
+                    }
                 }
                 acc[q][0] = acc[q][1] = 0.0;
             }
@@ -614,7 +654,8 @@ __global__ void __launch_bounds__(kThreads + 32, HSVD_GRAM_TMA_OCC) k_gram_tma(
 // contiguous), dim 1 = storage columns (ld doubles apart); box 16 x 1 with
 // the 128-byte swizzle (gather4 takes 4 dim-1 coordinates per copy).
 // Rows >= n read as zero.  Returns 0 on success.
-int make_gram_tensor_map(CUtensorMap *tm, const double *G, int64_t ld, int64_t n, int64_t ncols);
+int make_gram_tensor_map(CUtensorMap *tm, const double *G, int64_t ld, int64_t n, int64_t ncols,
+                         int box_cols = 1);
 
 // ---------------------------------------------------------------------
 // k_inner: one pass of 2x2 rotations on the 2b x 2b pivot Gram
@@ -630,6 +671,7 @@ struct InnerArgs {
     uint32_t *rotk, *skipk;
     uint8_t *tset;  // per slot: [count, touched columns...], kTsetStride bytes
     const int64_t *colmap;  // position -> storage column
+    const int64_t *orig;    // position -> original column (padding test)
     int64_t *colidx;        // per slot: storage column of each of its 2b columns
     double *maxt;
     unsigned long long *err;
@@ -809,7 +851,11 @@ static __global__ void __launch_bounds__(kPlanThreads) k_plan(const int64_t *__r
                           ? kSlotCross : kSlotFull;
             }
         }
-        if (slot < nslots) skipf[slot] = sk ? kSlotReused : cls;
+        if (slot < nslots) {
+            const uint8_t c = sk ? kSlotReused : cls;
+            skipf[slot] = c;
+            atomicAdd(&ru.planstat[c], 1ull);
+        }
         const int live = slot < nslots && !sk;
         const unsigned bal = __ballot_sync(0xffffffffu, live);
         if (lane == 0) wcnt[warp] = __popc(bal);
@@ -925,7 +971,7 @@ __global__ void __launch_bounds__(inner_threads<B2>()) k_inner(InnerArgs a)
     if (tid < B2) {
         const int64_t pos = slot_pos(tid, b, I, J);
         const int neg = a.jsign[pos] < 0;
-        const int pad = a.colmap[pos] >= a.real_cols;
+        const int pad = a.orig[pos] >= a.real_cols;
         S.js[tid] = neg ? -1 : 1;
         const unsigned mneg = __ballot_sync(0xffffffffu, neg);
         const unsigned mpad = __ballot_sync(0xffffffffu, pad);
@@ -1382,6 +1428,7 @@ inline bool gram_slots_ok(const GramPart &g)
 // sharded); js maps a position to its J sign.
 struct SlotWs {
     const int64_t *colmap, *js;
+    const int64_t *orig;  // position -> original column (NULL: colmap)
     int64_t *ip, *jp, *iblk, *jblk, *cur;
     uint8_t *C, *tset;
     uint32_t *rotk, *skipk;
@@ -1399,8 +1446,11 @@ struct SlotWs {
     uint8_t *skipf;
     int32_t *act, *nact;
     // k_gram_tma: tensor map of the storage colmap indexes (NULL: cp.async
-    // k_gram)
+    // k_gram); tile: the storage is in position order (block K = columns
+    // [K b, K b + b)), so a block's k-tile is one TMA box instead of
+    // gather4 copies through colmap
     const CUtensorMap *gmap;
+    bool tile;
 };
 
 // Carve the per-slot arrays for nslots slots of a problem with nb blocks
@@ -1412,7 +1462,8 @@ inline void carve_slots(Carve2 &c, int64_t n, int64_t nslots, int64_t nb, int b,
     const GramPart gp = gram_partition(n, nslots);
     const int ks = gram_maxseg(gp, nslots);
     SlotWs t;
-    t.colmap = t.js = nullptr;
+    t.colmap = t.js = t.orig = nullptr;
+    t.tile = false;
     t.ip = c.take<int64_t>(nslots);
     t.jp = c.take<int64_t>(nslots);
     t.iblk = c.take<int64_t>(nslots);
@@ -1435,6 +1486,7 @@ inline void carve_slots(Carve2 &c, int64_t n, int64_t nslots, int64_t nb, int b,
     t.ru.dsweep = nullptr;
     t.ru.dcache = nullptr;
     t.ru.dstamp = nullptr;
+    t.ru.planstat = nullptr;
     if (reuse) {
         t.ru.pairstamp = c.take<uint32_t>(nb * nb);
         t.ru.pairskip = c.take<uint32_t>(nb * nb);
@@ -1442,6 +1494,7 @@ inline void carve_slots(Carve2 &c, int64_t n, int64_t nslots, int64_t nb, int b,
         t.ru.dsweep = c.take<int32_t>(1);
         t.ru.dcache = c.take<double>(nb * b * b);
         t.ru.dstamp = c.take<uint32_t>(nb);
+        t.ru.planstat = c.take<unsigned long long>(4);
     }
     t.nslots = nslots;
     t.nb = nb;
@@ -1476,7 +1529,10 @@ struct BlockKernels {
         HSVD_CUDA(cudaFuncSetAttribute(k_gram<B2, KT, STAGES>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)gram_smem()));
-        HSVD_CUDA(cudaFuncSetAttribute(k_gram_tma<B2, KT, TSTAGES>,
+        HSVD_CUDA(cudaFuncSetAttribute(k_gram_tma<B2, KT, TSTAGES, false>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)gram_tma_smem()));
+        HSVD_CUDA(cudaFuncSetAttribute(k_gram_tma<B2, KT, TSTAGES, true>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)gram_tma_smem()));
         HSVD_CUDA(cudaFuncSetAttribute(k_inner<B2, true>,
@@ -1525,12 +1581,21 @@ struct BlockKernels {
                 lc.gridDim = dim3((unsigned)gp.P);
                 lc.blockDim = dim3(kThreads + 32);
                 lc.dynamicSmemBytes = gram_tma_smem();
-                HSVD_CUDA(cudaLaunchKernelEx(&lc, k_gram_tma<B2, KT, TSTAGES>, *w.gmap, n,
-                                             w.colmap, (const int64_t *)w.iblk,
-                                             (const int64_t *)w.jblk, gp, w.maxseg, w.Apart,
-                                             (const unsigned long long *)w.err, actp,
-                                             (const int32_t *)w.nact,
-                                             (const uint8_t *)w.skipf));
+                if (w.tile) {
+                    HSVD_CUDA(cudaLaunchKernelEx(&lc, k_gram_tma<B2, KT, TSTAGES, true>, *w.gmap,
+                                                 n, w.colmap, (const int64_t *)w.iblk,
+                                                 (const int64_t *)w.jblk, gp, w.maxseg, w.Apart,
+                                                 (const unsigned long long *)w.err, actp,
+                                                 (const int32_t *)w.nact,
+                                                 (const uint8_t *)w.skipf));
+                } else {
+                    HSVD_CUDA(cudaLaunchKernelEx(&lc, k_gram_tma<B2, KT, TSTAGES, false>, *w.gmap,
+                                                 n, w.colmap, (const int64_t *)w.iblk,
+                                                 (const int64_t *)w.jblk, gp, w.maxseg, w.Apart,
+                                                 (const unsigned long long *)w.err, actp,
+                                                 (const int32_t *)w.nact,
+                                                 (const uint8_t *)w.skipf));
+                }
             } else {
                 lc.gridDim = dim3((unsigned)gp.P);
                 lc.blockDim = dim3(kThreads);
@@ -1549,7 +1614,7 @@ struct BlockKernels {
         ia.part = gp; ia.maxseg = w.maxseg;
         ia.Apart = w.Apart; ia.Wg = w.Wg; ia.jsign = w.js;
         ia.ip = w.ip; ia.jp = w.jp; ia.iblk = w.iblk; ia.jblk = w.jblk; ia.cur = w.cur;
-        ia.C = w.C; ia.tset = w.tset; ia.colmap = w.colmap; ia.colidx = w.colidx; ia.rotk = w.rotk; ia.skipk = w.skipk; ia.maxt = w.maxt; ia.err = w.err;
+        ia.C = w.C; ia.tset = w.tset; ia.colmap = w.colmap; ia.orig = w.orig ? w.orig : w.colmap; ia.colidx = w.colidx; ia.rotk = w.rotk; ia.skipk = w.skipk; ia.maxt = w.maxt; ia.err = w.err;
         ia.nb = w.nb; ia.slot_base = w.slot_base; ia.real_cols = w.real_cols; ia.eps = cfg->eps; ia.teps = cfg->teps;
         ia.full = full; ia.use_skip = cfg->use_skip;
         ia.passes = cfg->inner_passes > 1 ? cfg->inner_passes : 1;
