@@ -492,8 +492,10 @@ static int block_drive_t(double *G, int64_t n, int64_t r, int64_t ldg, double *V
         } else {
             for (int64_t step = 0; step < nb; ++step) {
                 const int full = cfg->inner_full || step == 0;
+                // profile mode plans its eager steps too, so the profiled
+                // sweep sees the Gram classes of a graphed sweep
                 int e = K::step(G, ldg, (int)n, V, ldv, (int)r, w.sl, full, cfg, s, T, (int)step,
-                                plan_now);
+                                plan_now || (cfg->profile && reuse_ok));
                 if (e) return e;
             }
         }

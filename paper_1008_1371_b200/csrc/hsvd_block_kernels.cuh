@@ -24,6 +24,12 @@
 #ifndef HSVD_GRAM_TMA
 #define HSVD_GRAM_TMA 1
 #endif
+#ifndef HSVD_GRAM_NOMATH
+#define HSVD_GRAM_NOMATH 0  // diagnostics only (wrong results)
+#endif
+#ifndef HSVD_GRAM_NOLOAD
+#define HSVD_GRAM_NOLOAD 0
+#endif
 #ifndef HSVD_GRAM_TMA_GMAJOR
 #define HSVD_GRAM_TMA_GMAJOR 1
 #endif
@@ -534,6 +540,15 @@ __global__ void __launch_bounds__(kThreads + 32, HSVD_GRAM_TMA_OCC) k_gram_tma(
             const int st = i % STAGES;
             const unsigned ph = (unsigned)(i / STAGES) & 1u;
             if (i >= STAGES) mbar_wait(empty0 + 8 * st, ph ^ 1u);
+#if HSVD_GRAM_NOLOAD
+            // diagnostic: no operand traffic (the stage is released at once)
+            if (lane == 0) mbar_arrive(full0 + 8 * st);
+            if (++k == T) {
+                k = 0;
+                ++si;
+            }
+            continue;
+#endif
             if (lane == 0) mbar_expect_tx(full0 + 8 * st, Sm::STAGE_BYTES);
             __syncwarp();
             if (TILE) {
@@ -602,7 +617,9 @@ __global__ void __launch_bounds__(kThreads + 32, HSVD_GRAM_TMA_OCC) k_gram_tma(
         const bool cross = act && skipf[slot] == kSlotCross;
         mbar_wait(full0 + 8 * st, ph);
         const unsigned char *xs = S.x[st];
-        if (cross) {
+        if (HSVD_GRAM_NOMATH) {
+            // diagnostic: no DMMA (data movement floor)
+        } else if (cross) {
 #pragma unroll
             for (int kk = 0; kk < KT; kk += 4) {
                 const unsigned char *xq = xs + (kk >> 4) * (B2 * 128) + off[(kk >> 2) & 3];

@@ -15,12 +15,19 @@ from paper_1008_1371_b200 import _build  # noqa: E402
 BASE = list(_build.COMMON)
 args = sys.argv[1:]
 extra_bench = os.environ.get("BENCH_ARGS", "").split()
+script = os.environ.get("AB_SCRIPT")  # run this script instead of bench.py (prints its last line)
 for spec in args + ["default:"]:
     name, _, flags = spec.partition(":")
     _build.COMMON[:] = BASE + flags.split()
     _build.build(force=True)
     if name == "default":
         break
+    if script:
+        out = subprocess.run([sys.executable, *script.split()], capture_output=True, text=True,
+                             timeout=600)
+        print(f"{name:10s} {flags:40s} {out.stdout.strip().splitlines()[-1] if out.stdout.strip() else out.stderr[-500:]}",
+              flush=True)
+        continue
     out = subprocess.run([sys.executable, "bench.py", "--steps", "2", "--warmup", "1", "--no-cpu",
                           "--no-accuracy", *extra_bench], capture_output=True, text=True, timeout=600)
     try:
