@@ -236,22 +236,31 @@ def save_reference_telemetry(n, p, telemetry):
 
 def cpu_reference_estimate(G, signs, p, budget_s, threads, telemetry):
     """Time the reference algorithm (C restatement, oracle/) on the host:
-    sample A = the first modulus steps of sweep 0 on G (nearly all pairs
-    rotate), sample B = the same steps on an orthogonal factor (I, every
-    pair skips).  Per-visit costs c_rot, c_skip then price the exact
-    per-sweep rotation/skip counts of the full solve."""
+    sample A = modulus steps of sweep 0 on G (nearly all pairs rotate),
+    sample B = the same steps on an orthogonal factor (I, every pair skips).
+    Each sample is timed at N and 2N steps and the MARGINAL cost of the
+    second N steps is used (the first steps pay cold caches and page
+    faults: 141 ms per step for 10 steps vs 53 ms marginal at 20->40 on the
+    build host).  Per-visit costs c_rot, c_skip then price the exact
+    rotation/skip counts of the full solve.  Validated against a full run on
+    the build host (profiles/r02_cpu_estimate_validation.json)."""
     from oracle import oracle as O
     n, r = G.shape
     half = r // 2
-    # calibrate the step count to the budget
-    _, t1 = O.sample_steps(G, signs, p, 2, threads)
-    per_step = max(t1 / 2, 1e-4)
-    steps_a = int(max(2, min(r, 0.7 * budget_s / per_step)))
-    rot_a, ta = O.sample_steps(G, signs, p, steps_a, threads)
+
+    def marginal(M, frac):
+        # warm marginal step cost from 4 -> 8 steps sizes the sample
+        _, t4 = O.sample_steps(M, signs, p, 4, threads)
+        _, t8 = O.sample_steps(M, signs, p, 8, threads)
+        per = max((t8 - t4) / 4, t8 / 24, 1e-4)  # the 4->8 difference is noisy
+        N = int(max(16, min(512, r // 2, frac * budget_s / (3 * per))))
+        rot1, ta = O.sample_steps(M, signs, p, N, threads)
+        rot2, tb = O.sample_steps(M, signs, p, 2 * N, threads)
+        return N, rot2 - rot1, max(tb - ta, 1e-9), ta + tb
+
+    steps_a, rot_a, ta, wa = marginal(G, 0.7)
     Id = np.asfortranarray(np.eye(n, r))
-    _, t1b = O.sample_steps(Id, signs, p, 2, threads)
-    steps_b = int(max(2, min(r, 0.3 * budget_s / max(t1b / 2, 1e-4))))
-    _, tb = O.sample_steps(Id, signs, p, steps_b, threads)
+    steps_b, _, tb, wb = marginal(Id, 0.3)
     c_skip = tb / (steps_b * half)
     skip_a = steps_a * half - rot_a
     c_rot = max((ta - skip_a * c_skip) / max(rot_a, 1), c_skip)
@@ -267,8 +276,9 @@ def cpu_reference_estimate(G, signs, p, budget_s, threads, telemetry):
         how = "assumed 14 sweeps, every visit rotating (upper bound)"
     est = rot * c_rot + skip * c_skip
     sample = (f"EXTRAPOLATED: oracle C restatement (bit-exact with hjsvd), {threads} threads: "
-              f"{steps_a} steps of sweep 0 on G ({ta:.1f} s) + {steps_b} all-skip steps "
-              f"on I ({tb:.1f} s) -> c_rot={c_rot*1e6:.2f} us, c_skip={c_skip*1e6:.2f} us "
+              f"marginal cost of steps {steps_a}..{2 * steps_a} of sweep 0 on G and "
+              f"{steps_b}..{2 * steps_b} all-skip steps on I ({wa + wb:.1f} s sampled) -> "
+              f"c_rot={c_rot*1e6:.2f} us, c_skip={c_skip*1e6:.2f} us "
               f"per pair visit; extrapolated with {how}: {rot} rotations + {skip} skips "
               f"over {sweeps} sweeps")
     return est, sample
