@@ -268,7 +268,10 @@ HSVD_API int hsvd_drive_sharded(void *comm, int32_t nshards, int32_t nlocal,
  * hsvd_bp_workspace_size bytes (4 n^2 doubles + O(n)). */
 HSVD_API int hsvd_bp_workspace_size(int64_t n, size_t *bytes);
 /* the same on an unrounded double-double M = (M, Mlo) (generate_factor_pair,
- * factory.py:285-297, factorizes the generator's M before rounding) */
+ * factory.py:285-297, factorizes the generator's M before rounding).
+ * thresh < 0: the reference's n * eps * ||M||_F, computed from M on the
+ * device (G's storage is the scratch; it is written by the factorization
+ * afterwards). */
 HSVD_API int hsvd_bp_factor_dd(const double *M, const double *Mlo, int64_t n, int64_t ldm,
                                double thresh, double *G, int64_t ldg, int8_t *signs,
                                int64_t *perm, int64_t *p_out, int64_t *stage_out, void *ws,

@@ -49,7 +49,10 @@ def colmajor_to_device(G, dev):
     chunk k-1 at link rate (a pageable copy runs at a fraction of it)."""
     src = np.asarray(G, dtype=np.float64).T  # (r, n): C-contiguous for F-order G
     if src.nbytes < _STAGE_MIN or not src.flags.c_contiguous:
-        return torch.from_numpy(np.ascontiguousarray(src)).to(dev, non_blocking=False)
+        host = np.ascontiguousarray(src)
+        if not host.flags.writeable:  # torch.from_numpy wants a writable array
+            host = host.copy()
+        return torch.from_numpy(host).to(dev, non_blocking=False)
     out = torch.empty(src.shape, dtype=torch.float64, device=dev)
     host = torch.empty(src.shape, dtype=torch.float64, pin_memory=True)
     hv = host.numpy()

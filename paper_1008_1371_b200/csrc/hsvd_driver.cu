@@ -127,6 +127,7 @@ DevCtx *dev_ctx(int dev, int *status)
     if (e == cudaSuccess) e = cudaEventCreate(&c->t1);
     if (e == cudaSuccess) e = cudaHostAlloc((void **)&c->host, 64 * sizeof(int64_t),
                                             cudaHostAllocDefault);
+    if (e == cudaSuccess) e = cudaMalloc((void **)&c->dword, sizeof(unsigned long long));
     if (e != cudaSuccess) {
         *status = cuda_fail(e, "dev_ctx");
         delete c;
@@ -429,6 +430,25 @@ void hsvd_default_config(hsvd_config *cfg)
     cfg->block_streams = 2;
 }
 
+}  // extern "C"
+
+namespace hsvd {
+// smallest column index holding a NaN or an infinity (block.y = column)
+__global__ void k_first_nonfinite(const double *__restrict__ G, int64_t ldg, int64_t n,
+                                  unsigned long long *first)
+{
+    const int64_t c = blockIdx.y;
+    const double *g = G + c * ldg;
+    bool bad = false;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+         e += (int64_t)gridDim.x * blockDim.x)
+        bad |= !isfinite(g[e]);
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicMin(first, (unsigned long long)c);
+}
+}  // namespace hsvd
+
+extern "C" {
+
 int64_t hsvd_drive_workspace_size(int64_t n, int64_t r, const hsvd_config *cfg)
 {
     if (cfg->mode == HSVD_MODE_BLOCK) return block_workspace_size(n, r, cfg);
@@ -470,6 +490,22 @@ int hsvd_drive(double *G, int64_t n, int64_t r, int64_t ldg, double *Vinv_t,
     HSVD_CUDA(cudaEventRecord(ctx->ev, caller));
     HSVD_CUDA(cudaStreamWaitEvent(ctx->s, ctx->ev, 0));
     double *V = cfg->accumulate_v ? Vinv_t : nullptr;
+    // as_factor's finiteness check (linalg.py:58-65), on the device: one
+    // read of G before anything else touches it
+    {
+        HSVD_CUDA(cudaMemsetAsync(ctx->dword, 0xff, sizeof(unsigned long long), ctx->s));
+        const unsigned gx = (unsigned)((n + 255) / 256 < 8 ? (n + 255) / 256 : 8);
+        k_first_nonfinite<<<dim3(gx, (unsigned)r), 256, 0, ctx->s>>>(G, ldg, n, ctx->dword);
+        HSVD_LAUNCH_CHECK("k_first_nonfinite");
+        HSVD_CUDA(cudaMemcpyAsync(ctx->host, ctx->dword, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                                  ctx->s));
+        HSVD_CUDA(cudaStreamSynchronize(ctx->s));
+        if ((unsigned long long)ctx->host[0] != kNoError) {
+            set_error("G contains non-finite entries (column " + std::to_string(ctx->host[0]) +
+                      ")");
+            return res_host->status = HSVD_ERR_ARG;
+        }
+    }
     int st;
     if (cfg->mode == HSVD_MODE_BLOCK)
         st = block_drive(G, n, r, ldg, V, ldv, signs_host, p, cfg, sigma, lam,

@@ -678,6 +678,40 @@ HSVD_API int hsvd_bp_workspace_size(int64_t n, size_t *bytes)
     return HSVD_OK;
 }
 
+}  // extern "C"
+
+namespace hsvd {
+// ||M||_F^2 of an n x n column-major M in a fixed order (deterministic):
+// block k sums columns k, k + grid, ... (each column's rows strided over the
+// threads, then a fixed tree); one block folds the partials in block order
+constexpr int FROB_BLOCKS = 256;
+__global__ void k_frob_partials(const double *__restrict__ M, int64_t ldm, int64_t n,
+                                double *__restrict__ part)
+{
+    __shared__ double sh[256];
+    double acc = 0.0;
+    for (int64_t c = blockIdx.x; c < n; c += gridDim.x)
+        for (int64_t e = threadIdx.x; e < n; e += blockDim.x) acc = fma(M[c * ldm + e], M[c * ldm + e], acc);
+    sh[threadIdx.x] = acc;
+    __syncthreads();
+    for (int o = 128; o; o >>= 1) {
+        if ((int)threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+}
+__global__ void k_frob_fold(const double *__restrict__ part, int nparts, double *out)
+{
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int k = 0; k < nparts; ++k) t += part[k];
+        *out = t;
+    }
+}
+}  // namespace hsvd
+
+extern "C" {
+
 HSVD_API int hsvd_bp_factor_dd(const double *M, const double *Mlo, int64_t n, int64_t ldm,
                                double thresh, double *G, int64_t ldg, int8_t *signs,
                                int64_t *perm, int64_t *p_out, int64_t *stage_out, void *ws,
@@ -702,6 +736,20 @@ HSVD_API int hsvd_bp_factor_dd(const double *M, const double *Mlo, int64_t n, in
     if (ctx->host_reserve(8) != HSVD_OK) return HSVD_ERR_CUDA;
     int64_t *hbuf = ctx->host;  // pinned
     const double alpha = (1.0 + sqrt(17.0)) / 8.0;
+    if (thresh < 0.0) {
+        // the reference's singularity threshold n eps ||M||_F (factory.py:
+        // 270-282), from M on the device (G's storage as the partial buffer:
+        // it is written only after this)
+        const int parts = (int)(n < FROB_BLOCKS ? n : FROB_BLOCKS);  // <= n <= n * ldg
+        k_frob_partials<<<parts, 256, 0, s>>>(M, ldm, n, G);
+        k_frob_fold<<<1, 32, 0, s>>>(G, parts, G);  // total into G[0] (in place)
+        HSVD_LAUNCH_CHECK("k_frob");
+        HSVD_CUDA(cudaMemcpyAsync(hbuf, G, sizeof(double), cudaMemcpyDeviceToHost, s));
+        HSVD_CUDA(cudaStreamSynchronize(s));
+        double ss;
+        memcpy(&ss, hbuf, sizeof(double));
+        thresh = (double)n * 0x1p-52 * sqrt(ss);
+    }
 
     k_bp_init<<<1184, 256, 0, s>>>(M, Mlo, ldm, n, w);
     k_bp_init_state<<<1, 256, 0, s>>>(n, w, perm);

@@ -97,6 +97,7 @@ struct DevCtx {
     cudaEvent_t ev = nullptr, t0 = nullptr, t1 = nullptr;
     int64_t *host = nullptr;  // pinned
     int64_t host_len = 0;
+    unsigned long long *dword = nullptr;  // one device word (input checks)
     std::vector<cudaStream_t> xs;
     std::vector<cudaEvent_t> xev, xt0, xt1;
     std::vector<cudaEvent_t> evs;   // plain (non-timing) events

@@ -103,7 +103,7 @@ def bunch_parlett_factor_device(Mt, thresh=None):
         raise ShapeError("M must be square")
     Mt = Mt.contiguous()
     if thresh is None:
-        thresh = n * EPS * float(torch.linalg.norm(Mt))
+        thresh = -1.0  # n eps ||M||_F, computed by the library on the device
     L = _lib.load()
     size = ctypes.c_size_t(0)
     _lib.check(L.hsvd_bp_workspace_size(n, ctypes.byref(size)))

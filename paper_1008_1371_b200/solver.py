@@ -242,8 +242,6 @@ def drive(G, J, cfg=None):
     if isinstance(G, torch.Tensor) and G.is_cuda:
         if G.dim() != 2:
             raise ShapeError("G must be a matrix")
-        if not bool(torch.isfinite(G).all()):
-            raise ValueError("G contains non-finite entries")
         # always a fresh buffer: drive_device overwrites it with U, and the
         # caller's G is never mutated (solver.py:188).  (.t().contiguous()
         # would alias a column-major float64 G.)
@@ -254,7 +252,7 @@ def drive(G, J, cfg=None):
             res.Vinv_t = res.Vinv_t.t()
         return res
     # as_factor (linalg.py:58-65) without its host-side finiteness scan: the
-    # factor is checked on the device right after the upload instead
+    # library checks the factor on the device before the solve (ValueError)
     G = np.asfortranarray(G, dtype=np.float64)
     if G.ndim != 2:
         raise ShapeError("G must be a matrix")
@@ -267,8 +265,6 @@ def drive(G, J, cfg=None):
         raise ShapeError("G must have n >= r")
     dev = _device.require_cuda()
     Gt = _device.colmajor_to_device(G, dev)
-    if not bool(torch.isfinite(Gt).all()):
-        raise ValueError("G contains non-finite entries")
     res = drive_device(Gt, J, cfg)
     # results land in page-locked host memory (a pageable device->host copy
     # runs at a fraction of the link rate); the numpy arrays keep it alive

@@ -173,3 +173,17 @@ def test_shape_errors():
         H.drive(np.eye(3), H.SignatureVector.from_p(3, 3))
     with pytest.raises(H.ShapeError):
         H.drive(np.ones((2, 4)), H.SignatureVector.from_p(4, 4))
+
+
+@pytest.mark.parametrize("mode", ["pointwise", "block"])
+@pytest.mark.parametrize("bad", [np.nan, np.inf, -np.inf])
+def test_nonfinite_input_raises(mode, bad):
+    """as_factor's finiteness rule (linalg.py:58-65), checked on the device
+    by the library (no host scan): numpy and CUDA-tensor inputs alike."""
+    G = make_case_input(64, 64, 1, "gauss")
+    G[17, 40] = bad
+    cfg = H.SolverConfig(mode=mode, block_cols=16)
+    with pytest.raises(ValueError, match="non-finite"):
+        H.drive(G, H.SignatureVector.from_p(64, 32), cfg)
+    with pytest.raises(ValueError, match="non-finite"):
+        H.drive(torch.from_numpy(G).cuda(), H.SignatureVector.from_p(64, 32), cfg)
