@@ -210,6 +210,44 @@ struct GramRoles<64> {
     // super-tile (4 tiles); warps 4 and 5 add one diagonal tile each, (1,1)
     // and (3,3); warps 6 and 7 own the remaining 10 diagonal-block tiles.
     static constexpr int NACC = 5;  // accumulator tiles per warp (max)
+    static constexpr int NFRAG = 5;  // fragments per warp and k-step (max)
+    // split form for software pipelining: load() the k-step's fragments,
+    // compute() its DMMAs (the same operations and order as mma())
+    template <class LD>
+    __device__ static void load(int warp, LD &&ld, double (&f)[NFRAG])
+    {
+        if (warp < 6) {
+            const int R = warp < 3 ? 0 : (warp < 5 ? 1 : 2);
+            const int C = warp < 3 ? warp + 1 : (warp < 5 ? warp - 1 : 3);
+            f[0] = ld(16 * R);
+            f[1] = ld(16 * R + 8);
+            f[2] = ld(16 * C);
+            f[3] = ld(16 * C + 8);
+            if (warp >= 4) f[4] = ld(8 * (2 * warp - 7));
+        } else {
+            const int d = warp - 6;
+            f[0] = ld(16 * d);
+            f[1] = ld(16 * d + 8);
+            f[2] = ld(16 * (d + 2));
+            f[3] = ld(16 * (d + 2) + 8);
+        }
+    }
+    __device__ static void compute(int warp, const double (&f)[NFRAG], double (&acc)[NACC][2])
+    {
+        if (warp < 6) {
+            dmma(acc[0][0], acc[0][1], f[0], f[2]);
+            dmma(acc[1][0], acc[1][1], f[0], f[3]);
+            dmma(acc[2][0], acc[2][1], f[1], f[2]);
+            dmma(acc[3][0], acc[3][1], f[1], f[3]);
+            if (warp >= 4) dmma(acc[4][0], acc[4][1], f[4], f[4]);
+        } else {
+            dmma(acc[0][0], acc[0][1], f[0], f[0]);
+            dmma(acc[1][0], acc[1][1], f[0], f[1]);
+            dmma(acc[2][0], acc[2][1], f[2], f[2]);
+            dmma(acc[3][0], acc[3][1], f[2], f[3]);
+            dmma(acc[4][0], acc[4][1], f[3], f[3]);
+        }
+    }
     template <class LD>
     __device__ static void mma(int warp, LD &&ld, double (&acc)[NACC][2])
     {
@@ -286,6 +324,25 @@ struct GramRoles<32> {
             dmma(acc[1][0], acc[1][1], ld(8 * rt), ld(8 * ct));
         }
     }
+    static constexpr int NFRAG = 4;
+    template <class LD>
+    __device__ static void load(int warp, LD &&ld, double (&f)[NFRAG])
+    {
+        int rt, ct;
+        tile(warp, 0, rt, ct);
+        f[0] = ld(8 * rt);
+        f[1] = ld(8 * ct);
+        if (warp < 2) {
+            tile(warp, 1, rt, ct);
+            f[2] = ld(8 * rt);
+            f[3] = ld(8 * ct);
+        }
+    }
+    __device__ static void compute(int warp, const double (&f)[NFRAG], double (&acc)[NACC][2])
+    {
+        dmma(acc[0][0], acc[0][1], f[0], f[1]);
+        if (warp < 2) dmma(acc[1][0], acc[1][1], f[2], f[3]);
+    }
 };
 
 // Cross-block roles (kSlotCross): only the b x b block G_I^T G_J (8x8 tile
@@ -305,6 +362,30 @@ struct GramRolesX {
         } else if (q == 0 && warp < 4) {
             rt = warp >> 1;
             ct = TT + (warp & 1);
+        }
+    }
+    static constexpr int NFRAG = 3;
+    template <class LD>
+    __device__ static void load(int warp, LD &&ld, double (&f)[NFRAG])
+    {
+        if (B2 == 64) {
+            const int c0 = TT + 2 * (warp & 1);
+            f[0] = ld(8 * (warp >> 1));
+            f[1] = ld(8 * c0);
+            f[2] = ld(8 * (c0 + 1));
+        } else if (warp < 4) {
+            f[0] = ld(8 * (warp >> 1));
+            f[1] = ld(8 * (TT + (warp & 1)));
+        }
+    }
+    template <int NACC>
+    __device__ static void compute(int warp, const double (&f)[NFRAG], double (&acc)[NACC][2])
+    {
+        if (B2 == 64) {
+            dmma(acc[0][0], acc[0][1], f[0], f[1]);
+            dmma(acc[1][0], acc[1][1], f[0], f[2]);
+        } else if (warp < 4) {
+            dmma(acc[0][0], acc[0][1], f[0], f[1]);
         }
     }
     template <class LD, int NACC>
@@ -617,20 +698,35 @@ __global__ void __launch_bounds__(kThreads + 32, HSVD_GRAM_TMA_OCC) k_gram_tma(
         const bool cross = act && skipf[slot] == kSlotCross;
         mbar_wait(full0 + 8 * st, ph);
         const unsigned char *xs = S.x[st];
+        // fragments of k-step kk + 4 are loaded while k-step kk's DMMAs run
+        // (two register sets): the loads no longer wait for the previous
+        // DMMAs to release their operand registers
+        auto ldk = [&](int kk) {
+            const unsigned char *xq = xs + (kk >> 4) * (B2 * 128) + off[(kk >> 2) & 3];
+            return [xq](int R) { return *(const double *)(xq + R * 128); };
+        };
         if (HSVD_GRAM_NOMATH) {
             // diagnostic: no DMMA (data movement floor)
         } else if (cross) {
+            using RX = GramRolesX<B2>;
+            double fa[RX::NFRAG], fb[RX::NFRAG];
+            RX::load(warp, ldk(0), fa);
 #pragma unroll
-            for (int kk = 0; kk < KT; kk += 4) {
-                const unsigned char *xq = xs + (kk >> 4) * (B2 * 128) + off[(kk >> 2) & 3];
-                GramRolesX<B2>::mma(warp, [&](int R) { return *(const double *)(xq + R * 128); },
-                                    acc);
+            for (int kk = 0; kk < KT; kk += 8) {
+                RX::load(warp, ldk(kk + 4), fb);
+                RX::compute(warp, fa, acc);
+                if (kk + 8 < KT) RX::load(warp, ldk(kk + 8), fa);
+                RX::compute(warp, fb, acc);
             }
         } else {
+            double fa[Roles::NFRAG], fb[Roles::NFRAG];
+            Roles::load(warp, ldk(0), fa);
 #pragma unroll
-            for (int kk = 0; kk < KT; kk += 4) {
-                const unsigned char *xq = xs + (kk >> 4) * (B2 * 128) + off[(kk >> 2) & 3];
-                Roles::mma(warp, [&](int R) { return *(const double *)(xq + R * 128); }, acc);
+            for (int kk = 0; kk < KT; kk += 8) {
+                Roles::load(warp, ldk(kk + 4), fb);
+                Roles::compute(warp, fa, acc);
+                if (kk + 8 < KT) Roles::load(warp, ldk(kk + 8), fa);
+                Roles::compute(warp, fb, acc);
             }
         }
         __syncwarp();
