@@ -557,6 +557,56 @@ struct GramTmaSmem {
     alignas(1024) unsigned char x[STAGES][STAGE_BYTES];
     unsigned long long full[STAGES], empty[STAGES];
     int cidx[MAXSLOTS][B2];
+    int64_t slot[MAXSLOTS];  // the CTA's slots (through the active list)
+    int cross[MAXSLOTS];     // their Gram class (kSlotCross or not)
+};
+
+// One stage (KT rows) of a warp's DMMAs with the role resolved outside the
+// k loop: the loop body is straight-line code, so the next k-step's
+// fragment loads can be scheduled under the current k-step's DMMAs.
+// NF fragments per k-step at byte offsets fo[] (row base * 128) from the
+// lane's swizzled k-chunk; PAIRS lists the DMMAs as (A fragment, B
+// fragment) into accumulators 0..ND-1 -- the same operations, in the same
+// order, as GramRoles<64>::mma / GramRolesX<64>::mma.
+template <int KT, int NF, int ND, class PAIRS, int NACC>
+__device__ __forceinline__ void gram_stage(const unsigned char *xs, const unsigned (&off)[4],
+                                           const int (&fo)[NF], double (&acc)[NACC][2],
+                                           int sub_bytes)
+{
+    double fa[NF], fb[NF];
+    auto load = [&](int kk, double (&f)[NF]) {
+        const unsigned char *xq = xs + (kk >> 4) * sub_bytes + off[(kk >> 2) & 3];
+#pragma unroll
+        for (int j = 0; j < NF; ++j) f[j] = *(const double *)(xq + fo[j]);
+    };
+    auto comp = [&](const double (&f)[NF]) {
+#pragma unroll
+        for (int q = 0; q < ND; ++q)
+            dmma(acc[q][0], acc[q][1], f[PAIRS::a(q)], f[PAIRS::b(q)]);
+    };
+    load(0, fa);
+#pragma unroll
+    for (int kk = 0; kk < KT; kk += 8) {
+        load(kk + 4, fb);
+        comp(fa);
+        if (kk + 8 < KT) load(kk + 8, fa);
+        comp(fb);
+    }
+}
+// GramRoles<64> warps 0-5: 2x2 super-tile (a0 a1 b0 b1) [+ diagonal e]
+struct PairsSuper {
+    __device__ static constexpr int a(int q) { return q < 4 ? (q >> 1) : 4; }
+    __device__ static constexpr int b(int q) { return q < 4 ? 2 + (q & 1) : 4; }
+};
+// GramRoles<64> warps 6-7: f0 f1 g0 g1 -> (f0 f0) (f0 f1) (g0 g0) (g0 g1) (g1 g1)
+struct PairsDiag {
+    __device__ static constexpr int a(int q) { return q < 2 ? 0 : (q < 4 ? 2 : 3); }
+    __device__ static constexpr int b(int q) { return q == 0 ? 0 : (q == 1 ? 1 : (q == 2 ? 2 : 3)); }
+};
+// GramRolesX<64>: a b0 b1 -> (a b0) (a b1)
+struct PairsCross {
+    __device__ static constexpr int a(int) { return 0; }
+    __device__ static constexpr int b(int q) { return 1 + q; }
 };
 
 // fragment row f of an 8-row group <-> line p(f) of the 8-line swizzle atom
@@ -598,6 +648,12 @@ __global__ void __launch_bounds__(kThreads + 32, HSVD_GRAM_TMA_OCC) k_gram_tma(
         int64_t I = iblk[slot], J = jblk[slot];
         if (I > J) { int64_t t = I; I = J; J = t; }
         S.cidx[si][c] = (int)rho[slot_pos(c, b, I, J)];
+        if (c == 0) {
+            // slot id and Gram class, read once here rather than through
+            // two dependent global loads at every stage
+            S.slot[si] = slot;
+            S.cross[si] = act && skipf[slot] == kSlotCross;
+        }
     }
     const unsigned full0 = (unsigned)__cvta_generic_to_shared(&S.full[0]);
     const unsigned empty0 = (unsigned)__cvta_generic_to_shared(&S.empty[0]);
@@ -687,15 +743,36 @@ __global__ void __launch_bounds__(kThreads + 32, HSVD_GRAM_TMA_OCC) k_gram_tma(
 #pragma unroll
     for (int a = 0; a < 4; ++a)
         off[a] = (unsigned)(lp * 128 + ((((2 * a) | (fk >> 1)) ^ lp) << 4) + (fk & 1) * 8);
+    // fragment row bases (x 128 bytes) of this warp's role (B2 = 64; the
+    // same rows GramRoles<64> / GramRolesX<64> read)
+    int fo4[4], fo5[5], foX[3];
+    {
+        const int R = warp < 3 ? 0 : (warp < 5 ? 1 : 2);
+        const int C = warp < 3 ? warp + 1 : (warp < 5 ? warp - 1 : 3);
+        const int d = warp - 6;
+        const bool diag = warp >= 6;
+        fo4[0] = (diag ? 16 * d : 16 * R) * 128;
+        fo4[1] = (diag ? 16 * d + 8 : 16 * R + 8) * 128;
+        fo4[2] = (diag ? 16 * (d + 2) : 16 * C) * 128;
+        fo4[3] = (diag ? 16 * (d + 2) + 8 : 16 * C + 8) * 128;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) fo5[j] = fo4[j];
+        fo5[4] = (warp >= 4 && warp < 6 ? 8 * (2 * warp - 7) : 0) * 128;
+        const int c0 = B2 / 16 + 2 * (warp & 1);
+        foX[0] = 8 * (warp >> 1) * 128;
+        foX[1] = 8 * c0 * 128;
+        foX[2] = 8 * (c0 + 1) * 128;
+    }
     double acc[Roles::NACC][2];
 #pragma unroll
     for (int q = 0; q < Roles::NACC; ++q) acc[q][0] = acc[q][1] = 0.0;
     int c_si = 0, c_k = kt0;
+    int c_seg = kt0 / Lseg, c_in = kt0 % Lseg;  // segment, k-tiles done in it
     for (int i = 0; i < nitems; ++i) {
         const int st = i % STAGES;
         const unsigned ph = (unsigned)(i / STAGES) & 1u;
-        const int64_t slot = act ? act[slot0 + c_si] : slot0 + c_si;
-        const bool cross = act && skipf[slot] == kSlotCross;
+        const int64_t slot = S.slot[c_si];
+        const bool cross = S.cross[c_si] != 0;
         mbar_wait(full0 + 8 * st, ph);
         const unsigned char *xs = S.x[st];
         // fragments of k-step kk + 4 are loaded while k-step kk's DMMAs run
@@ -707,6 +784,17 @@ __global__ void __launch_bounds__(kThreads + 32, HSVD_GRAM_TMA_OCC) k_gram_tma(
         };
         if (HSVD_GRAM_NOMATH) {
             // diagnostic: no DMMA (data movement floor)
+        } else if (B2 == 64) {
+            constexpr int SB = B2 * 128;
+            if (cross) {
+                gram_stage<KT, 3, 2, PairsCross>(xs, off, foX, acc, SB);
+            } else if (warp < 4) {
+                gram_stage<KT, 4, 4, PairsSuper>(xs, off, fo4, acc, SB);
+            } else if (warp < 6) {
+                gram_stage<KT, 5, 5, PairsSuper>(xs, off, fo5, acc, SB);
+            } else {
+                gram_stage<KT, 4, 5, PairsDiag>(xs, off, fo4, acc, SB);
+            }
         } else if (cross) {
             using RX = GramRolesX<B2>;
             double fa[RX::NFRAG], fb[RX::NFRAG];
@@ -731,10 +819,16 @@ __global__ void __launch_bounds__(kThreads + 32, HSVD_GRAM_TMA_OCC) k_gram_tma(
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(empty0 + 8 * st);
-        const int seg = c_k / Lseg;
-        const bool seg_end = c_k == T - 1 || c_k + 1 == (seg + 1) * Lseg;
+        // segment bookkeeping without a division per stage
+        const int seg = c_seg;
+        const bool seg_end = c_k == T - 1 || ++c_in == Lseg;
+        if (seg_end) {
+            c_in = 0;
+            ++c_seg;
+        }
         if (++c_k == T) {
             c_k = 0;
+            c_seg = 0;
             ++c_si;
         }
         if (seg_end) {
