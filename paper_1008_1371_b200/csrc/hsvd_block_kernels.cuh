@@ -957,10 +957,42 @@ __device__ __forceinline__ int rotation_fast_wide(double a_ii, double a_jj, doub
     return 0;
 }
 
-// The trigonometric and hyperbolic forms share one division, one square root
-// and one reciprocal square root, selected per lane: a warp whose pairs mix
-// both kinds (every pivot block that straddles the sign boundary) runs one
-// dependent chain instead of both branches one after the other.
+// Branch-free FP64 reciprocal, reciprocal square root and square root for
+// the rotation's critical chain: the hardware approximation (MUFU) refined by
+// two Newton steps (error ~2^-20 -> ~2^-80, i.e. within an ulp or so), for
+// positive normal operands in [1e-300, 1e300].  The library routines carry a
+// slow-path branch each, which keeps the compiler from overlapping them.
+__device__ __forceinline__ double fast_rcp(double x)
+{
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double e = fma(-x, y, 1.0);
+    y = fma(y, e, y);
+    e = fma(-x, y, 1.0);
+    return fma(y, e, y);
+}
+__device__ __forceinline__ double fast_rsqrt(double x)
+{
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double e = fma(-x * y, y, 1.0);  // 1 - x y^2
+    y = fma(0.5 * y, e, y);
+    e = fma(-x * y, y, 1.0);
+    return fma(0.5 * y, e, y);
+}
+__device__ __forceinline__ double fast_sqrt(double x)
+{
+    const double y = fast_rsqrt(x);
+    const double s = x * y;
+    return fma(0.5 * y, fma(-s, s, x), s);  // one correction of x y
+}
+
+// The trigonometric and hyperbolic forms share one square root, one
+// reciprocal and one reciprocal square root, selected per lane: a warp whose
+// pairs mix both kinds (every pivot block that straddles the sign boundary)
+// runs one dependent chain instead of both branches one after the other.
+//   w = base + sqrt(rad),  t = num / w,  c = 1 / sqrt(1 +- t^2) = w / sqrt(w^2 +- e^2)
+// so the quotient and c's reciprocal square root run side by side.
 __device__ __forceinline__ int rotation_fast(double a_ii, double a_jj, double a_ij, int hyp,
                                              double &t_out, double &c_out)
 {
@@ -971,15 +1003,21 @@ __device__ __forceinline__ int rotation_fast(double a_ii, double a_jj, double a_
     const bool h = hyp > 0;
     const double d = a_jj - a_ii, ad = fabs(d), sm = a_ii + a_jj;
     const double base = h ? sm : ad;
-    if (!(base < 1e150 && ae < 1e150)) return rotation_fast_wide(a_ii, a_jj, a_ij, hyp, t_out, c_out);
+    const double big = fmax(base, ae);
+    // operands beyond 1e150 or below 1e-140: the quotient forms
+    if (!(big < 1e150 && big > 1e-140)) return rotation_fast_wide(a_ii, a_jj, a_ij, hyp, t_out, c_out);
     const double sg = (d == 0.0 || (d > 0.0) == (e > 0.0)) ? ae : -ae;
     const double num = h ? -e : sg;
     const double rad = h ? (sm - ae) * (sm + ae) : fma(d, d, e * e);
-    const double t = num / (base + sqrt(rad));
-    const double u = fma(h ? -t : t, t, 1.0);
-    if (h && !(rad > 0.0 && u > 0.0)) return 1;
+    if (h && !(rad > 0.0)) return 1;
+    const double w = base + fast_sqrt(rad);
+    const double g = h ? (w - ae) * (w + ae) : fma(w, w, ae * ae);
+    if (h && !(g > 0.0)) return 1;
+    const double rw = fast_rcp(w);
+    double t = num * rw;
+    t = fma(fma(-w, t, num), rw, t);  // one correction of the quotient
     t_out = t;
-    c_out = rsqrt(u);
+    c_out = w * fast_rsqrt(g);
     return 0;
 }
 
@@ -1100,7 +1138,7 @@ static __global__ void k_reuse_sweep_end(const int64_t *__restrict__ rho,
 static __global__ void k_reuse_next_sweep(int32_t *dsweep) { *dsweep += 1; }
 
 template <int B2, bool FAST>
-__global__ void __launch_bounds__(inner_threads<B2>()) k_inner(InnerArgs a)
+__global__ void __launch_bounds__(inner_threads<B2>()) k_inner_v1(InnerArgs a)
 {
     constexpr int NT = inner_threads<B2>();
     extern __shared__ __align__(16) unsigned char ism_raw[];
@@ -1433,6 +1471,8 @@ __global__ void __launch_bounds__(inner_threads<B2>()) k_inner(InnerArgs a)
     }
 }
 
+#include "hsvd_inner.cuh"
+
 // ---------------------------------------------------------------------
 // k_update: [G_P; V_P] <- [G_P; V_P] W_P in place, FP64 tensor cores
 // ---------------------------------------------------------------------
@@ -1729,7 +1769,7 @@ struct BlockKernels {
     static constexpr int TSTAGES = HSVD_GRAM_TMA_STAGES;
     static size_t gram_smem() { return sizeof(GramSmem<B2, KT, STAGES>); }
     static size_t gram_tma_smem() { return sizeof(GramTmaSmem<B2, KT, TSTAGES>) + 1024; }
-    static size_t inner_smem() { return sizeof(InnerSmem<B2>); }
+    static size_t inner_smem() { return sizeof(InnerSmem2<B2>); }
     static size_t upd_smem() { return sizeof(UpdSmem<B2, MT>); }
     static int setup()
     {
@@ -1742,10 +1782,16 @@ struct BlockKernels {
         HSVD_CUDA(cudaFuncSetAttribute(k_gram_tma<B2, KT, TSTAGES, true>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)gram_tma_smem()));
-        HSVD_CUDA(cudaFuncSetAttribute(k_inner<B2, true>,
+        HSVD_CUDA(cudaFuncSetAttribute(k_inner<B2, true, true>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)inner_smem()));
-        HSVD_CUDA(cudaFuncSetAttribute(k_inner<B2, false>,
+        HSVD_CUDA(cudaFuncSetAttribute(k_inner<B2, true, false>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)inner_smem()));
+        HSVD_CUDA(cudaFuncSetAttribute(k_inner<B2, false, true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)inner_smem()));
+        HSVD_CUDA(cudaFuncSetAttribute(k_inner<B2, false, false>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)inner_smem()));
         HSVD_CUDA(cudaFuncSetAttribute(k_update<B2, MT>,
@@ -1836,7 +1882,7 @@ struct BlockKernels {
             // of a concurrent stream (split mode)
             cudaLaunchConfig_t lc = {};
             lc.gridDim = dim3((unsigned)nslots);
-            lc.blockDim = dim3(inner_threads<B2>());
+            lc.blockDim = dim3(inner2_threads<B2>());
             lc.dynamicSmemBytes = inner_smem();
             lc.stream = s;
             cudaLaunchAttribute at[1];
@@ -1844,10 +1890,15 @@ struct BlockKernels {
             at[0].val.priority = inner_priority();
             lc.attrs = at;
             lc.numAttrs = 1;
-            if (cfg->block_rotation == HSVD_ROTATION_FAST) {
-                HSVD_CUDA(cudaLaunchKernelEx(&lc, k_inner<B2, true>, ia));
+            const bool fast = cfg->block_rotation == HSVD_ROTATION_FAST;
+            if (fast && full) {
+                HSVD_CUDA(cudaLaunchKernelEx(&lc, k_inner<B2, true, true>, ia));
+            } else if (fast) {
+                HSVD_CUDA(cudaLaunchKernelEx(&lc, k_inner<B2, true, false>, ia));
+            } else if (full) {
+                HSVD_CUDA(cudaLaunchKernelEx(&lc, k_inner<B2, false, true>, ia));
             } else {
-                HSVD_CUDA(cudaLaunchKernelEx(&lc, k_inner<B2, false>, ia));
+                HSVD_CUDA(cudaLaunchKernelEx(&lc, k_inner<B2, false, false>, ia));
             }
         }
         T.end(s);

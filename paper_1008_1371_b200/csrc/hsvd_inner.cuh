@@ -1,0 +1,553 @@
+// hsvd_inner.cuh -- k_inner: one pass of 2x2 rotations on the 2b x 2b pivot
+// Gram A_P in shared memory, accumulating the J-orthogonal W_P
+// (A_P <- W^T A_P W).  Included by hsvd_block_kernels.cuh (namespace hsvd).
+//
+// The pass is a chain of 2b-1 (full ordering) or b (oriented) rounds of b
+// disjoint rotations; each round needs the previous round's A.  The kernel
+// is laid out around that chain (round-1 k_inner_v1 moved ~128 KB of shared
+// memory per round and ran at ~2.7k cycles per round):
+//
+// * A holds only its upper triangle: entry (r, c) lives at [min][max].  A
+//   round is the congruence A <- R^T A R with R block-diagonal in 2x2
+//   blocks, so only the b(b+1)/2 blocks (p, q), q = p + d (mod b),
+//   d = 0..b/2, are rewritten: half the shared-memory traffic of updating
+//   both triangles, and A stays exactly symmetric.
+// * Warp 0 forms the round's b rotations (lane q owns pair q) and publishes
+//   them into a per-round log (t, c, st) with an mbarrier per round
+//   (release/acquire: the other warps' stores of round k wait for warp 0's
+//   loads of round k).  The A warps then update their blocks; one named
+//   barrier among the A warps ends an active round.  A round in which no
+//   pair rotates costs no barrier.
+// * W never touches shared memory: W_P's rows are independent under
+//   W <- W R, so each of the 2b rows lives in the registers of one thread of
+//   the W warps, which replay the rotation log behind the A chain (off its
+//   critical path).  Registers cannot be indexed at run time, so a W row is
+//   kept in "position space": under the circle method pair x of round rd is
+//   columns (rd + x, rd - x) mod (2b-1) (pair 0: (2b-1, rd)), which in
+//   positions pos(c) = (c - rd) mod (2b-1) is the FIXED pairing (x, 2b-1-x),
+//   (0, 2b-1); between rounds every position moves down by one.  The move is
+//   register renaming inside U unrolled rounds and one cyclic shift of the
+//   row per U rounds.  The oriented ordering is the same with the j half
+//   cycling.
+// The element operations (and their order) are those of k_inner_v1, so a
+// W row sees exactly the same FMA sequence; A's upper entries are computed
+// by the same formulas (block (p, q) as rows of pair p, columns of pair q).
+
+#ifndef HSVD_INNER_DIAG_NOW
+#define HSVD_INNER_DIAG_NOW 0
+#endif
+#ifndef HSVD_INNER_DIAG_NOUPD
+#define HSVD_INNER_DIAG_NOUPD 0
+#endif
+#ifndef HSVD_INNER_AWARPS64
+#define HSVD_INNER_AWARPS64 6  // A warps at b = 32 (+ 2 W warps: 8 warps, 255 registers)
+#endif
+
+template <int B2>
+struct InnerCfg {
+    static constexpr int b = B2 / 2;
+    static constexpr int NAW = B2 == 64 ? HSVD_INNER_AWARPS64 : 4;  // A warps
+    static constexpr int NA = NAW * 32;                            // A threads
+    static constexpr int NWW = B2 / 32;                            // W warps: a row per thread
+    static constexpr int NT = NA + NWW * 32;
+    static constexpr int LDA = B2;
+    // upper blocks (p, p + d): d = 0..b/2-1 for every p, d = b/2 for p < b/2
+    static constexpr int NBLK = b * (b / 2) + b / 2;
+    static constexpr int NB = (NBLK + NA - 1) / NA;  // blocks per A thread (at most)
+    static_assert(NA % b == 0, "k_inner: A warp count");
+    // full ordering: 2b-1 rounds, cyclic over M = 2b-1 positions; U rounds
+    // are renamed in registers between row shifts (U divides the rounds)
+    static constexpr int M = B2 - 1;
+    static constexpr int UF = (M % 3 == 0) ? 3 : 1;
+    static constexpr int UO = 4;  // oriented: b rounds, b % 4 == 0
+};
+
+template <int B2>
+struct InnerSmem2 {
+    double A[B2 * B2];               // upper triangle, [min][max], ld B2
+    double2 ltc[B2][B2 / 2];         // rotation log of the pass: (t, c) per round and pair
+    unsigned long long full[B2];     // mbarrier per round: the log entry is published
+    unsigned long long wdone;        // W warps have replayed a whole pass
+    int lflag[B2];                   // bit 0: some pair rotated, bit 1: a pair failed
+    unsigned int lact[B2];           // per round: the pairs that rotated (bit x: pair x)
+    unsigned int lhyp[B2];           // per round: hyperbolic pairs (st = t), else st = -t
+    unsigned int jneg[2], padm[2];   // per-column bit masks (J = -1, padding)
+    unsigned int rot, skip, big;
+    unsigned long long maxt_bits;
+    unsigned long long fail;
+    unsigned long long touched;
+};
+
+template <int B2>
+__host__ __device__ constexpr int inner2_threads() { return InnerCfg<B2>::NT; }
+
+__device__ __forceinline__ void named_bar_sync(int id, int count)
+{
+    asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+
+// W warps wait for a published round without polling the shared-memory
+// pipe: the suspend hint parks the warp until the phase completes
+__device__ __forceinline__ void mbar_wait_parked(unsigned bar, unsigned parity)
+{
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "HSVD_MBP_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+        " @!p bra HSVD_MBP_%=;\n}\n" ::"r"(bar),
+        "r"(parity), "r"(1000000)
+        : "memory");
+}
+
+// columns of pair x in round rd: circle method on B2 players (FULL), or the
+// block-oriented pairing x <-> b + (x + rd) mod b.  Selects, no branches.
+template <int B2, bool FULL>
+__device__ __forceinline__ void inner_cols(int x, int rd, int &ci, int &cj)
+{
+    constexpr int b = B2 / 2;
+    if (FULL) {
+        constexpr int m = B2 - 1;
+        int u = rd + x, v = rd - x;
+        u = u >= m ? u - m : u;
+        v = v < 0 ? v + m : v;
+        ci = x == 0 ? m : u;
+        cj = v;  // x = 0: v = rd
+    } else {
+        int v = rd + x;
+        v = v >= b ? v - b : v;
+        ci = x;
+        cj = v + b;
+    }
+}
+
+// register of position p after S renamed rounds
+template <int B2, bool FULL>
+__host__ __device__ constexpr int inner_wreg(int p, int S)
+{
+    return FULL ? (p == B2 - 1 ? p : (p + S) % (B2 - 1))
+                : (p < B2 / 2 ? p : B2 / 2 + (p - B2 / 2 + S) % (B2 / 2));
+}
+
+// st = t for a hyperbolic pair, -t for a trigonometric one (a sign flip)
+__device__ __forceinline__ double inner_st(double t, unsigned hyp)
+{
+    return __longlong_as_double(__double_as_longlong(t) ^ ((unsigned long long)(hyp ^ 1u) << 63));
+}
+
+// per-pass statistics kept by W warp 0 (lane x: pair x), off the A chain
+struct InnerStats {
+    unsigned int rot = 0, skip = 0, big = 0;
+    unsigned long long touch = 0;
+    double maxt = 0.0;
+};
+
+// one round of the W replay on a register-resident row (sub-round S of U).
+// Straight-line: an inactive pair (and every pair of an inactive round) has
+// t = st = 0, c = 1, an exact no-op on the row up to the sign of a zero; no
+// branch keeps the 2b live doubles out of phi copies at every join.
+template <int B2, bool FULL, int S>
+__device__ __forceinline__ int inner_w_round(double (&w)[B2], const InnerSmem2<B2> &Sm, int rd,
+                                             unsigned bar, unsigned par, bool stats,
+                                             InnerStats &st_, unsigned long long padm,
+                                             double teps)
+{
+    constexpr int b = B2 / 2, M = B2 - 1;
+    mbar_wait_parked(bar, par);
+    const int f = *(volatile const int *)&Sm.lflag[rd];
+    const unsigned hm = Sm.lhyp[rd];
+#pragma unroll
+    for (int x = 0; x < b; ++x) {
+        // pair x in position space: full (x, M - x), pair 0 (M, 0);
+        // oriented (x, b + x)
+        const int pi = FULL ? (x == 0 ? M : x) : x;
+        const int pj = FULL ? (x == 0 ? 0 : M - x) : b + x;
+        const int ri = inner_wreg<B2, FULL>(pi, S), rj = inner_wreg<B2, FULL>(pj, S);
+        const double2 tc = Sm.ltc[rd][x];
+        const double t = tc.x, c = tc.y, st = inner_st(t, (hm >> x) & 1u);
+        const double wx = w[ri], wy = w[rj];
+        w[ri] = fma(st, wy, wx) * c;
+        w[rj] = fma(t, wx, wy) * c;
+    }
+    if (stats) {
+        // the reference's per-visit statistics (_kernels.py:218-233): lane x
+        // counts pair x of this round
+        const unsigned lane = threadIdx.x & 31;
+        if (lane < (unsigned)b && !(f & 2)) {
+            int i, j;
+            inner_cols<B2, FULL>((int)lane, rd, i, j);
+            const bool act = (Sm.lact[rd] >> lane) & 1u;
+            if (act) {
+                const double at = fabs(Sm.ltc[rd][lane].x);
+                ++st_.rot;
+                st_.touch |= (1ull << i) | (1ull << j);
+                st_.big |= at > teps;
+                st_.maxt = fmax(st_.maxt, at);
+            } else if (!(((padm >> i) | (padm >> j)) & 1)) {
+                ++st_.skip;  // pairs with a padding column are not visits
+            }
+        }
+    }
+    return f;
+}
+
+// W warps: replay the log onto one row of W (registers), U rounds per
+// cyclic shift of the row; returns false if the pass failed
+template <int B2, bool FULL>
+__device__ __forceinline__ bool inner_w_replay(double (&w)[B2], const InnerSmem2<B2> &Sm,
+                                               int passes, unsigned full0, unsigned wdone,
+                                               bool stats, InnerStats &st_,
+                                               unsigned long long padm, double teps)
+{
+    using C = InnerCfg<B2>;
+    constexpr int U = FULL ? C::UF : C::UO;
+    constexpr int rounds = FULL ? B2 - 1 : B2 / 2;
+    static_assert(U <= 4 && rounds % U == 0, "k_inner: W unroll");
+    for (int ps = 0; ps < passes; ++ps) {
+        const unsigned par = (unsigned)ps & 1u;
+        for (int r0 = 0; r0 < rounds; r0 += U) {
+            int f = inner_w_round<B2, FULL, 0>(w, Sm, r0, full0 + 8 * r0, par, stats, st_, padm, teps);
+            if (U > 1) f |= inner_w_round<B2, FULL, (U > 1 ? 1 : 0)>(w, Sm, r0 + 1, full0 + 8 * (r0 + 1), par, stats, st_, padm, teps);
+            if (U > 2) f |= inner_w_round<B2, FULL, (U > 2 ? 2 : 0)>(w, Sm, r0 + 2, full0 + 8 * (r0 + 2), par, stats, st_, padm, teps);
+            if (U > 3) f |= inner_w_round<B2, FULL, (U > 3 ? 3 : 0)>(w, Sm, r0 + 3, full0 + 8 * (r0 + 3), par, stats, st_, padm, teps);
+            // a failed round and every later round of the pass are published
+            // as failed: stop at the group that failed
+            if (f & 2) return false;
+            // positions move down by U: new reg[p] = old reg[p + U] (cyclic)
+            if (FULL) {
+                constexpr int M = B2 - 1;
+                double tmp[U];
+#pragma unroll
+                for (int k = 0; k < U; ++k) tmp[k] = w[k];
+#pragma unroll
+                for (int p = 0; p < M - U; ++p) w[p] = w[p + U];
+#pragma unroll
+                for (int k = 0; k < U; ++k) w[M - U + k] = tmp[k];
+            } else {
+                constexpr int b = B2 / 2;
+                double tmp[U];
+#pragma unroll
+                for (int k = 0; k < U; ++k) tmp[k] = w[b + k];
+#pragma unroll
+                for (int p = 0; p < b - U; ++p) w[b + p] = w[b + p + U];
+#pragma unroll
+                for (int k = 0; k < U; ++k) w[B2 - U + k] = tmp[k];
+            }
+        }
+        mbar_arrive(wdone);  // every W lane: this pass's log entries are consumed
+    }
+    return true;
+}
+
+template <int B2, bool FAST, bool FULL>
+__global__ void __launch_bounds__(inner2_threads<B2>()) k_inner(InnerArgs a)
+{
+    using C = InnerCfg<B2>;
+    constexpr int NA = C::NA, NT = C::NT, LDA = C::LDA, b = C::b;
+    constexpr int rounds = FULL ? B2 - 1 : b;
+    extern __shared__ __align__(16) unsigned char ism_raw[];
+    auto &S = *reinterpret_cast<InnerSmem2<B2> *>(ism_raw);
+    if (*(volatile unsigned long long *)a.err != kNoError) return;
+    const int slot = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    int64_t I = a.iblk[slot], J = a.jblk[slot];
+    if (I > J) { int64_t t = I; I = J; J = t; }
+    if (a.skipf && a.skipf[slot] == kSlotReused) {
+        // reused all-skip visit: the recorded statistics, no rotation, no
+        // update (empty touched set), stepper advanced as usual
+        if (tid == 0) {
+            a.tset[(int64_t)slot * kTsetStride] = 0;
+            a.skipk[slot] += a.ru.pairskip[I * a.nb + J];
+            inner_advance(a, slot, I, J);
+        }
+        return;
+    }
+    const unsigned full0 = (unsigned)__cvta_generic_to_shared(&S.full[0]);
+    const unsigned wdone = (unsigned)__cvta_generic_to_shared(&S.wdone);
+    const bool wwarp = warp >= C::NAW;
+
+    if (wwarp) {
+        // ---- W warps: their own code path (barrier 0 is shared with the A
+        // warps by count, so the row's registers never overlap the fold's)
+        const int wrow = (warp - C::NAW) * 32 + lane;
+        double w[B2];  // row `wrow` of W in position space
+#pragma unroll
+        for (int p = 0; p < B2; ++p) w[p] = p == wrow ? 1.0 : 0.0;
+        named_bar_sync(0, NT);  // the prologue (A, masks, mbarriers) is done
+        const unsigned long long padm =
+            B2 == 64 ? ((unsigned long long)S.padm[1] << 32) | S.padm[0] : S.padm[0];
+        const bool stats = warp == C::NAW;
+        InnerStats st_;
+#if !HSVD_INNER_DIAG_NOW  // diagnostics only (wrong W): no replay
+        inner_w_replay<B2, FULL>(w, S, a.passes, full0, wdone, stats, st_, padm, a.teps);
+#endif
+        if (stats) {
+            atomicAdd(&S.rot, st_.rot);
+            atomicAdd(&S.skip, st_.skip);
+            atomicOr(&S.big, st_.big);
+            atomicMax(&S.maxt_bits, (unsigned long long)__double_as_longlong(st_.maxt));
+            atomicOr(&S.touched, st_.touch);
+        }
+        named_bar_sync(0, NT);  // statistics and failure word are in
+        if (S.fail != kNoError) return;
+        // W column-major: Wg[slot][c * B2 + k] = W[k][c]; after whole passes
+        // every position is its column again
+        double *Wout = a.Wg + (int64_t)slot * B2 * B2 + wrow;
+#pragma unroll
+        for (int c = 0; c < B2; ++c) Wout[c * B2] = w[c];
+        if (a.trace && blockIdx.x == 0 && wrow == 0) a.trace[8 * 64] = clock64();
+        return;
+    }
+
+    {
+        // A = sum of the slot's partial segments in segment order (upper
+        // triangle, coalesced); all loads of a batch of segments are issued
+        // before the sums
+        const double *P0 = a.Apart + (int64_t)slot * a.maxseg * (B2 * B2);
+        const int nseg = (int)a.part.NSEG;
+        constexpr int PER = (B2 * B2 + NA - 1) / NA;
+        // cross class: the two diagonal blocks come from the cache, only the
+        // cross block from the partials (the same segment folds as a fresh
+        // visit, so the same bits)
+        const bool cross = a.skipf && a.skipf[slot] == kSlotCross;
+        double v[PER];
+#pragma unroll
+        for (int k = 0; k < PER; ++k) v[k] = 0.0;
+        constexpr int BATCH = 2;
+        for (int s0 = 0; s0 < nseg; s0 += BATCH) {
+            double x[BATCH][PER];
+#pragma unroll
+            for (int u = 0; u < BATCH; ++u)
+#pragma unroll
+                for (int k = 0; k < PER; ++k) {
+                    const int e = tid + k * NA, i = e / B2, j = e % B2;
+                    x[u][k] = (s0 + u < nseg && e < B2 * B2 && i <= j &&
+                               (!cross || (i < b && j >= b)))
+                                  ? P0[(int64_t)(s0 + u) * B2 * B2 + e] : 0.0;
+                }
+#pragma unroll
+            for (int u = 0; u < BATCH; ++u)
+#pragma unroll
+                for (int k = 0; k < PER; ++k)
+                    if (s0 + u < nseg) v[k] += x[u][k];
+        }
+        const bool cache = a.ru.dcache != nullptr;
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int e = tid + k * NA, i = e / B2, j = e % B2;
+            if (e < B2 * B2 && i <= j) {
+                const bool dI = j < b, dJ = i >= b;  // inside a diagonal block
+                if (cross && (dI || dJ)) {
+                    v[k] = dI ? a.ru.dcache[(I * b + i) * b + j]
+                              : a.ru.dcache[(J * b + (i - b)) * b + (j - b)];
+                } else if (cache && !cross && (dI || dJ)) {
+                    if (dI) a.ru.dcache[(I * b + i) * b + j] = v[k];
+                    else a.ru.dcache[(J * b + (i - b)) * b + (j - b)] = v[k];
+                }
+                S.A[i * LDA + j] = v[k];
+            }
+        }
+        if (tid < B2) {
+            const int64_t pos = slot_pos(tid, b, I, J);
+            const int neg = a.jsign[pos] < 0;
+            const int pad = a.orig[pos] >= a.real_cols;
+            const unsigned mneg = __ballot_sync(0xffffffffu, neg);
+            const unsigned mpad = __ballot_sync(0xffffffffu, pad);
+            if (lane == 0) {
+                S.jneg[warp] = mneg;
+                S.padm[warp] = mpad;
+            }
+        }
+        if (tid == 0) {
+            S.rot = S.skip = S.big = 0;
+            S.maxt_bits = 0;
+            S.fail = kNoError;
+            S.touched = 0;
+            for (int k = 0; k < rounds; ++k) mbar_init(full0 + 8 * k, 32);
+            mbar_init(wdone, C::NWW * 32);
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        }
+    }
+    named_bar_sync(0, NT);
+
+    {
+        const unsigned long long jneg =
+            B2 == 64 ? ((unsigned long long)S.jneg[1] << 32) | S.jneg[0] : S.jneg[0];
+        // block assignment: thread (group g = tid / b, pair p = tid % b)
+        // owns blocks (p, p + d), d = g + G k: d < b/2 for every p, d = b/2
+        // for p < b/2 (the rest of the upper triangle's blocks), larger d
+        // are dead slots.  p is the same in every slot: its rotation is
+        // loaded once per round
+        constexpr int G = NA / b, NB = (b / 2 + G) / G;
+        const int pk = tid % b, g = tid / b;
+        int qk[NB];
+        bool dg[NB], live[NB];
+#pragma unroll
+        for (int k = 0; k < NB; ++k) {
+            const int d = g + G * k;
+            live[k] = d < b / 2 || (d == b / 2 && pk < b / 2);
+            qk[k] = (pk + (live[k] ? d : 0)) % b;  // dead slots reload block (p, p)
+            dg[k] = qk[k] == pk;
+        }
+        const int q = lane % b;  // warp 0: pair owned by this lane
+        long long *tr = (a.trace && blockIdx.x == 0 && tid == 0) ? a.trace : nullptr;
+#define HSVD_STAMP(k) \
+    if (tr && it < 64) tr[8 * it + (k)] = clock64();
+        int rd = 0;
+        const int total = rounds * a.passes;
+        for (int it = 0; it < total; ++it, rd = rd + 1 == rounds ? 0 : rd + 1) {
+            HSVD_STAMP(0)
+            if (it > 0 && rd == 0) {
+                // pass boundary (passes > 1): the W warps must have replayed
+                // the previous pass before its log is overwritten
+                if (warp == 0) mbar_wait(wdone, (unsigned)((it / rounds) & 1) ^ 1u);
+            }
+            if (warp == 0) {
+                // ---- the round's b rotations.  The pair is rotated in its
+                // schedule orientation (i, j): the closed forms are odd
+                // (trig) or symmetric (hyperbolic) in the roles, so this is
+                // the sorted form's transformation except at zeta = 0
+                int i, j;
+                inner_cols<B2, FULL>(q, rd, i, j);
+                const int lo = i < j ? i : j, hi = i < j ? j : i;
+                const double a_ii = S.A[i * (LDA + 1)], a_jj = S.A[j * (LDA + 1)],
+                             a_ij = S.A[lo * LDA + hi];
+                // relative-orthogonality skip |a_ij| < eps sqrt(a_ii a_jj)
+                // (_kernels.py:211), squared: no square root on the chain;
+                // the rotation is formed beside the test (a_ij = 0 gives the
+                // identity) and selected
+                const bool skip = a_ij == 0.0 ||
+                                  (a.use_skip && a_ij * a_ij < (a.eps * a.eps) * (a_ii * a_jj));
+                HSVD_STAMP(5)
+                const int hyp = (((jneg >> i) ^ (jneg >> j)) & 1) ? 1 : -1;
+                double t, c;
+                const int status = FAST ? rotation_fast(a_ii, a_jj, a_ij, hyp, t, c)
+                                        : rotation_tc(a_ii, a_jj, a_ij, hyp, t, c);
+                const bool bad = !skip && status != 0, act = !skip && status == 0;
+                t = act ? t : 0.0;
+                c = act ? c : 1.0;
+                HSVD_STAMP(1)
+                if (lane < b) S.ltc[rd][q] = make_double2(t, c);
+                const unsigned va = __ballot_sync(0xffffffffu, act),
+                               vb = __ballot_sync(0xffffffffu, bad),
+                               vh = __ballot_sync(0xffffffffu, hyp > 0);
+                if (lane == 0) {
+                    S.lflag[rd] = (va ? 1 : 0) | (vb ? 2 : 0);
+                    S.lact[rd] = va;
+                    S.lhyp[rd] = vh;
+                }
+                if (bad && lane < b)
+                    atomicMin(&S.fail, pack_err(a.slot_base + slot, slot_pos(lo, b, I, J),
+                                                slot_pos(hi, b, I, J)));
+                if (vb) {
+                    // the W warps wait round by round: publish the rest of
+                    // the pass as failed so none of them waits forever
+                    for (int r2 = rd + 1; r2 < rounds; ++r2) {
+                        if (lane == 0) S.lflag[r2] = 2;
+                        mbar_arrive(full0 + 8 * r2);
+                    }
+                }
+                mbar_arrive(full0 + 8 * rd);  // release to the W warps
+            }
+            named_bar_sync(2, NA);  // the round's rotations are published (A warps)
+            HSVD_STAMP(2)
+            const int f = S.lflag[rd];
+            if (f & 2) break;
+            if (!(f & 1)) continue;
+#if HSVD_INNER_DIAG_NOUPD  // diagnostics only (wrong A): no block updates
+            if (1) { HSVD_STAMP(3) named_bar_sync(1, NA); HSVD_STAMP(4) continue; }
+#endif
+            // ---- blocks (p, q) of the upper triangle: rows of pair p,
+            // columns of pair q; X' = R_p^T X R_q.  Offsets first, then every
+            // load, then the arithmetic and the stores.
+            {
+                const unsigned hm = S.lhyp[rd];
+                int ip, jp;
+                inner_cols<B2, FULL>(pk, rd, ip, jp);
+                const double2 tcp = S.ltc[rd][pk];
+                const double tp = tcp.x, cp = tcp.y, sp = inner_st(tp, (hm >> pk) & 1u);
+                int o[NB][4];
+                double x[NB][4], tq[NB], cq[NB], sq[NB];
+#pragma unroll
+                for (int k = 0; k < NB; ++k) {
+                    int iq, jq;
+                    inner_cols<B2, FULL>(qk[k], rd, iq, jq);
+                    // canonical [min][max] offsets of (ip,iq) (ip,jq) (jp,iq) (jp,jq);
+                    // a diagonal block is (ip,ip) (ip,jp) (jp,ip) (jp,jp)
+                    o[k][0] = dg[k] ? ip * (LDA + 1) : min(ip, iq) * LDA + max(ip, iq);
+                    o[k][1] = min(ip, jq) * LDA + max(ip, jq);
+                    o[k][2] = min(jp, iq) * LDA + max(jp, iq);
+                    o[k][3] = dg[k] ? jp * (LDA + 1) : min(jp, jq) * LDA + max(jp, jq);
+                    const double2 tcq = S.ltc[rd][qk[k]];
+                    tq[k] = tcq.x;
+                    cq[k] = tcq.y;
+                    sq[k] = inner_st(tcq.x, (hm >> qk[k]) & 1u);
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) x[k][u] = S.A[o[k][u]];
+                }
+#pragma unroll
+                for (int k = 0; k < NB; ++k) {
+                    if (!live[k] || (tp == 0.0 && tq[k] == 0.0)) continue;
+                    const double y00 = fma(sq[k], x[k][1], x[k][0]) * cq[k];
+                    const double y01 = fma(tq[k], x[k][0], x[k][1]) * cq[k];
+                    const double y10 = fma(sq[k], x[k][3], x[k][2]) * cq[k];
+                    const double y11 = fma(tq[k], x[k][2], x[k][3]) * cq[k];
+                    S.A[o[k][0]] = fma(sp, y10, y00) * cp;
+                    S.A[o[k][3]] = fma(tp, y01, y11) * cp;
+                    if (dg[k]) {  // the pair itself: annihilated
+                        S.A[o[k][1]] = 0.0;
+                    } else {
+                        S.A[o[k][1]] = fma(sp, y11, y01) * cp;
+                        S.A[o[k][2]] = fma(tp, y00, y10) * cp;
+                    }
+                }
+            }
+            HSVD_STAMP(3)
+            named_bar_sync(1, NA);  // the round's updates are visible
+            HSVD_STAMP(4)
+        }
+#undef HSVD_STAMP
+    }
+    named_bar_sync(0, NT);
+    if (S.fail != kNoError) {
+        if (tid == 0) atomicMin(a.err, S.fail);
+        return;
+    }
+    // storage columns of the slot's 2b columns, for the update's prologue
+    if (tid < B2) a.colidx[(int64_t)slot * B2 + tid] = a.colmap[slot_pos(tid, b, I, J)];
+    if (tid == 0) {
+        if (a.trace && blockIdx.x == 0) a.trace[8 * 64 + 1] = clock64();
+        // touched columns (W == I outside T x T; T empty: k_update skips)
+        uint8_t *ts = a.tset + (int64_t)slot * kTsetStride;
+        unsigned long long m = S.touched;
+        int cnt = 0;
+        while (m) {
+            const int c = __ffsll((long long)m) - 1;
+            m &= m - 1;
+            ts[1 + cnt++] = (uint8_t)c;
+        }
+        ts[0] = (uint8_t)cnt;
+        // convergence code (_kernels.py:227-231 semantics per slot)
+        if (S.big) a.C[slot] = 3;
+        else if (S.rot) a.C[slot] |= 1;
+        a.rotk[slot] += S.rot;
+        a.skipk[slot] += S.skip;
+        const double mt = __longlong_as_double((long long)S.maxt_bits);
+        if (mt > a.maxt[slot]) a.maxt[slot] = mt;
+        if (a.ru.pairstamp) {
+            const uint32_t stamp = reuse_stamp(a.ru.dsweep, a.nb, a.step);
+            if (a.ru.dcache && !(a.skipf && a.skipf[slot] == kSlotCross)) {
+                // this visit folded both diagonal blocks fresh: cached as of now
+                a.ru.dstamp[I] = stamp;
+                a.ru.dstamp[J] = stamp;
+            }
+            if (S.touched) {
+                // the blocks' columns are rewritten by this step's update
+                a.ru.blkmod[I] = stamp;
+                a.ru.blkmod[J] = stamp;
+            } else if (!S.rot) {
+                // an all-skip visit: recorded for reuse
+                a.ru.pairstamp[I * a.nb + J] = stamp | ((uint32_t)FULL << 31);
+                a.ru.pairskip[I * a.nb + J] = S.skip;
+            }
+        }
+        inner_advance(a, slot, I, J);
+    }
+}

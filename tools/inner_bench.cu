@@ -105,15 +105,19 @@ int main(int argc, char **argv)
     CK(cudaMemset(dC, 0, nslots)); CK(cudaMemset(drot, 0, nslots * 4));
     CK(cudaMemset(dskip, 0, nslots * 4)); CK(cudaMemset(dmaxt, 0, nslots * 8));
     InnerArgs ia{};
-    ia.part.W = nslots; ia.part.P = nslots; ia.part.T = 1;
+    ia.part.T = 1; ia.part.L = 1; ia.part.NSEG = 1; ia.part.NS = nslots; ia.part.P = nslots;
     ia.maxseg = 1; ia.Apart = dA; ia.Wg = dW; ia.jsign = djs;
     ia.ip = dip; ia.jp = djp; ia.iblk = dib; ia.jblk = djb; ia.cur = dcur;
     ia.C = dC; ia.tset = dts; ia.rotk = drot; ia.skipk = dskip; ia.maxt = dmaxt; ia.err = derr;
     ia.nb = nb; ia.slot_base = 0; ia.eps = 0x1p-52; ia.teps = 0x1p-27;
     ia.full = full; ia.use_skip = 1; ia.passes = 1; ia.trace = nullptr;
     ia.colmap = dcolmap; ia.colidx = dcolidx;
+    ia.orig = dcolmap; ia.real_cols = r; ia.skipf = nullptr;
     const size_t smem = sizeof(InnerSmem<B2>), smem_reg = sizeof(InnerRegSmem);
-    CK(cudaFuncSetAttribute(k_inner<B2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const size_t smem2 = sizeof(InnerSmem2<B2>);
+    CK(cudaFuncSetAttribute(k_inner<B2, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+    CK(cudaFuncSetAttribute(k_inner<B2, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+    CK(cudaFuncSetAttribute(k_inner_v1<B2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CK(cudaFuncSetAttribute(k_inner_reg<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_reg));
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0); cudaEventCreate(&e1);
@@ -127,14 +131,16 @@ int main(int argc, char **argv)
         cudaMemset(dW, 0, A.size() * 8);
     };
     auto launch = [&](int kind) {
-        if (kind == 0) k_inner<B2, true><<<nslots, inner_threads<B2>(), smem>>>(ia);
+        if (kind == 0 && full) k_inner<B2, true, true><<<nslots, inner2_threads<B2>(), smem2>>>(ia);
+        else if (kind == 0) k_inner<B2, true, false><<<nslots, inner2_threads<B2>(), smem2>>>(ia);
+        else if (kind == 1) k_inner_v1<B2, true><<<nslots, inner_threads<B2>(), smem>>>(ia);
         else k_inner_reg<true><<<nslots, 256, smem_reg>>>(ia);
     };
     const int rounds = full ? B2 - 1 : b;
-    std::vector<double> Wk[2];
-    std::vector<uint32_t> rotk[2];
-    std::vector<uint8_t> tsk[2];
-    for (int kind = 0; kind < (full ? 2 : 1); ++kind) {
+    std::vector<double> Wk[3];
+    std::vector<uint32_t> rotk[3];
+    std::vector<uint8_t> tsk[3];
+    for (int kind = 0; kind < (full ? 3 : 2); ++kind) {
         ia.trace = nullptr;
         for (int w = 0; w < 3; ++w) { reset(); launch(kind); }
         CK(cudaDeviceSynchronize());
@@ -147,7 +153,7 @@ int main(int argc, char **argv)
             cudaEventSynchronize(e1);
             float ms; cudaEventElapsedTime(&ms, e0, e1); tot += ms;
         }
-        printf("%s nslots=%d full=%d jmode=%d: %.2f us per launch\n", kind ? "k_inner_reg" : "k_inner<64>",
+        printf("%s nslots=%d full=%d jmode=%d: %.2f us per launch\n", kind == 2 ? "k_inner_reg" : kind ? "k_inner_v1<64>" : "k_inner<64>",
                nslots, full, jmode, 1e3 * tot / iters);
         Wk[kind].resize(A.size());
         rotk[kind].resize(nslots);
@@ -172,20 +178,46 @@ int main(int argc, char **argv)
         printf("  avg cycles per round: phases %.0f / %.0f / %.0f / %.0f; total round %.0f\n",
                sum[0] / rounds, sum[1] / rounds, sum[2] / rounds, sum[3] / rounds,
                (double)(tr[8 * (rounds - 1) + 4] - tr[0]) / rounds);
+        if (kind == 0) {
+            double s5 = 0;
+            for (int it = 0; it < rounds; ++it) s5 += tr[8 * it + 5] - tr[8 * it];
+            printf("  k_inner: round start -> rotation inputs loaded and skip-tested %.0f cycles\n", s5 / rounds);
+        }
+        if (kind == 0)
+            printf("  k_inner CTA 0: A chain done %lld cycles after round 0, W replay done %lld, epilogue %lld\n",
+                   tr[8 * (rounds - 1) + 4] - tr[0], tr[8 * 64] - tr[0], tr[8 * 64 + 1] - tr[0]);
     }
-    if (full) {
-        size_t diff = 0;
+    // pairwise comparison of the kernels' W, rotation counts and touched sets
+    auto cmp = [&](int x, int y, const char *what) {
+        size_t diff = 0, rdiff = 0, tdiff = 0;
         double maxd = 0;
         for (size_t e = 0; e < A.size(); ++e)
-            if (Wk[0][e] != Wk[1][e]) {
+            if (Wk[x][e] != Wk[y][e]) {
                 ++diff;
-                maxd = fmax(maxd, fabs(Wk[0][e] - Wk[1][e]));
+                maxd = fmax(maxd, fabs(Wk[x][e] - Wk[y][e]));
             }
-        size_t rdiff = 0, tdiff = 0;
-        for (int k = 0; k < nslots; ++k) rdiff += rotk[0][k] != rotk[1][k];
-        for (size_t e = 0; e < tsk[0].size(); ++e) tdiff += tsk[0][e] != tsk[1][e];
-        printf("reg vs smem kernel: W entries differing %zu of %zu (max |diff| %.3e), rot counts differing %zu, tset bytes differing %zu\n",
-               diff, A.size(), maxd, rdiff, tdiff);
+        for (int k = 0; k < nslots; ++k) rdiff += rotk[x][k] != rotk[y][k];
+        for (size_t e = 0; e < tsk[x].size(); ++e) tdiff += tsk[x][e] != tsk[y][e];
+        printf("%s: W entries differing %zu of %zu (max |diff| %.3e), rot counts differing %zu, tset bytes differing %zu\n",
+               what, diff, A.size(), maxd, rdiff, tdiff);
+    };
+    cmp(0, 1, "k_inner vs k_inner_v1");
+    if (full) cmp(1, 2, "k_inner_v1 vs k_inner_reg");
+    {
+        // W J-orthogonality of the new kernel: W^T J_P W = J_P (per slot)
+        double worst = 0;
+        for (int s = 0; s < nslots; ++s) {
+            const double *Wm = &Wk[0][(size_t)s * B2 * B2];  // column-major
+            const int64_t I = ib[s] < jb[s] ? ib[s] : jb[s], Jb = ib[s] < jb[s] ? jb[s] : ib[s];
+            auto sg = [&](int c) { return (double)js[c < b ? I * b + c : Jb * b + (c - b)]; };
+            for (int i = 0; i < B2; ++i)
+                for (int j = 0; j < B2; ++j) {
+                    double acc = 0;
+                    for (int k = 0; k < B2; ++k) acc += Wm[i * B2 + k] * sg(k) * Wm[j * B2 + k];
+                    worst = fmax(worst, fabs(acc - (i == j ? sg(i) : 0.0)));
+                }
+        }
+        printf("k_inner: max |W^T J W - J| = %.3e\n", worst);
     }
     {
         double *o; long long *cy, h;

@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_inner_reg(InnerArgs a)
     // A = sum of the slot's partial segments in segment order (as k_inner)
     {
         const double *P0 = a.Apart + (int64_t)slot * a.maxseg * (B2 * B2);
-        const int nseg = (int)a.part.nseg(slot);
+        const int nseg = (int)a.part.NSEG;
         constexpr int PER = B2 * B2 / kThreads;
         double v[PER];
 #pragma unroll
