@@ -39,22 +39,25 @@
 #ifndef HSVD_INNER_DIAG_NOUPD
 #define HSVD_INNER_DIAG_NOUPD 0
 #endif
-#ifndef HSVD_INNER_AWARPS64
-#define HSVD_INNER_AWARPS64 6  // A warps at b = 32 (+ 2 W warps: 8 warps, 255 registers)
+#ifndef HSVD_INNER_BWARPS64
+#define HSVD_INNER_BWARPS64 5  // bulk warps at b = 32 (+ leader + 2 W warps: 8 warps, 255 registers)
 #endif
 
 template <int B2>
 struct InnerCfg {
     static constexpr int b = B2 / 2;
-    static constexpr int NAW = B2 == 64 ? HSVD_INNER_AWARPS64 : 4;  // A warps
-    static constexpr int NA = NAW * 32;                            // A threads
+    static constexpr int NBW = B2 == 64 ? HSVD_INNER_BWARPS64 : 3;  // bulk warps
+    static constexpr int NBT = NBW * 32;                           // bulk threads
+    static constexpr int NAW = 1 + NBW;                            // leader + bulk ("A side")
+    static constexpr int NA = NAW * 32;
     static constexpr int NWW = B2 / 32;                            // W warps: a row per thread
     static constexpr int NT = NA + NWW * 32;
     static constexpr int LDA = B2;
-    // upper blocks (p, p + d): d = 0..b/2-1 for every p, d = b/2 for p < b/2
-    static constexpr int NBLK = b * (b / 2) + b / 2;
-    static constexpr int NB = (NBLK + NA - 1) / NA;  // blocks per A thread (at most)
-    static_assert(NA % b == 0, "k_inner: A warp count");
+    // bulk block slots: thread (g, p) of the bulk owns blocks (p, p + d),
+    // d = g + G k; d < b/2 for every p, d = b/2 for p < b/2
+    static constexpr int G = NBT / b;
+    static constexpr int NB = (b / 2 + G) / G;
+    static_assert(NBT % b == 0, "k_inner: bulk warp count");
     // full ordering: 2b-1 rounds, cyclic over M = 2b-1 positions; U rounds
     // are renamed in registers between row shifts (U divides the rounds)
     static constexpr int M = B2 - 1;
@@ -64,9 +67,11 @@ struct InnerCfg {
 
 template <int B2>
 struct InnerSmem2 {
-    double A[B2 * B2];               // upper triangle, [min][max], ld B2
+    double A[2][B2 * B2];            // two copies (round k reads one, writes the other);
+                                     // upper triangle, [min][max], ld B2
     double2 ltc[B2][B2 / 2];         // rotation log of the pass: (t, c) per round and pair
     unsigned long long full[B2];     // mbarrier per round: the log entry is published
+    unsigned long long done[2];      // mbarrier by round parity: the bulk finished a round
     unsigned long long wdone;        // W warps have replayed a whole pass
     int lflag[B2];                   // bit 0: some pair rotated, bit 1: a pair failed
     unsigned int lact[B2];           // per round: the pairs that rotated (bit x: pair x)
@@ -117,6 +122,64 @@ __device__ __forceinline__ void inner_cols(int x, int rd, int &ci, int &cj)
         ci = x;
         cj = v + b;
     }
+}
+
+// pair of column c in round rd and its role (false: the pair's first
+// column ci, true: its second cj); inverse of inner_cols
+template <int B2, bool FULL>
+__device__ __forceinline__ void inner_pair_of(int c, int rd, int &x, bool &isj)
+{
+    constexpr int b = B2 / 2;
+    if (FULL) {
+        constexpr int m = B2 - 1;
+        int u = c - rd;
+        u = u < 0 ? u + m : u;
+        x = c == m ? 0 : (u == 0 ? 0 : (u < b ? u : m - u));
+        isj = c != m && (u == 0 || u >= b);
+    } else {
+        int y = c - b - rd;
+        y = y < 0 ? y + b : y;
+        x = c < b ? c : y;
+        isj = c >= b;
+    }
+}
+
+// Entries of S_k = R^T S_{k-1} R (round k's congruence, pairing rd) from
+// S_{k-1} in Ab, with the bulk's formulas and operation order (so the same
+// bits).  Diagonal entry of the pair's column ci (isj false) or cj:
+template <int B2, bool FULL>
+__device__ __forceinline__ double inner_diag_after(const double *Ab, int P, bool isj, int rd,
+                                                   double t, double c, double st)
+{
+    constexpr int LDA = B2;
+    int iP, jP;
+    inner_cols<B2, FULL>(P, rd, iP, jP);
+    const double a_ii = Ab[iP * (LDA + 1)], a_jj = Ab[jP * (LDA + 1)],
+                 a_ij = Ab[min(iP, jP) * LDA + max(iP, jP)];
+    const double ya = isj ? fma(t, a_ii, a_ij) * c : fma(st, a_ij, a_ii) * c;  // y01 / y00
+    const double yb = isj ? fma(t, a_ij, a_jj) * c : fma(st, a_jj, a_ij) * c;  // y11 / y10
+    const double v = isj ? fma(t, ya, yb) * c : fma(st, yb, ya) * c;
+    return t == 0.0 ? (isj ? a_jj : a_ii) : v;  // a skipped pair's block is copied
+}
+// off-diagonal entry of block (p, q) (rows of pair p, columns of pair q): the
+// row member of p with role rpj and the column member of q with role rqj
+template <int B2, bool FULL>
+__device__ __forceinline__ double inner_off_after(const double *Ab, int p, int q, bool rpj, bool rqj,
+                                                  int rd, double tp, double cp, double sp,
+                                                  double tq, double cq, double sq)
+{
+    constexpr int LDA = B2;
+    int ip, jp, iq, jq;
+    inner_cols<B2, FULL>(p, rd, ip, jp);
+    inner_cols<B2, FULL>(q, rd, iq, jq);
+    const double x0 = Ab[min(ip, iq) * LDA + max(ip, iq)], x1 = Ab[min(ip, jq) * LDA + max(ip, jq)];
+    const double x2 = Ab[min(jp, iq) * LDA + max(jp, iq)], x3 = Ab[min(jp, jq) * LDA + max(jp, jq)];
+    // column step (R_q) on the needed column, then the row step (R_p)
+    const double ya = rqj ? fma(tq, x0, x1) * cq : fma(sq, x1, x0) * cq;  // y01 / y00
+    const double yb = rqj ? fma(tq, x2, x3) * cq : fma(sq, x3, x2) * cq;  // y11 / y10
+    const double v = rpj ? fma(tp, ya, yb) * cp : fma(sp, yb, ya) * cp;
+    const double xo = rpj ? (rqj ? x3 : x2) : (rqj ? x1 : x0);
+    return (tp == 0.0 && tq == 0.0) ? xo : v;  // both pairs skipped: copied
 }
 
 // register of position p after S renamed rounds
@@ -237,6 +300,72 @@ __device__ __forceinline__ bool inner_w_replay(double (&w)[B2], const InnerSmem2
     return true;
 }
 
+// A_P = sum of the slot's partial Gram segments in segment order (the upper
+// triangle; the same additions in the same order as a one-element-per-thread
+// fold, so the same bits).  Every thread of the CTA takes part: chunks of two
+// adjacent row entries are read 16 bytes at a time, four segments in flight.
+template <int B2>
+__device__ __forceinline__ void inner_fold(const InnerArgs &a, double *A, int slot, int64_t I,
+                                           int64_t J, int tid)
+{
+    using C = InnerCfg<B2>;
+    constexpr int NT = C::NT, LDA = B2, b = B2 / 2;
+    constexpr int NCHUNK = B2 * B2 / 2, PER = (NCHUNK + NT - 1) / NT, BATCH = 4;
+    const double2 *P0 = reinterpret_cast<const double2 *>(a.Apart + (int64_t)slot * a.maxseg * (B2 * B2));
+    const int nseg = (int)a.part.NSEG;
+    // cross class: the two diagonal blocks come from the cache, only the
+    // cross block from the partials (the same segment folds as a fresh
+    // visit, so the same bits)
+    const bool cross = a.skipf && a.skipf[slot] == kSlotCross;
+    bool need[PER];
+    double2 v[PER];
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+        const int ch = tid + k * NT, i = ch / (B2 / 2), j0 = 2 * (ch % (B2 / 2));
+        need[k] = ch < NCHUNK && j0 + 1 >= i && (!cross || (i < b && j0 >= b));
+        v[k] = make_double2(0.0, 0.0);
+    }
+    for (int s0 = 0; s0 < nseg; s0 += BATCH) {
+        double2 x[BATCH][PER];
+#pragma unroll
+        for (int u = 0; u < BATCH; ++u)
+#pragma unroll
+            for (int k = 0; k < PER; ++k)
+                x[u][k] = (s0 + u < nseg && need[k])
+                              ? P0[(int64_t)(s0 + u) * (NCHUNK) + tid + k * NT]
+                              : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int u = 0; u < BATCH; ++u)
+#pragma unroll
+            for (int k = 0; k < PER; ++k)
+                if (s0 + u < nseg) {
+                    v[k].x += x[u][k].x;
+                    v[k].y += x[u][k].y;
+                }
+    }
+    const bool cache = a.ru.dcache != nullptr;
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+        const int ch = tid + k * NT, i = ch / (B2 / 2), j0 = 2 * (ch % (B2 / 2));
+        if (ch >= NCHUNK) continue;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int j = j0 + h;
+            if (i > j) continue;
+            double val = h ? v[k].y : v[k].x;
+            const bool dI = j < b, dJ = i >= b;  // inside a diagonal block
+            if (cross && (dI || dJ)) {
+                val = dI ? a.ru.dcache[(I * b + i) * b + j]
+                         : a.ru.dcache[(J * b + (i - b)) * b + (j - b)];
+            } else if (cache && !cross && (dI || dJ)) {
+                if (dI) a.ru.dcache[(I * b + i) * b + j] = val;
+                else a.ru.dcache[(J * b + (i - b)) * b + (j - b)] = val;
+            }
+            A[i * LDA + j] = val;
+        }
+    }
+}
+
 template <int B2, bool FAST, bool FULL>
 __global__ void __launch_bounds__(inner2_threads<B2>()) k_inner(InnerArgs a)
 {
@@ -245,6 +374,7 @@ __global__ void __launch_bounds__(inner2_threads<B2>()) k_inner(InnerArgs a)
     constexpr int rounds = FULL ? B2 - 1 : b;
     extern __shared__ __align__(16) unsigned char ism_raw[];
     auto &S = *reinterpret_cast<InnerSmem2<B2> *>(ism_raw);
+    const long long t_entry = clock64();
     if (*(volatile unsigned long long *)a.err != kNoError) return;
     const int slot = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     int64_t I = a.iblk[slot], J = a.jblk[slot];
@@ -261,7 +391,15 @@ __global__ void __launch_bounds__(inner2_threads<B2>()) k_inner(InnerArgs a)
     }
     const unsigned full0 = (unsigned)__cvta_generic_to_shared(&S.full[0]);
     const unsigned wdone = (unsigned)__cvta_generic_to_shared(&S.wdone);
+    const unsigned done0 = (unsigned)__cvta_generic_to_shared(&S.done[0]);
+    // roles: warp 0 leads, warps 1..NBW bulk, then the W warps (the bulk is
+    // spread over all four SM sub-partitions: measured faster than keeping
+    // the leader's sub-partition free of bulk warps)
     const bool wwarp = warp >= C::NAW;
+    const int arank = warp;  // rank among leader + bulk warps
+    const int atid = arank * 32 + lane;
+
+    inner_fold<B2>(a, S.A[0], slot, I, J, tid);
 
     if (wwarp) {
         // ---- W warps: their own code path (barrier 0 is shared with the A
@@ -297,53 +435,6 @@ __global__ void __launch_bounds__(inner2_threads<B2>()) k_inner(InnerArgs a)
     }
 
     {
-        // A = sum of the slot's partial segments in segment order (upper
-        // triangle, coalesced); all loads of a batch of segments are issued
-        // before the sums
-        const double *P0 = a.Apart + (int64_t)slot * a.maxseg * (B2 * B2);
-        const int nseg = (int)a.part.NSEG;
-        constexpr int PER = (B2 * B2 + NA - 1) / NA;
-        // cross class: the two diagonal blocks come from the cache, only the
-        // cross block from the partials (the same segment folds as a fresh
-        // visit, so the same bits)
-        const bool cross = a.skipf && a.skipf[slot] == kSlotCross;
-        double v[PER];
-#pragma unroll
-        for (int k = 0; k < PER; ++k) v[k] = 0.0;
-        constexpr int BATCH = 2;
-        for (int s0 = 0; s0 < nseg; s0 += BATCH) {
-            double x[BATCH][PER];
-#pragma unroll
-            for (int u = 0; u < BATCH; ++u)
-#pragma unroll
-                for (int k = 0; k < PER; ++k) {
-                    const int e = tid + k * NA, i = e / B2, j = e % B2;
-                    x[u][k] = (s0 + u < nseg && e < B2 * B2 && i <= j &&
-                               (!cross || (i < b && j >= b)))
-                                  ? P0[(int64_t)(s0 + u) * B2 * B2 + e] : 0.0;
-                }
-#pragma unroll
-            for (int u = 0; u < BATCH; ++u)
-#pragma unroll
-                for (int k = 0; k < PER; ++k)
-                    if (s0 + u < nseg) v[k] += x[u][k];
-        }
-        const bool cache = a.ru.dcache != nullptr;
-#pragma unroll
-        for (int k = 0; k < PER; ++k) {
-            const int e = tid + k * NA, i = e / B2, j = e % B2;
-            if (e < B2 * B2 && i <= j) {
-                const bool dI = j < b, dJ = i >= b;  // inside a diagonal block
-                if (cross && (dI || dJ)) {
-                    v[k] = dI ? a.ru.dcache[(I * b + i) * b + j]
-                              : a.ru.dcache[(J * b + (i - b)) * b + (j - b)];
-                } else if (cache && !cross && (dI || dJ)) {
-                    if (dI) a.ru.dcache[(I * b + i) * b + j] = v[k];
-                    else a.ru.dcache[(J * b + (i - b)) * b + (j - b)] = v[k];
-                }
-                S.A[i * LDA + j] = v[k];
-            }
-        }
         if (tid < B2) {
             const int64_t pos = slot_pos(tid, b, I, J);
             const int neg = a.jsign[pos] < 0;
@@ -361,22 +452,133 @@ __global__ void __launch_bounds__(inner2_threads<B2>()) k_inner(InnerArgs a)
             S.fail = kNoError;
             S.touched = 0;
             for (int k = 0; k < rounds; ++k) mbar_init(full0 + 8 * k, 32);
+            mbar_init(done0, C::NBT);
+            mbar_init(done0 + 8, C::NBT);
             mbar_init(wdone, C::NWW * 32);
             asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
         }
     }
     named_bar_sync(0, NT);
+    if (a.trace && blockIdx.x == 0 && tid == 0) {
+        a.trace[8 * 64 + 2] = t_entry;
+        a.trace[8 * 64 + 3] = clock64();
+    }
 
-    {
+    const int total = rounds * a.passes;
+    long long *tr = (a.trace && blockIdx.x == 0 && tid == 0) ? a.trace : nullptr;
+#define HSVD_STAMP(k) \
+    if (tr && it < 64) tr[8 * it + (k)] = clock64();
+    if (warp == 0) {
+        // ---- leader: forms round it's b rotations while the bulk applies
+        // round it-1.  Its pivots are entries of S_{it-1} = R^T S_{it-2} R
+        // (round it-1's congruence): lane x recomputes its three from
+        // S_{it-2} (complete once the bulk finished round it-2) with exactly
+        // the bulk's block formulas and orientation, so they are the bits
+        // the bulk writes
         const unsigned long long jneg =
             B2 == 64 ? ((unsigned long long)S.jneg[1] << 32) | S.jneg[0] : S.jneg[0];
-        // block assignment: thread (group g = tid / b, pair p = tid % b)
-        // owns blocks (p, p + d), d = g + G k: d < b/2 for every p, d = b/2
-        // for p < b/2 (the rest of the upper triangle's blocks), larger d
-        // are dead slots.  p is the same in every slot: its rotation is
-        // loaded once per round
-        constexpr int G = NA / b, NB = (b / 2 + G) / G;
-        const int pk = tid % b, g = tid / b;
+        const int q = lane % b;  // pair owned by this lane
+        double tprev = 0.0, cprev = 1.0;
+        unsigned hprev = 0, vprev = 0;  // previous round: hyperbolic / active masks
+        int lb = 0;  // buffer holding S_{it-2}
+        int rd = 0, rdp = 0;
+        for (int it = 0; it < total; ++it, rdp = rd, rd = rd + 1 == rounds ? 0 : rd + 1) {
+            HSVD_STAMP(0)
+            if (it > 0 && rd == 0) {
+                // pass boundary (passes > 1): the W warps must have replayed
+                // the previous pass before its log is overwritten
+                mbar_wait(wdone, (unsigned)((it / rounds) & 1) ^ 1u);
+            }
+            if (it >= 2) mbar_wait(done0 + 8 * (it & 1), (unsigned)((it - 2) >> 1) & 1u);
+            const double *Ab = S.A[lb];
+            int i, j;
+            inner_cols<B2, FULL>(q, rd, i, j);
+            const int lo = i < j ? i : j, hi = i < j ? j : i;
+            double a_ii, a_jj, a_ij;
+            if (it == 0 || vprev == 0) {
+                // S_{it-1} = S_{it-2}: the buffer holds the pivots
+                a_ii = Ab[i * (LDA + 1)];
+                a_jj = Ab[j * (LDA + 1)];
+                a_ij = Ab[lo * LDA + hi];
+            } else {
+                // pairs of i and j in round it-1 (rdp) and their rotations
+                int pi, pj;
+                bool ri, rj;  // column is the pair's second ("j") member
+                inner_pair_of<B2, FULL>(i, rdp, pi, ri);
+                inner_pair_of<B2, FULL>(j, rdp, pj, rj);
+                const double ti = __shfl_sync(0xffffffffu, tprev, pi),
+                             ci = __shfl_sync(0xffffffffu, cprev, pi);
+                const double tj = __shfl_sync(0xffffffffu, tprev, pj),
+                             cj = __shfl_sync(0xffffffffu, cprev, pj);
+                const double si = inner_st(ti, (hprev >> pi) & 1u),
+                             sj = inner_st(tj, (hprev >> pj) & 1u);
+                a_ii = inner_diag_after<B2, FULL>(Ab, pi, ri, rdp, ti, ci, si);
+                a_jj = inner_diag_after<B2, FULL>(Ab, pj, rj, rdp, tj, cj, sj);
+                // (i, j) lies in the off-diagonal block of pairs pi, pj; the
+                // bulk rotates it as rows of p, columns of q with
+                // q = p + d (mod b), d <= b/2 (d = b/2 only for p < b/2)
+                const int d1 = (pj - pi + b) % b;
+                const bool iprow = d1 < b / 2 || (d1 == b / 2 && pi < b / 2);
+                a_ij = iprow ? inner_off_after<B2, FULL>(Ab, pi, pj, ri, rj, rdp, ti, ci, si, tj, cj, sj)
+                             : inner_off_after<B2, FULL>(Ab, pj, pi, rj, ri, rdp, tj, cj, sj, ti, ci, si);
+            }
+            // relative-orthogonality skip |a_ij| < eps sqrt(a_ii a_jj)
+            // (_kernels.py:211), squared: no square root on the chain; the
+            // rotation is formed beside the test (a_ij = 0 gives the
+            // identity) and selected.  The pair is rotated in its schedule
+            // orientation (i, j): the closed forms are odd (trig) or
+            // symmetric (hyperbolic) in the roles, so this is the sorted
+            // form's transformation except at zeta = 0
+            const bool skip = a_ij == 0.0 ||
+                              (a.use_skip && a_ij * a_ij < (a.eps * a.eps) * (a_ii * a_jj));
+            HSVD_STAMP(5)
+            const int hyp = (((jneg >> i) ^ (jneg >> j)) & 1) ? 1 : -1;
+            double t, c;
+            const int status = FAST ? rotation_fast(a_ii, a_jj, a_ij, hyp, t, c)
+                                    : rotation_tc(a_ii, a_jj, a_ij, hyp, t, c);
+            const bool bad = !skip && status != 0, act = !skip && status == 0;
+            t = act ? t : 0.0;
+            c = act ? c : 1.0;
+            HSVD_STAMP(1)
+            if (lane < b) S.ltc[rd][q] = make_double2(t, c);
+            const unsigned va = __ballot_sync(0xffffffffu, act),
+                           vb = __ballot_sync(0xffffffffu, bad),
+                           vh = __ballot_sync(0xffffffffu, hyp > 0);
+            if (lane == 0) {
+                S.lflag[rd] = (va ? 1 : 0) | (vb ? 2 : 0);
+                S.lact[rd] = va;
+                S.lhyp[rd] = vh;
+            }
+            if (bad && lane < b)
+                atomicMin(&S.fail, pack_err(a.slot_base + slot, slot_pos(lo, b, I, J),
+                                            slot_pos(hi, b, I, J)));
+            if (vb) {
+                // the other warps wait round by round: publish the rest of
+                // the pass as failed so none of them waits forever
+                for (int r2 = rd + 1; r2 < rounds; ++r2) {
+                    if (lane == 0) S.lflag[r2] = 2;
+                    mbar_arrive(full0 + 8 * r2);
+                }
+            }
+            mbar_arrive(full0 + 8 * rd);  // release: the round's log entry
+            HSVD_STAMP(2)
+            if (vb) break;
+            // the bulk writes S_{it} over the buffer of S_{it-2} once round
+            // it-1 has rotated (else the buffers do not move)
+            if (it > 0 && vprev) lb ^= 1;
+            tprev = t;
+            cprev = c;
+            hprev = vh;
+            vprev = va;
+        }
+    } else {
+        // ---- bulk: round it's congruence on the upper blocks, buffer cb to
+        // cb ^ 1.  Thread (group g, pair p) owns blocks (p, p + d), d = g + G k
+        // (the rest of the upper triangle's blocks), larger d are dead slots;
+        // p is the same in every slot
+        constexpr int G = C::G, NB = C::NB;
+        const int bt = atid - 32;
+        const int pk = bt % b, g = bt / b;
         int qk[NB];
         bool dg[NB], live[NB];
 #pragma unroll
@@ -386,78 +588,23 @@ __global__ void __launch_bounds__(inner2_threads<B2>()) k_inner(InnerArgs a)
             qk[k] = (pk + (live[k] ? d : 0)) % b;  // dead slots reload block (p, p)
             dg[k] = qk[k] == pk;
         }
-        const int q = lane % b;  // warp 0: pair owned by this lane
-        long long *tr = (a.trace && blockIdx.x == 0 && tid == 0) ? a.trace : nullptr;
-#define HSVD_STAMP(k) \
-    if (tr && it < 64) tr[8 * it + (k)] = clock64();
+        int cb = 0;  // buffer holding S_{it-1}
         int rd = 0;
-        const int total = rounds * a.passes;
+        long long *btr = (a.trace && blockIdx.x == 0 && tid == 32) ? a.trace + 1024 : nullptr;
         for (int it = 0; it < total; ++it, rd = rd + 1 == rounds ? 0 : rd + 1) {
-            HSVD_STAMP(0)
-            if (it > 0 && rd == 0) {
-                // pass boundary (passes > 1): the W warps must have replayed
-                // the previous pass before its log is overwritten
-                if (warp == 0) mbar_wait(wdone, (unsigned)((it / rounds) & 1) ^ 1u);
-            }
-            if (warp == 0) {
-                // ---- the round's b rotations.  The pair is rotated in its
-                // schedule orientation (i, j): the closed forms are odd
-                // (trig) or symmetric (hyperbolic) in the roles, so this is
-                // the sorted form's transformation except at zeta = 0
-                int i, j;
-                inner_cols<B2, FULL>(q, rd, i, j);
-                const int lo = i < j ? i : j, hi = i < j ? j : i;
-                const double a_ii = S.A[i * (LDA + 1)], a_jj = S.A[j * (LDA + 1)],
-                             a_ij = S.A[lo * LDA + hi];
-                // relative-orthogonality skip |a_ij| < eps sqrt(a_ii a_jj)
-                // (_kernels.py:211), squared: no square root on the chain;
-                // the rotation is formed beside the test (a_ij = 0 gives the
-                // identity) and selected
-                const bool skip = a_ij == 0.0 ||
-                                  (a.use_skip && a_ij * a_ij < (a.eps * a.eps) * (a_ii * a_jj));
-                HSVD_STAMP(5)
-                const int hyp = (((jneg >> i) ^ (jneg >> j)) & 1) ? 1 : -1;
-                double t, c;
-                const int status = FAST ? rotation_fast(a_ii, a_jj, a_ij, hyp, t, c)
-                                        : rotation_tc(a_ii, a_jj, a_ij, hyp, t, c);
-                const bool bad = !skip && status != 0, act = !skip && status == 0;
-                t = act ? t : 0.0;
-                c = act ? c : 1.0;
-                HSVD_STAMP(1)
-                if (lane < b) S.ltc[rd][q] = make_double2(t, c);
-                const unsigned va = __ballot_sync(0xffffffffu, act),
-                               vb = __ballot_sync(0xffffffffu, bad),
-                               vh = __ballot_sync(0xffffffffu, hyp > 0);
-                if (lane == 0) {
-                    S.lflag[rd] = (va ? 1 : 0) | (vb ? 2 : 0);
-                    S.lact[rd] = va;
-                    S.lhyp[rd] = vh;
-                }
-                if (bad && lane < b)
-                    atomicMin(&S.fail, pack_err(a.slot_base + slot, slot_pos(lo, b, I, J),
-                                                slot_pos(hi, b, I, J)));
-                if (vb) {
-                    // the W warps wait round by round: publish the rest of
-                    // the pass as failed so none of them waits forever
-                    for (int r2 = rd + 1; r2 < rounds; ++r2) {
-                        if (lane == 0) S.lflag[r2] = 2;
-                        mbar_arrive(full0 + 8 * r2);
-                    }
-                }
-                mbar_arrive(full0 + 8 * rd);  // release to the W warps
-            }
-            named_bar_sync(2, NA);  // the round's rotations are published (A warps)
-            HSVD_STAMP(2)
+            if (btr && it < 64) btr[8 * it] = clock64();
+            mbar_wait(full0 + 8 * rd, (unsigned)((it / rounds) & 1));
+            if (btr && it < 64) btr[8 * it + 1] = clock64();
+            // S_{it-1} complete: every bulk thread finished round it-1
+            if (it >= 1) mbar_wait(done0 + 8 * ((it - 1) & 1), (unsigned)((it - 1) >> 1) & 1u);
+            if (btr && it < 64) btr[8 * it + 2] = clock64();
             const int f = S.lflag[rd];
             if (f & 2) break;
-            if (!(f & 1)) continue;
-#if HSVD_INNER_DIAG_NOUPD  // diagnostics only (wrong A): no block updates
-            if (1) { HSVD_STAMP(3) named_bar_sync(1, NA); HSVD_STAMP(4) continue; }
-#endif
-            // ---- blocks (p, q) of the upper triangle: rows of pair p,
-            // columns of pair q; X' = R_p^T X R_q.  Offsets first, then every
-            // load, then the arithmetic and the stores.
-            {
+            if (f & 1) {
+                // X' = R_p^T X R_q per block (rows of pair p, columns of pair
+                // q); blocks whose two pairs both skipped are copied through
+                const double *Ar = S.A[cb];
+                double *Aw = S.A[cb ^ 1];
                 const unsigned hm = S.lhyp[rd];
                 int ip, jp;
                 inner_cols<B2, FULL>(pk, rd, ip, jp);
@@ -479,32 +626,37 @@ __global__ void __launch_bounds__(inner2_threads<B2>()) k_inner(InnerArgs a)
                     tq[k] = tcq.x;
                     cq[k] = tcq.y;
                     sq[k] = inner_st(tcq.x, (hm >> qk[k]) & 1u);
+                    if (live[k]) {
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) x[k][u] = S.A[o[k][u]];
+                        for (int u = 0; u < 4; ++u) x[k][u] = Ar[o[k][u]];
+                    }
                 }
 #pragma unroll
                 for (int k = 0; k < NB; ++k) {
-                    if (!live[k] || (tp == 0.0 && tq[k] == 0.0)) continue;
-                    const double y00 = fma(sq[k], x[k][1], x[k][0]) * cq[k];
-                    const double y01 = fma(tq[k], x[k][0], x[k][1]) * cq[k];
-                    const double y10 = fma(sq[k], x[k][3], x[k][2]) * cq[k];
-                    const double y11 = fma(tq[k], x[k][2], x[k][3]) * cq[k];
-                    S.A[o[k][0]] = fma(sp, y10, y00) * cp;
-                    S.A[o[k][3]] = fma(tp, y01, y11) * cp;
-                    if (dg[k]) {  // the pair itself: annihilated
-                        S.A[o[k][1]] = 0.0;
-                    } else {
-                        S.A[o[k][1]] = fma(sp, y11, y01) * cp;
-                        S.A[o[k][2]] = fma(tp, y00, y10) * cp;
+                    if (!live[k]) continue;
+                    double n0 = x[k][0], n1 = x[k][1], n2 = x[k][2], n3 = x[k][3];
+                    if (!(tp == 0.0 && tq[k] == 0.0)) {
+                        const double y00 = fma(sq[k], x[k][1], x[k][0]) * cq[k];
+                        const double y01 = fma(tq[k], x[k][0], x[k][1]) * cq[k];
+                        const double y10 = fma(sq[k], x[k][3], x[k][2]) * cq[k];
+                        const double y11 = fma(tq[k], x[k][2], x[k][3]) * cq[k];
+                        n0 = fma(sp, y10, y00) * cp;
+                        n3 = fma(tp, y01, y11) * cp;
+                        n1 = dg[k] ? 0.0 : fma(sp, y11, y01) * cp;  // the pair itself: annihilated
+                        n2 = fma(tp, y00, y10) * cp;
                     }
+                    Aw[o[k][0]] = n0;
+                    Aw[o[k][3]] = n3;
+                    Aw[o[k][1]] = n1;
+                    if (!dg[k]) Aw[o[k][2]] = n2;
                 }
+                cb ^= 1;
             }
-            HSVD_STAMP(3)
-            named_bar_sync(1, NA);  // the round's updates are visible
-            HSVD_STAMP(4)
+            if (btr && it < 64) btr[8 * it + 3] = clock64();
+            mbar_arrive(done0 + 8 * (it & 1));  // release: this thread's part of S_it
         }
-#undef HSVD_STAMP
     }
+#undef HSVD_STAMP
     named_bar_sync(0, NT);
     if (S.fail != kNoError) {
         if (tid == 0) atomicMin(a.err, S.fail);

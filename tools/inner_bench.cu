@@ -57,6 +57,7 @@ int main(int argc, char **argv)
     const int full = argc > 2 ? atoi(argv[2]) : 1;
     const int iters = argc > 3 ? atoi(argv[3]) : 20;
     const int jmode = argc > 4 ? atoi(argv[4]) : 0;  // 0: mixed signs, 1: all +1
+    const int nseg = argc > 5 ? atoi(argv[5]) : 1;   // Gram segments folded per slot (product: 16)
     const int nb = 2 * nslots, r = nb * b, K = 256;
     std::mt19937_64 rng(1);
     std::normal_distribution<double> N01;
@@ -80,7 +81,8 @@ int main(int argc, char **argv)
     uint32_t *drot, *dskip;
     unsigned long long *derr;
     long long *dtrace;
-    CK(cudaMalloc(&dA, A.size() * 8));
+    CK(cudaMalloc(&dA, A.size() * 8 * nseg));
+    CK(cudaMemset(dA, 0, A.size() * 8 * nseg));
     CK(cudaMalloc(&dW, A.size() * 8));
     CK(cudaMalloc(&djs, r * 8));
     CK(cudaMalloc(&dip, nslots * 8)); CK(cudaMalloc(&djp, nslots * 8));
@@ -99,14 +101,17 @@ int main(int argc, char **argv)
         CK(cudaMemcpy(dcolmap, cm.data(), r * 8, cudaMemcpyHostToDevice));
     }
     CK(cudaMalloc(&dtrace, 8 * 8 * 64 * 4));
-    CK(cudaMemcpy(dA, A.data(), A.size() * 8, cudaMemcpyHostToDevice));
+    // slot s's segment 0 holds its Gram, the other segments zeros (same A)
+    for (int sl = 0; sl < nslots; ++sl)
+        CK(cudaMemcpy(dA + (size_t)sl * nseg * B2 * B2, A.data() + (size_t)sl * B2 * B2,
+                      B2 * B2 * 8, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(djs, js.data(), r * 8, cudaMemcpyHostToDevice));
     CK(cudaMemset(derr, 0xff, 8));
     CK(cudaMemset(dC, 0, nslots)); CK(cudaMemset(drot, 0, nslots * 4));
     CK(cudaMemset(dskip, 0, nslots * 4)); CK(cudaMemset(dmaxt, 0, nslots * 8));
     InnerArgs ia{};
-    ia.part.T = 1; ia.part.L = 1; ia.part.NSEG = 1; ia.part.NS = nslots; ia.part.P = nslots;
-    ia.maxseg = 1; ia.Apart = dA; ia.Wg = dW; ia.jsign = djs;
+    ia.part.T = 1; ia.part.L = 1; ia.part.NSEG = nseg; ia.part.NS = nslots; ia.part.P = nslots;
+    ia.maxseg = nseg; ia.Apart = dA; ia.Wg = dW; ia.jsign = djs;
     ia.ip = dip; ia.jp = djp; ia.iblk = dib; ia.jblk = djb; ia.cur = dcur;
     ia.C = dC; ia.tset = dts; ia.rotk = drot; ia.skipk = dskip; ia.maxt = dmaxt; ia.err = derr;
     ia.nb = nb; ia.slot_base = 0; ia.eps = 0x1p-52; ia.teps = 0x1p-27;
@@ -170,22 +175,39 @@ int main(int argc, char **argv)
         ia.trace = nullptr;
         std::vector<long long> tr(8 * 64 * 4);
         CK(cudaMemcpy(tr.data(), dtrace, tr.size() * 8, cudaMemcpyDeviceToHost));
-        double sum[4] = {0, 0, 0, 0};
-        for (int it = 0; it < rounds; ++it) {
-            long long *t = &tr[8 * it];
-            sum[0] += t[1] - t[0]; sum[1] += t[2] - t[1]; sum[2] += t[3] - t[2]; sum[3] += t[4] - t[3];
-        }
-        printf("  avg cycles per round: phases %.0f / %.0f / %.0f / %.0f; total round %.0f\n",
-               sum[0] / rounds, sum[1] / rounds, sum[2] / rounds, sum[3] / rounds,
-               (double)(tr[8 * (rounds - 1) + 4] - tr[0]) / rounds);
         if (kind == 0) {
-            double s5 = 0;
-            for (int it = 0; it < rounds; ++it) s5 += tr[8 * it + 5] - tr[8 * it];
-            printf("  k_inner: round start -> rotation inputs loaded and skip-tested %.0f cycles\n", s5 / rounds);
+            // k_inner (leader/bulk): stamps 0 round start, 5 pivots ready,
+            // 1 rotation formed, 2 published
+            double s05 = 0, s51 = 0, s12 = 0, per = 0;
+            for (int it = 0; it < rounds; ++it) {
+                long long *t = &tr[8 * it];
+                s05 += t[5] - t[0]; s51 += t[1] - t[5]; s12 += t[2] - t[1];
+                if (it + 1 < rounds) per += tr[8 * (it + 1)] - t[0];
+            }
+            printf("  k_inner leader per round: pivots %.0f / rotation %.0f / publish %.0f; period %.0f cycles\n",
+                   s05 / rounds, s51 / rounds, s12 / rounds, per / (rounds - 1));
+            double b01 = 0, b12 = 0, b23 = 0, bper = 0;
+            for (int it = 1; it < rounds; ++it) {
+                long long *t = &tr[1024 + 8 * it];
+                b01 += t[1] - t[0]; b12 += t[2] - t[1]; b23 += t[3] - t[2];
+                if (it + 1 < rounds) bper += t[8] - t[0];
+            }
+            printf("  k_inner bulk warp 1 per round: wait R %.0f / wait previous round %.0f / blocks %.0f; period %.0f\n",
+                   b01 / (rounds - 1), b12 / (rounds - 1), b23 / (rounds - 1), bper / (rounds - 2));
+            printf("  k_inner CTA 0: entry -> prologue done %lld cycles, prologue done -> round 0 %lld\n",
+                   tr[8 * 64 + 3] - tr[8 * 64 + 2], tr[0] - tr[8 * 64 + 3]);
+            printf("  k_inner CTA 0: leader done %lld cycles after round 0, W replay done %lld, epilogue %lld\n",
+                   tr[8 * (rounds - 1) + 2] - tr[0], tr[8 * 64] - tr[0], tr[8 * 64 + 1] - tr[0]);
+        } else {
+            double sum[4] = {0, 0, 0, 0};
+            for (int it = 0; it < rounds; ++it) {
+                long long *t = &tr[8 * it];
+                sum[0] += t[1] - t[0]; sum[1] += t[2] - t[1]; sum[2] += t[3] - t[2]; sum[3] += t[4] - t[3];
+            }
+            printf("  avg cycles per round: phases %.0f / %.0f / %.0f / %.0f; total round %.0f\n",
+                   sum[0] / rounds, sum[1] / rounds, sum[2] / rounds, sum[3] / rounds,
+                   (double)(tr[8 * (rounds - 1) + 4] - tr[0]) / rounds);
         }
-        if (kind == 0)
-            printf("  k_inner CTA 0: A chain done %lld cycles after round 0, W replay done %lld, epilogue %lld\n",
-                   tr[8 * (rounds - 1) + 4] - tr[0], tr[8 * 64] - tr[0], tr[8 * 64 + 1] - tr[0]);
     }
     // pairwise comparison of the kernels' W, rotation counts and touched sets
     auto cmp = [&](int x, int y, const char *what) {
