@@ -58,6 +58,8 @@ struct InnerCfg {
     static constexpr int G = NBT / b;
     static constexpr int NB = (b / 2 + G) / G;
     static_assert(NBT % b == 0, "k_inner: bulk warp count");
+    // bulk warps holding the critical groups 1 and 2 (threads b .. 3b-1)
+    static constexpr int CW0 = b / 32, NCW = (3 * b - 1) / 32 - b / 32 + 1;
     // full ordering: 2b-1 rounds, cyclic over M = 2b-1 positions; U rounds
     // are renamed in registers between row shifts (U divides the rounds)
     static constexpr int M = B2 - 1;
@@ -71,7 +73,6 @@ struct InnerSmem2 {
                                      // upper triangle, [min][max], ld B2
     double2 ltc[B2][B2 / 2];         // rotation log of the pass: (t, c) per round and pair
     unsigned long long full[B2];     // mbarrier per round: the log entry is published
-    unsigned long long done[2];      // mbarrier by round parity: the bulk finished a round
     unsigned long long wdone;        // W warps have replayed a whole pass
     int lflag[B2];                   // bit 0: some pair rotated, bit 1: a pair failed
     unsigned int lact[B2];           // per round: the pairs that rotated (bit x: pair x)
@@ -90,6 +91,17 @@ __device__ __forceinline__ void named_bar_sync(int id, int count)
 {
     asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
 }
+__device__ __forceinline__ void named_bar_arrive(int id, int count)
+{
+    asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+// named barriers of k_inner: 0 the whole CTA; leader -> bulk (a round's
+// rotations are published); bulk -> leader (the critical blocks of a round
+// are written); bulk only (a round is complete).  Hardware barriers park the
+// waiting warps without polling, and each is passed once per round by
+// construction (no lapping: the bulk reaches round k+1's barriers only after
+// the leader consumed round k's)
+constexpr int kBarRound = 1, kBarCrit = 2, kBarDone = 3;
 
 // W warps wait for a published round without polling the shared-memory
 // pipe: the suspend hint parks the warp until the phase completes
@@ -391,7 +403,6 @@ __global__ void __launch_bounds__(inner2_threads<B2>()) k_inner(InnerArgs a)
     }
     const unsigned full0 = (unsigned)__cvta_generic_to_shared(&S.full[0]);
     const unsigned wdone = (unsigned)__cvta_generic_to_shared(&S.wdone);
-    const unsigned done0 = (unsigned)__cvta_generic_to_shared(&S.done[0]);
     // roles: warp 0 leads, warps 1..NBW bulk, then the W warps (the bulk is
     // spread over all four SM sub-partitions: measured faster than keeping
     // the leader's sub-partition free of bulk warps)
@@ -452,8 +463,6 @@ __global__ void __launch_bounds__(inner2_threads<B2>()) k_inner(InnerArgs a)
             S.fail = kNoError;
             S.touched = 0;
             for (int k = 0; k < rounds; ++k) mbar_init(full0 + 8 * k, 32);
-            mbar_init(done0, C::NBT);
-            mbar_init(done0 + 8, C::NBT);
             mbar_init(wdone, C::NWW * 32);
             asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
         }
@@ -469,59 +478,36 @@ __global__ void __launch_bounds__(inner2_threads<B2>()) k_inner(InnerArgs a)
 #define HSVD_STAMP(k) \
     if (tr && it < 64) tr[8 * it + (k)] = clock64();
     if (warp == 0) {
-        // ---- leader: forms round it's b rotations while the bulk applies
-        // round it-1.  Its pivots are entries of S_{it-1} = R^T S_{it-2} R
-        // (round it-1's congruence): lane x recomputes its three from
-        // S_{it-2} (complete once the bulk finished round it-2) with exactly
-        // the bulk's block formulas and orientation, so they are the bits
-        // the bulk writes
+        // ---- leader: forms round it's b rotations while the bulk finishes
+        // round it-1.  Lane x keeps the diagonal entries of its pair in
+        // registers (it updates them itself with the bulk's formulas and
+        // passes them on by shuffles), so the only entry it reads is the
+        // pivot a_ij = S_{it-1}(i, j).  That entry lies in one of the bulk's
+        // "critical" blocks of round it-1 (d = 1 or 2: the pairs that hand
+        // i and j to this round), which the bulk computes first and signals
+        // (mbarrier crit), before the rest of round it-1.
         const unsigned long long jneg =
             B2 == 64 ? ((unsigned long long)S.jneg[1] << 32) | S.jneg[0] : S.jneg[0];
         const int q = lane % b;  // pair owned by this lane
-        double tprev = 0.0, cprev = 1.0;
-        unsigned hprev = 0, vprev = 0;  // previous round: hyperbolic / active masks
-        int lb = 0;  // buffer holding S_{it-2}
-        int rd = 0, rdp = 0;
-        for (int it = 0; it < total; ++it, rdp = rd, rd = rd + 1 == rounds ? 0 : rd + 1) {
+        int lbuf = 0;            // buffer holding S_{it-1}
+        int i, j;
+        inner_cols<B2, FULL>(q, 0, i, j);
+        double dci = S.A[0][i * (LDA + 1)], dcj = S.A[0][j * (LDA + 1)];
+        int rd = 0;
+        for (int it = 0; it < total; ++it) {
             HSVD_STAMP(0)
             if (it > 0 && rd == 0) {
                 // pass boundary (passes > 1): the W warps must have replayed
                 // the previous pass before its log is overwritten
                 mbar_wait(wdone, (unsigned)((it / rounds) & 1) ^ 1u);
             }
-            if (it >= 2) mbar_wait(done0 + 8 * (it & 1), (unsigned)((it - 2) >> 1) & 1u);
-            const double *Ab = S.A[lb];
-            int i, j;
-            inner_cols<B2, FULL>(q, rd, i, j);
             const int lo = i < j ? i : j, hi = i < j ? j : i;
-            double a_ii, a_jj, a_ij;
-            if (it == 0 || vprev == 0) {
-                // S_{it-1} = S_{it-2}: the buffer holds the pivots
-                a_ii = Ab[i * (LDA + 1)];
-                a_jj = Ab[j * (LDA + 1)];
-                a_ij = Ab[lo * LDA + hi];
-            } else {
-                // pairs of i and j in round it-1 (rdp) and their rotations
-                int pi, pj;
-                bool ri, rj;  // column is the pair's second ("j") member
-                inner_pair_of<B2, FULL>(i, rdp, pi, ri);
-                inner_pair_of<B2, FULL>(j, rdp, pj, rj);
-                const double ti = __shfl_sync(0xffffffffu, tprev, pi),
-                             ci = __shfl_sync(0xffffffffu, cprev, pi);
-                const double tj = __shfl_sync(0xffffffffu, tprev, pj),
-                             cj = __shfl_sync(0xffffffffu, cprev, pj);
-                const double si = inner_st(ti, (hprev >> pi) & 1u),
-                             sj = inner_st(tj, (hprev >> pj) & 1u);
-                a_ii = inner_diag_after<B2, FULL>(Ab, pi, ri, rdp, ti, ci, si);
-                a_jj = inner_diag_after<B2, FULL>(Ab, pj, rj, rdp, tj, cj, sj);
-                // (i, j) lies in the off-diagonal block of pairs pi, pj; the
-                // bulk rotates it as rows of p, columns of q with
-                // q = p + d (mod b), d <= b/2 (d = b/2 only for p < b/2)
-                const int d1 = (pj - pi + b) % b;
-                const bool iprow = d1 < b / 2 || (d1 == b / 2 && pi < b / 2);
-                a_ij = iprow ? inner_off_after<B2, FULL>(Ab, pi, pj, ri, rj, rdp, ti, ci, si, tj, cj, sj)
-                             : inner_off_after<B2, FULL>(Ab, pj, pi, rj, ri, rdp, tj, cj, sj, ti, ci, si);
-            }
+            const int hyp = (((jneg >> i) ^ (jneg >> j)) & 1) ? 1 : -1;
+            const unsigned vh = __ballot_sync(0xffffffffu, hyp > 0);
+            const double a_ii = dci, a_jj = dcj, thr = (a.eps * a.eps) * (a_ii * a_jj);
+            if (it >= 1) named_bar_sync(kBarCrit, 32 + C::NCW * 32);  // round it-1's critical blocks
+            HSVD_STAMP(7)
+            const double a_ij = S.A[lbuf][lo * LDA + hi];
             // relative-orthogonality skip |a_ij| < eps sqrt(a_ii a_jj)
             // (_kernels.py:211), squared: no square root on the chain; the
             // rotation is formed beside the test (a_ij = 0 gives the
@@ -529,10 +515,8 @@ __global__ void __launch_bounds__(inner2_threads<B2>()) k_inner(InnerArgs a)
             // orientation (i, j): the closed forms are odd (trig) or
             // symmetric (hyperbolic) in the roles, so this is the sorted
             // form's transformation except at zeta = 0
-            const bool skip = a_ij == 0.0 ||
-                              (a.use_skip && a_ij * a_ij < (a.eps * a.eps) * (a_ii * a_jj));
+            const bool skip = a_ij == 0.0 || (a.use_skip && a_ij * a_ij < thr);
             HSVD_STAMP(5)
-            const int hyp = (((jneg >> i) ^ (jneg >> j)) & 1) ? 1 : -1;
             double t, c;
             const int status = FAST ? rotation_fast(a_ii, a_jj, a_ij, hyp, t, c)
                                     : rotation_tc(a_ii, a_jj, a_ij, hyp, t, c);
@@ -542,13 +526,13 @@ __global__ void __launch_bounds__(inner2_threads<B2>()) k_inner(InnerArgs a)
             HSVD_STAMP(1)
             if (lane < b) S.ltc[rd][q] = make_double2(t, c);
             const unsigned va = __ballot_sync(0xffffffffu, act),
-                           vb = __ballot_sync(0xffffffffu, bad),
-                           vh = __ballot_sync(0xffffffffu, hyp > 0);
+                           vb = __ballot_sync(0xffffffffu, bad);
             if (lane == 0) {
                 S.lflag[rd] = (va ? 1 : 0) | (vb ? 2 : 0);
                 S.lact[rd] = va;
                 S.lhyp[rd] = vh;
             }
+            named_bar_arrive(kBarRound, 32 + C::NBT);  // release to the bulk
             if (bad && lane < b)
                 atomicMin(&S.fail, pack_err(a.slot_base + slot, slot_pos(lo, b, I, J),
                                             slot_pos(hi, b, I, J)));
@@ -560,25 +544,50 @@ __global__ void __launch_bounds__(inner2_threads<B2>()) k_inner(InnerArgs a)
                     mbar_arrive(full0 + 8 * r2);
                 }
             }
-            mbar_arrive(full0 + 8 * rd);  // release: the round's log entry
+            mbar_arrive(full0 + 8 * rd);  // release to the W warps
             HSVD_STAMP(2)
             if (vb) break;
-            // the bulk writes S_{it} over the buffer of S_{it-2} once round
-            // it-1 has rotated (else the buffers do not move)
-            if (it > 0 && vprev) lb ^= 1;
-            tprev = t;
-            cprev = c;
-            hprev = vh;
-            vprev = va;
+            // this pair's diagonal after the round (the bulk's diagonal-block
+            // formulas, so its bits; a skipped pair keeps its entries)
+            const double st = inner_st(t, hyp > 0);
+            double nci = a_ii, ncj = a_jj;
+            if (act) {
+                const double y00 = fma(st, a_ij, a_ii) * c, y10 = fma(st, a_jj, a_ij) * c;
+                const double y01 = fma(t, a_ii, a_ij) * c, y11 = fma(t, a_ij, a_jj) * c;
+                nci = fma(st, y10, y00) * c;
+                ncj = fma(t, y01, y11) * c;
+            }
+            // next round's pair and where its two diagonal entries are now
+            const int rdn = rd + 1 == rounds ? 0 : rd + 1;
+            inner_cols<B2, FULL>(q, rdn, i, j);
+            int pi, pj;
+            bool ri, rj;
+            inner_pair_of<B2, FULL>(i, rd, pi, ri);
+            inner_pair_of<B2, FULL>(j, rd, pj, rj);
+            const double xi = __shfl_sync(0xffffffffu, nci, pi), yi = __shfl_sync(0xffffffffu, ncj, pi);
+            const double xj = __shfl_sync(0xffffffffu, nci, pj), yj = __shfl_sync(0xffffffffu, ncj, pj);
+            dci = ri ? yi : xi;
+            dcj = rj ? yj : xj;
+            if (va) lbuf ^= 1;  // the bulk writes S_it into the other buffer
+            rd = rdn;
+            HSVD_STAMP(6)
+            // the last round's critical signal is consumed too (balanced barrier)
+            if (it + 1 == total) named_bar_sync(kBarCrit, 32 + C::NCW * 32);
         }
     } else {
         // ---- bulk: round it's congruence on the upper blocks, buffer cb to
         // cb ^ 1.  Thread (group g, pair p) owns blocks (p, p + d), d = g + G k
         // (the rest of the upper triangle's blocks), larger d are dead slots;
-        // p is the same in every slot
+        // p is the same in every slot.  Slot 0 of groups 1 and 2 (d = 1, 2)
+        // holds the blocks the leader's next pivots come from: it is done
+        // first and signalled (crit)
         constexpr int G = C::G, NB = C::NB;
+        static_assert(G >= 3, "k_inner: the critical blocks need d = 1, 2 in slot 0");
         const int bt = atid - 32;
         const int pk = bt % b, g = bt / b;
+        // the warps holding groups 1 and 2 signal as whole warps (a named
+        // barrier counts warps): bulk warps CW0 .. CW0 + NCW - 1
+        const bool critg = bt / 32 >= C::CW0 && bt / 32 < C::CW0 + C::NCW;
         int qk[NB];
         bool dg[NB], live[NB];
 #pragma unroll
@@ -593,10 +602,8 @@ __global__ void __launch_bounds__(inner2_threads<B2>()) k_inner(InnerArgs a)
         long long *btr = (a.trace && blockIdx.x == 0 && tid == 32) ? a.trace + 1024 : nullptr;
         for (int it = 0; it < total; ++it, rd = rd + 1 == rounds ? 0 : rd + 1) {
             if (btr && it < 64) btr[8 * it] = clock64();
-            mbar_wait(full0 + 8 * rd, (unsigned)((it / rounds) & 1));
+            named_bar_sync(kBarRound, 32 + C::NBT);  // the leader published round it
             if (btr && it < 64) btr[8 * it + 1] = clock64();
-            // S_{it-1} complete: every bulk thread finished round it-1
-            if (it >= 1) mbar_wait(done0 + 8 * ((it - 1) & 1), (unsigned)((it - 1) >> 1) & 1u);
             if (btr && it < 64) btr[8 * it + 2] = clock64();
             const int f = S.lflag[rd];
             if (f & 2) break;
@@ -610,18 +617,51 @@ __global__ void __launch_bounds__(inner2_threads<B2>()) k_inner(InnerArgs a)
                 inner_cols<B2, FULL>(pk, rd, ip, jp);
                 const double2 tcp = S.ltc[rd][pk];
                 const double tp = tcp.x, cp = tcp.y, sp = inner_st(tp, (hm >> pk) & 1u);
-                int o[NB][4];
-                double x[NB][4], tq[NB], cq[NB], sq[NB];
-#pragma unroll
-                for (int k = 0; k < NB; ++k) {
+                auto slot_offsets = [&](int k, int (&o)[4]) {
                     int iq, jq;
                     inner_cols<B2, FULL>(qk[k], rd, iq, jq);
                     // canonical [min][max] offsets of (ip,iq) (ip,jq) (jp,iq) (jp,jq);
                     // a diagonal block is (ip,ip) (ip,jp) (jp,ip) (jp,jp)
-                    o[k][0] = dg[k] ? ip * (LDA + 1) : min(ip, iq) * LDA + max(ip, iq);
-                    o[k][1] = min(ip, jq) * LDA + max(ip, jq);
-                    o[k][2] = min(jp, iq) * LDA + max(jp, iq);
-                    o[k][3] = dg[k] ? jp * (LDA + 1) : min(jp, jq) * LDA + max(jp, jq);
+                    o[0] = dg[k] ? ip * (LDA + 1) : min(ip, iq) * LDA + max(ip, iq);
+                    o[1] = min(ip, jq) * LDA + max(ip, jq);
+                    o[2] = min(jp, iq) * LDA + max(jp, iq);
+                    o[3] = dg[k] ? jp * (LDA + 1) : min(jp, jq) * LDA + max(jp, jq);
+                };
+                auto slot_apply = [&](int k, const int (&o)[4], const double (&x)[4], double tq,
+                                      double cq, double sq) {
+                    double n0 = x[0], n1 = x[1], n2 = x[2], n3 = x[3];
+                    if (!(tp == 0.0 && tq == 0.0)) {
+                        const double y00 = fma(sq, x[1], x[0]) * cq;
+                        const double y01 = fma(tq, x[0], x[1]) * cq;
+                        const double y10 = fma(sq, x[3], x[2]) * cq;
+                        const double y11 = fma(tq, x[2], x[3]) * cq;
+                        n0 = fma(sp, y10, y00) * cp;
+                        n3 = fma(tp, y01, y11) * cp;
+                        n1 = dg[k] ? 0.0 : fma(sp, y11, y01) * cp;  // the pair itself: annihilated
+                        n2 = fma(tp, y00, y10) * cp;
+                    }
+                    Aw[o[0]] = n0;
+                    Aw[o[3]] = n3;
+                    Aw[o[1]] = n1;
+                    if (!dg[k]) Aw[o[2]] = n2;
+                };
+                // slot 0 first (the critical blocks), then the others batched
+                {
+                    int o[4];
+                    double x[4];
+                    slot_offsets(0, o);
+                    const double2 tcq = S.ltc[rd][qk[0]];
+                    const double sq = inner_st(tcq.x, (hm >> qk[0]) & 1u);
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) x[u] = Ar[o[u]];
+                    if (live[0]) slot_apply(0, o, x, tcq.x, tcq.y, sq);
+                }
+                if (critg) named_bar_arrive(kBarCrit, 32 + C::NCW * 32);  // release: S_it's critical blocks
+                int o[NB][4];
+                double x[NB][4], tq[NB], cq[NB], sq[NB];
+#pragma unroll
+                for (int k = 1; k < NB; ++k) {
+                    slot_offsets(k, o[k]);
                     const double2 tcq = S.ltc[rd][qk[k]];
                     tq[k] = tcq.x;
                     cq[k] = tcq.y;
@@ -632,28 +672,14 @@ __global__ void __launch_bounds__(inner2_threads<B2>()) k_inner(InnerArgs a)
                     }
                 }
 #pragma unroll
-                for (int k = 0; k < NB; ++k) {
-                    if (!live[k]) continue;
-                    double n0 = x[k][0], n1 = x[k][1], n2 = x[k][2], n3 = x[k][3];
-                    if (!(tp == 0.0 && tq[k] == 0.0)) {
-                        const double y00 = fma(sq[k], x[k][1], x[k][0]) * cq[k];
-                        const double y01 = fma(tq[k], x[k][0], x[k][1]) * cq[k];
-                        const double y10 = fma(sq[k], x[k][3], x[k][2]) * cq[k];
-                        const double y11 = fma(tq[k], x[k][2], x[k][3]) * cq[k];
-                        n0 = fma(sp, y10, y00) * cp;
-                        n3 = fma(tp, y01, y11) * cp;
-                        n1 = dg[k] ? 0.0 : fma(sp, y11, y01) * cp;  // the pair itself: annihilated
-                        n2 = fma(tp, y00, y10) * cp;
-                    }
-                    Aw[o[k][0]] = n0;
-                    Aw[o[k][3]] = n3;
-                    Aw[o[k][1]] = n1;
-                    if (!dg[k]) Aw[o[k][2]] = n2;
-                }
+                for (int k = 1; k < NB; ++k)
+                    if (live[k]) slot_apply(k, o[k], x[k], tq[k], cq[k], sq[k]);
                 cb ^= 1;
+            } else if (critg) {
+                named_bar_arrive(kBarCrit, 32 + C::NCW * 32);  // nothing moved: S_it = S_{it-1}
             }
             if (btr && it < 64) btr[8 * it + 3] = clock64();
-            mbar_arrive(done0 + 8 * (it & 1));  // release: this thread's part of S_it
+            named_bar_sync(kBarDone, C::NBT);  // S_it complete before round it+1 reads it
         }
     }
 #undef HSVD_STAMP

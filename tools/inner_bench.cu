@@ -186,6 +186,13 @@ int main(int argc, char **argv)
             }
             printf("  k_inner leader per round: pivots %.0f / rotation %.0f / publish %.0f; period %.0f cycles\n",
                    s05 / rounds, s51 / rounds, s12 / rounds, per / (rounds - 1));
+            double s07 = 0, s75 = 0, s26 = 0;
+            for (int it = 1; it < rounds; ++it) {
+                long long *t = &tr[8 * it];
+                s07 += t[7] - t[0]; s75 += t[5] - t[7]; s26 += t[6] - t[2];
+            }
+            printf("  k_inner leader: wait crit %.0f, a_ij + skip test %.0f, after publish %.0f\n",
+                   s07 / (rounds - 1), s75 / (rounds - 1), s26 / (rounds - 1));
             double b01 = 0, b12 = 0, b23 = 0, bper = 0;
             for (int it = 1; it < rounds; ++it) {
                 long long *t = &tr[1024 + 8 * it];
