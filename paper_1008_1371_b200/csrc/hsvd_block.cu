@@ -11,14 +11,16 @@
 //             m8n8k4 -> SASS DMMA.8x8x4); each slot's K range is cut into
 //             fixed segments (a function of n only) streamed over the CTAs,
 //             upper-triangle tiles only.
-//   k_inner   one CTA per slot: folds the segment partials in order, runs one
-//             pass of 2x2 rotations on (A_P, J_P) in shared memory -- trig or
-//             hyperbolic from the signs, with the relative-orthogonality skip
-//             (_kernels.py:211); "fast" plain-fp64 closed forms by default,
-//             the reference's double-double rotation_tc (_kernels.py:128-173)
-//             with block_rotation="dd" -- and accumulates the J-orthogonal
-//             W_P; writes convergence codes and statistics, advances the
-//             stepper.
+//   k_inner   one CTA per slot (hsvd_inner.cuh): folds the segment partials
+//             in order, runs one pass of 2x2 rotations on (A_P, J_P) in
+//             shared memory -- a leader warp forms each round's rotations
+//             (trig or hyperbolic from the signs, relative-orthogonality skip
+//             _kernels.py:211; "fast" plain-fp64 closed forms by default, the
+//             reference's double-double rotation_tc _kernels.py:128-173 with
+//             block_rotation="dd") while bulk warps apply the previous round
+//             to the upper triangle of A and W warps accumulate the
+//             J-orthogonal W_P in registers; writes convergence codes and
+//             statistics, advances the stepper.
 //   k_update  [G_P; V_P] <- [G_P; V_P] W_P, FP64 tensor cores, in place.
 //
 // The inner ordering is "full" by default (every pair of the pivot block,

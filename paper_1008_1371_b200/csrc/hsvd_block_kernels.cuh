@@ -1021,17 +1021,16 @@ __device__ __forceinline__ int rotation_fast(double a_ii, double a_jj, double a_
     return 0;
 }
 
-// One pass of disjoint 2x2 rotations on the 2b x 2b pivot Gram A_P in shared
-// memory, accumulating W_P (A_P <- W^T A_P W, W J-orthogonal).
+// k_inner_v1: the round-1 inner pass (both triangles of A and W in shared
+// memory, warp 0 forms the rotations, two barriers per round).  The product
+// runs k_inner (hsvd_inner.cuh); this kernel stays only as the A/B and
+// cross-check reference of tools/inner_bench.cu (it is never instantiated by
+// the library).
 //
 // A round's b pairs are disjoint, so the round is the congruence
 // A <- R^T A R with R block-diagonal in 2x2 blocks: every 2x2 block (p, q) of
 // A (rows {i_p, j_p}, columns {i_q, j_q}) becomes R_p^T A_pq R_q on its own.
-// Every warp computes all b rotations of the round redundantly (lane q owns
-// pair q; a warp-uniform decision skips inactive rounds without a barrier),
-// then updates its share of the blocks and of W from registers and shuffles:
-// two barriers per active round, none per inactive round.
-// threads of one k_inner CTA
+// threads of one k_inner_v1 CTA
 constexpr int kInnerThreads = HSVD_INNER_THREADS;
 template <int B2>
 __host__ __device__ constexpr int inner_threads() { return B2 == 64 ? kInnerThreads : 256; }

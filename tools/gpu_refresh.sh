@@ -3,7 +3,7 @@
 # full captures of the block kernels (one-stream step).
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
-timeout 2400 python -m pytest tests -m gpu -q -rf > gpurun_out/pytest_gpu.log 2>&1
+timeout 2400 python -m pytest tests -m gpu -q -rf --timeout=600 --timeout-method=thread > gpurun_out/pytest_gpu.log 2>&1
 tail -12 gpurun_out/pytest_gpu.log
 grep -h "block sigma rel diff" gpurun_out/pytest_gpu.log
 timeout 1200 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err
