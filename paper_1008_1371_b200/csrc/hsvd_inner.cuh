@@ -39,6 +39,12 @@
 #ifndef HSVD_INNER_DIAG_NOUPD
 #define HSVD_INNER_DIAG_NOUPD 0
 #endif
+#ifndef HSVD_INNER_WHALF
+#define HSVD_INNER_WHALF 0  // 1: W rows split over two threads (half rows; measured slower: 1600 vs 1470 cycles per round)
+#endif
+#ifndef HSVD_INNER_BWARPS64H
+#define HSVD_INNER_BWARPS64H 7  // bulk warps at b = 32 with half rows (+ leader + 4 W: 12 warps)
+#endif
 #ifndef HSVD_INNER_BWARPS64
 #define HSVD_INNER_BWARPS64 5  // bulk warps at b = 32 (+ leader + 2 W warps: 8 warps, 255 registers)
 #endif
@@ -46,11 +52,19 @@
 template <int B2>
 struct InnerCfg {
     static constexpr int b = B2 / 2;
+#if HSVD_INNER_WHALF
+    static constexpr int NBW = B2 == 64 ? HSVD_INNER_BWARPS64H : 3;  // bulk warps
+#else
     static constexpr int NBW = B2 == 64 ? HSVD_INNER_BWARPS64 : 3;  // bulk warps
+#endif
     static constexpr int NBT = NBW * 32;                           // bulk threads
     static constexpr int NAW = 1 + NBW;                            // leader + bulk ("A side")
     static constexpr int NA = NAW * 32;
-    static constexpr int NWW = B2 / 32;                            // W warps: a row per thread
+#if HSVD_INNER_WHALF
+    static constexpr int NWW = B2 / 16;  // W warps: half a row per thread, two halves per row group
+#else
+    static constexpr int NWW = B2 / 32;  // W warps: a row per thread
+#endif
     static constexpr int NT = NA + NWW * 32;
     static constexpr int LDA = B2;
     // bulk block slots: thread (g, p) of the bulk owns blocks (p, p + d),
@@ -78,6 +92,7 @@ struct InnerSmem2 {
     unsigned int lact[B2];           // per round: the pairs that rotated (bit x: pair x)
     unsigned int lhyp[B2];           // per round: hyperbolic pairs (st = t), else st = -t
     unsigned int jneg[2], padm[2];   // per-column bit masks (J = -1, padding)
+    double wx[2][2][B2];             // W half-row exchange: [round parity][half][row]
     unsigned int rot, skip, big;
     unsigned long long maxt_bits;
     unsigned long long fail;
@@ -312,6 +327,153 @@ __device__ __forceinline__ bool inner_w_replay(double (&w)[B2], const InnerSmem2
     return true;
 }
 
+// ---- W rows split in two halves (HSVD_INNER_WHALF): the b pairs of a
+// round in position space are split into two fixed halves (pairs 0..b/2-1
+// and b/2..b-1); each half's positions form one "arc" of the moving
+// positions (plus fixed ones), and between rounds exactly one value leaves
+// each arc for the other.  A W row is held by two threads (warps of
+// different halves, the same rows), 32 doubles each, exchanging one double
+// per round through shared memory: registers fall from ~240 to ~100 per
+// thread, so the CTA can carry more bulk warps.
+//
+// full ordering (M = 2b-1 moving positions + position M fixed):
+//   half 0: arc a in [0, b/2-1) = position M-b/2+1+a, a in [b/2-1, b-1) =
+//           position a-(b/2-1); fixed: position M.  pair 0 = (fixed, arc
+//           b/2-1), pair j = (arc b/2-1+j, arc b/2-1-j)
+//   half 1: arc a = position b/2+a (b of them); pair b/2+j = (arc j, arc b-1-j)
+// oriented ordering (i side fixed, j side cycling over b positions):
+//   half h: fixed f = column h b/2 + f, arc a = position b + h b/2 + a;
+//           pair h b/2 + j = (fixed j, arc j)
+// Values move from arc index a to a-1; arc 0 leaves for the other half's
+// last arc index.  Within U renamed rounds arc a of sub-round s lives in
+// register (a + s) mod L.
+template <int B2, bool FULL, int HALF>
+struct WHalf {
+    static constexpr int b = B2 / 2, hb = b / 2, M = B2 - 1;
+    static constexpr int L = FULL ? (HALF == 0 ? b - 1 : b) : hb;  // arc length
+    static constexpr int NF = FULL ? (HALF == 0 ? 1 : 0) : hb;     // fixed registers
+    static constexpr int NFA = NF > 0 ? NF : 1;
+    // local pair j: (kind, index) of its ci and cj; kind 1 = fixed, 0 = arc
+    __host__ __device__ static constexpr int ci_fixed(int j) { return FULL ? (HALF == 0 && j == 0) : 1; }
+    __host__ __device__ static constexpr int ci_idx(int j)
+    {
+        return FULL ? (HALF == 0 ? (j == 0 ? 0 : hb - 1 + j) : j) : j;
+    }
+    __host__ __device__ static constexpr int cj_idx(int j)
+    {
+        return FULL ? (HALF == 0 ? hb - 1 - j : b - 1 - j) : j;
+    }
+    // column of arc index a / fixed register f (after whole passes)
+    __host__ __device__ static constexpr int arc_col(int a)
+    {
+        return FULL ? (HALF == 0 ? (a <= hb - 2 ? M - hb + 1 + a : a - (hb - 1)) : hb + a)
+                    : b + HALF * hb + a;
+    }
+    __host__ __device__ static constexpr int fix_col(int f) { return FULL ? M : HALF * hb + f; }
+};
+
+template <int B2, bool FULL, int HALF, int S>
+__device__ __forceinline__ int inner_wh_round(double (&ar)[WHalf<B2, FULL, HALF>::L],
+                                              double (&fx)[WHalf<B2, FULL, HALF>::NFA],
+                                              InnerSmem2<B2> &Sm, int rd, unsigned bar,
+                                              unsigned par, int rnd, int row, int rg, bool stats,
+                                              InnerStats &st_, unsigned long long padm, double teps)
+{
+    using H = WHalf<B2, FULL, HALF>;
+    constexpr int L = H::L, hb = H::hb;
+    mbar_wait_parked(bar, par);
+    const int f = *(volatile const int *)&Sm.lflag[rd];
+    const unsigned hm = Sm.lhyp[rd];
+#pragma unroll
+    for (int j = 0; j < hb; ++j) {
+        const int x = HALF * hb + j;
+        const double2 tc = Sm.ltc[rd][x];
+        const double t = tc.x, c = tc.y, st = inner_st(t, (hm >> x) & 1u);
+        const int ra = (H::ci_idx(j) + S) % L, rb = (H::cj_idx(j) + S) % L;
+        if (H::ci_fixed(j)) {
+            const double wx = fx[H::ci_idx(j) < H::NFA ? H::ci_idx(j) : 0], wy = ar[rb];
+            fx[H::ci_idx(j) < H::NFA ? H::ci_idx(j) : 0] = fma(st, wy, wx) * c;
+            ar[rb] = fma(t, wx, wy) * c;
+        } else {
+            const double wx = ar[ra], wy = ar[rb];
+            ar[ra] = fma(st, wy, wx) * c;
+            ar[rb] = fma(t, wx, wy) * c;
+        }
+    }
+    // one value leaves each arc for the other half (arc 0 -> last arc index)
+    Sm.wx[rnd & 1][HALF][row] = ar[S % L];
+    named_bar_sync(4 + rg, 64);
+    ar[S % L] = Sm.wx[rnd & 1][HALF ^ 1][row];
+    if (stats) {
+        // the reference's per-visit statistics (_kernels.py:218-233): lane x
+        // counts pair x of this round
+        const unsigned lane = threadIdx.x & 31;
+        constexpr int b = B2 / 2;
+        if (lane < (unsigned)b && !(f & 2)) {
+            int i, j;
+            inner_cols<B2, FULL>((int)lane, rd, i, j);
+            const bool act = (Sm.lact[rd] >> lane) & 1u;
+            if (act) {
+                const double at = fabs(Sm.ltc[rd][lane].x);
+                ++st_.rot;
+                st_.touch |= (1ull << i) | (1ull << j);
+                st_.big |= at > teps;
+                st_.maxt = fmax(st_.maxt, at);
+            } else if (!(((padm >> i) | (padm >> j)) & 1)) {
+                ++st_.skip;  // pairs with a padding column are not visits
+            }
+        }
+    }
+    return f;
+}
+
+// one half of a W row: replay the pass(es); false if the pass failed.  Writes
+// the half's columns of row `row` to Wout (column-major, ld B2) on success.
+template <int B2, bool FULL, int HALF>
+__device__ __forceinline__ bool inner_wh_replay(InnerSmem2<B2> &Sm, int passes, unsigned full0,
+                                                unsigned wdone, int row, int rg, bool stats,
+                                                InnerStats &st_, unsigned long long padm,
+                                                double teps, double *Wout)
+{
+    using C = InnerCfg<B2>;
+    using H = WHalf<B2, FULL, HALF>;
+    constexpr int L = H::L, U = FULL ? C::UF : C::UO;
+    constexpr int rounds = FULL ? B2 - 1 : B2 / 2;
+    static_assert(U <= 4 && rounds % U == 0, "k_inner: W unroll");
+    double ar[L], fx[H::NFA];
+#pragma unroll
+    for (int a = 0; a < L; ++a) ar[a] = H::arc_col(a) == row ? 1.0 : 0.0;
+#pragma unroll
+    for (int k = 0; k < H::NFA; ++k) fx[k] = (H::NF > 0 && H::fix_col(k) == row) ? 1.0 : 0.0;
+    int rnd = 0;
+    for (int ps = 0; ps < passes; ++ps) {
+        const unsigned par = (unsigned)ps & 1u;
+        for (int r0 = 0; r0 < rounds; r0 += U, rnd += U) {
+            int f = inner_wh_round<B2, FULL, HALF, 0>(ar, fx, Sm, r0, full0 + 8 * r0, par, rnd, row, rg, stats, st_, padm, teps);
+            if (U > 1) f |= inner_wh_round<B2, FULL, HALF, (U > 1 ? 1 : 0)>(ar, fx, Sm, r0 + 1, full0 + 8 * (r0 + 1), par, rnd + 1, row, rg, stats, st_, padm, teps);
+            if (U > 2) f |= inner_wh_round<B2, FULL, HALF, (U > 2 ? 2 : 0)>(ar, fx, Sm, r0 + 2, full0 + 8 * (r0 + 2), par, rnd + 2, row, rg, stats, st_, padm, teps);
+            if (U > 3) f |= inner_wh_round<B2, FULL, HALF, (U > 3 ? 3 : 0)>(ar, fx, Sm, r0 + 3, full0 + 8 * (r0 + 3), par, rnd + 3, row, rg, stats, st_, padm, teps);
+            if (f & 2) return false;
+            // arc a moves to register a: new reg[a] = old reg[(a + U) mod L]
+            double tmp[U];
+#pragma unroll
+            for (int k = 0; k < U; ++k) tmp[k] = ar[k];
+#pragma unroll
+            for (int a = 0; a < L - U; ++a) ar[a] = ar[a + U];
+#pragma unroll
+            for (int k = 0; k < U; ++k) ar[L - U + k] = tmp[k];
+        }
+        mbar_arrive(wdone);  // every W lane: this pass's log entries are consumed
+    }
+    // W column-major: Wout[c * B2 + row] = W[row][c]; after whole passes
+    // every position is its column again
+#pragma unroll
+    for (int a = 0; a < L; ++a) Wout[H::arc_col(a) * B2 + row] = ar[a];
+#pragma unroll
+    for (int k = 0; k < H::NF; ++k) Wout[H::fix_col(k) * B2 + row] = fx[k];
+    return true;
+}
+
 // A_P = sum of the slot's partial Gram segments in segment order (the upper
 // triangle; the same additions in the same order as a one-element-per-thread
 // fold, so the same bits).  Every thread of the CTA takes part: chunks of two
@@ -415,17 +577,38 @@ __global__ void __launch_bounds__(inner2_threads<B2>()) k_inner(InnerArgs a)
     if (wwarp) {
         // ---- W warps: their own code path (barrier 0 is shared with the A
         // warps by count, so the row's registers never overlap the fold's)
-        const int wrow = (warp - C::NAW) * 32 + lane;
-        double w[B2];  // row `wrow` of W in position space
-#pragma unroll
-        for (int p = 0; p < B2; ++p) w[p] = p == wrow ? 1.0 : 0.0;
+        const int wi = warp - C::NAW;
         named_bar_sync(0, NT);  // the prologue (A, masks, mbarriers) is done
         const unsigned long long padm =
             B2 == 64 ? ((unsigned long long)S.padm[1] << 32) | S.padm[0] : S.padm[0];
-        const bool stats = warp == C::NAW;
+        const bool stats = wi == 0;
         InnerStats st_;
+#if HSVD_INNER_WHALF
+        const int half = wi & 1, rg = wi >> 1, wrow = rg * 32 + lane;
+        double *Wout = a.Wg + (int64_t)slot * B2 * B2;
 #if !HSVD_INNER_DIAG_NOW  // diagnostics only (wrong W): no replay
-        inner_w_replay<B2, FULL>(w, S, a.passes, full0, wdone, stats, st_, padm, a.teps);
+        if (half == 0)
+            inner_wh_replay<B2, FULL, 0>(S, a.passes, full0, wdone, wrow, rg, stats, st_, padm, a.teps, Wout);
+        else
+            inner_wh_replay<B2, FULL, 1>(S, a.passes, full0, wdone, wrow, rg, stats, st_, padm, a.teps, Wout);
+#endif
+#else
+        const int wrow = wi * 32 + lane;
+        double w[B2];  // row `wrow` of W in position space
+#pragma unroll
+        for (int p = 0; p < B2; ++p) w[p] = p == wrow ? 1.0 : 0.0;
+#if !HSVD_INNER_DIAG_NOW  // diagnostics only (wrong W): no replay
+        const bool ok = inner_w_replay<B2, FULL>(w, S, a.passes, full0, wdone, stats, st_, padm, a.teps);
+#else
+        const bool ok = true;
+#endif
+        if (ok) {
+            // W column-major: Wg[slot][c * B2 + k] = W[k][c]; after whole
+            // passes every position is its column again
+            double *Wout = a.Wg + (int64_t)slot * B2 * B2 + wrow;
+#pragma unroll
+            for (int c = 0; c < B2; ++c) Wout[c * B2] = w[c];
+        }
 #endif
         if (stats) {
             atomicAdd(&S.rot, st_.rot);
@@ -435,12 +618,6 @@ __global__ void __launch_bounds__(inner2_threads<B2>()) k_inner(InnerArgs a)
             atomicOr(&S.touched, st_.touch);
         }
         named_bar_sync(0, NT);  // statistics and failure word are in
-        if (S.fail != kNoError) return;
-        // W column-major: Wg[slot][c * B2 + k] = W[k][c]; after whole passes
-        // every position is its column again
-        double *Wout = a.Wg + (int64_t)slot * B2 * B2 + wrow;
-#pragma unroll
-        for (int c = 0; c < B2; ++c) Wout[c * B2] = w[c];
         if (a.trace && blockIdx.x == 0 && wrow == 0) a.trace[8 * 64] = clock64();
         return;
     }
