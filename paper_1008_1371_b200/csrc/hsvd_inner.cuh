@@ -209,6 +209,82 @@ __device__ __forceinline__ double inner_off_after(const double *Ab, int p, int q
     return (tp == 0.0 && tq == 0.0) ? xo : v;  // both pairs skipped: copied
 }
 
+// ---- position space of the A copies (see the kernel).  FULL: moving
+// positions 0..M-1 (M = B2-1) shift down by one per round (0 wraps to M-1),
+// position M stays; oriented: the j half (b..2b-1) shifts, the i half stays.
+// fixed positions of pair x
+template <int B2, bool FULL>
+__host__ __device__ constexpr void inner_ppos(int x, int &u, int &v)
+{
+    if (FULL) {
+        u = x == 0 ? B2 - 1 : x;
+        v = x == 0 ? 0 : B2 - 1 - x;
+    } else {
+        u = x;
+        v = B2 / 2 + x;
+    }
+}
+// position in round k+1 of the value at position u in round k
+template <int B2, bool FULL>
+__host__ __device__ constexpr int inner_next(int u)
+{
+    constexpr int M = B2 - 1, b = B2 / 2;
+    return FULL ? (u == M ? M : (u == 0 ? M - 1 : u - 1)) : (u < b ? u : (u == b ? B2 - 1 : u - 1));
+}
+// position in round k - L of the value at position u in round k; L is
+// reduced (0 <= L < the period: M for FULL, b oriented, inner_lag)
+template <int B2, bool FULL>
+__host__ __device__ inline int inner_prev(int u, int L)
+{
+    constexpr int M = B2 - 1, b = B2 / 2;
+    if (FULL) {
+        if (u == M) return M;
+        const int w = u + L;
+        return w >= M ? w - M : w;
+    }
+    if (u < b) return u;
+    const int w = u - b + L;
+    return b + (w >= b ? w - b : w);
+}
+template <int B2, bool FULL>
+__host__ __device__ inline int inner_lag(int rounds_behind)
+{
+    return rounds_behind % (FULL ? B2 - 1 : B2 / 2);
+}
+// pair (and role: true = its second position) holding position w
+template <int B2, bool FULL>
+__host__ __device__ constexpr void inner_pos_pair(int w, int &x, bool &isj)
+{
+    constexpr int M = B2 - 1, b = B2 / 2;
+    if (FULL) {
+        x = w == M ? 0 : (w == 0 ? 0 : (w < b ? w : M - w));
+        isj = w != M && (w == 0 || w >= b);
+    } else {
+        x = w < b ? w : w - b;
+        isj = w >= b;
+    }
+}
+// canonical offset of the (symmetric) entry at positions (u, v)
+template <int B2>
+__host__ __device__ constexpr int inner_canon(int u, int v)
+{
+    return u < v ? u * B2 + v : v * B2 + u;
+}
+// a per-position bit mask moved to the next round's positions
+template <int B2, bool FULL>
+__device__ __forceinline__ unsigned long long inner_next_mask(unsigned long long m)
+{
+    constexpr int M = B2 - 1, b = B2 / 2;
+    if (FULL) {
+        const unsigned long long moving = (M == 64 ? ~0ull : ((1ull << M) - 1));
+        const unsigned long long mv = m & moving;
+        return (m & ~moving) | (mv >> 1) | ((mv & 1ull) << (M - 1));
+    }
+    const unsigned long long jm = ((1ull << b) - 1) << b;
+    const unsigned long long mv = m & jm;
+    return (m & ~jm) | ((mv >> 1) & jm) | ((mv & (1ull << b)) << (b - 1));
+}
+
 // register of position p after S renamed rounds
 template <int B2, bool FULL>
 __host__ __device__ constexpr int inner_wreg(int p, int S)
@@ -654,6 +730,14 @@ __global__ void __launch_bounds__(inner2_threads<B2>()) k_inner(InnerArgs a)
     long long *tr = (a.trace && blockIdx.x == 0 && tid == 0) ? a.trace : nullptr;
 #define HSVD_STAMP(k) \
     if (tr && it < 64) tr[8 * it + (k)] = clock64();
+    // A lives in "position space": in round k the entry of columns (c, c')
+    // is stored at positions (pos_k(c), pos_k(c')) (inner_pos), in which
+    // pair x is the FIXED position pair (inner_ppos).  The bulk reads round
+    // k's copy and writes S_k at round k+1's positions (every value moves to
+    // inner_next of its position), so every block address is loop-invariant
+    // and the accesses of a warp walk consecutive positions (no bank
+    // conflicts).  A round in which nothing rotates writes nothing: the copy
+    // then lags ("epoch" ep < k) and is read through inner_prev^(k - ep).
     if (warp == 0) {
         // ---- leader: forms round it's b rotations while the bulk finishes
         // round it-1.  Lane x keeps the diagonal entries of its pair in
@@ -661,15 +745,22 @@ __global__ void __launch_bounds__(inner2_threads<B2>()) k_inner(InnerArgs a)
         // passes them on by shuffles), so the only entry it reads is the
         // pivot a_ij = S_{it-1}(i, j).  That entry lies in one of the bulk's
         // "critical" blocks of round it-1 (d = 1 or 2: the pairs that hand
-        // i and j to this round), which the bulk computes first and signals
-        // (mbarrier crit), before the rest of round it-1.
-        const unsigned long long jneg =
-            B2 == 64 ? ((unsigned long long)S.jneg[1] << 32) | S.jneg[0] : S.jneg[0];
+        // i and j to this round), which the bulk computes first and signals.
         const int q = lane % b;  // pair owned by this lane
-        int lbuf = 0;            // buffer holding S_{it-1}
-        int i, j;
-        inner_cols<B2, FULL>(q, 0, i, j);
-        double dci = S.A[0][i * (LDA + 1)], dcj = S.A[0][j * (LDA + 1)];
+        int ux, vx;
+        inner_ppos<B2, FULL>(q, ux, vx);
+        const int oij = inner_canon<B2>(ux, vx);
+        // where this lane's next-round diagonal entries are in this round:
+        // the positions inner_prev(ux), inner_prev(vx) and their pairs
+        int si, sj;
+        bool ri, rj;
+        inner_pos_pair<B2, FULL>(inner_prev<B2, FULL>(ux, 1), si, ri);
+        inner_pos_pair<B2, FULL>(inner_prev<B2, FULL>(vx, 1), sj, rj);
+        // J signs by position (bit u: the column at position u is negative)
+        unsigned long long jpos =
+            B2 == 64 ? ((unsigned long long)S.jneg[1] << 32) | S.jneg[0] : S.jneg[0];
+        int lbuf = 0, ep = 0;  // buffer holding S_{it-1}, and its epoch
+        double dci = S.A[0][ux * (LDA + 1)], dcj = S.A[0][vx * (LDA + 1)];
         int rd = 0;
         for (int it = 0; it < total; ++it) {
             HSVD_STAMP(0)
@@ -678,18 +769,22 @@ __global__ void __launch_bounds__(inner2_threads<B2>()) k_inner(InnerArgs a)
                 // the previous pass before its log is overwritten
                 mbar_wait(wdone, (unsigned)((it / rounds) & 1) ^ 1u);
             }
-            const int lo = i < j ? i : j, hi = i < j ? j : i;
-            const int hyp = (((jneg >> i) ^ (jneg >> j)) & 1) ? 1 : -1;
+            const int hyp = (((jpos >> ux) ^ (jpos >> vx)) & 1) ? 1 : -1;
             const unsigned vh = __ballot_sync(0xffffffffu, hyp > 0);
             const double a_ii = dci, a_jj = dcj, thr = (a.eps * a.eps) * (a_ii * a_jj);
+            int oa = oij;
+            if (it != ep) {  // the copy lags behind inactive rounds (warp-uniform)
+                const int lag = inner_lag<B2, FULL>(it - ep);
+                oa = inner_canon<B2>(inner_prev<B2, FULL>(ux, lag), inner_prev<B2, FULL>(vx, lag));
+            }
             if (it >= 1) named_bar_sync(kBarCrit, 32 + C::NCW * 32);  // round it-1's critical blocks
             HSVD_STAMP(7)
-            const double a_ij = S.A[lbuf][lo * LDA + hi];
+            const double a_ij = S.A[lbuf][oa];
             // relative-orthogonality skip |a_ij| < eps sqrt(a_ii a_jj)
             // (_kernels.py:211), squared: no square root on the chain; the
             // rotation is formed beside the test (a_ij = 0 gives the
             // identity) and selected.  The pair is rotated in its schedule
-            // orientation (i, j): the closed forms are odd (trig) or
+            // orientation (ci, cj): the closed forms are odd (trig) or
             // symmetric (hyperbolic) in the roles, so this is the sorted
             // form's transformation except at zeta = 0
             const bool skip = a_ij == 0.0 || (a.use_skip && a_ij * a_ij < thr);
@@ -710,9 +805,13 @@ __global__ void __launch_bounds__(inner2_threads<B2>()) k_inner(InnerArgs a)
                 S.lhyp[rd] = vh;
             }
             named_bar_arrive(kBarRound, 32 + C::NBT);  // release to the bulk
-            if (bad && lane < b)
+            if (bad && lane < b) {
+                int i, j;
+                inner_cols<B2, FULL>(q, rd, i, j);
+                const int lo = i < j ? i : j, hi = i < j ? j : i;
                 atomicMin(&S.fail, pack_err(a.slot_base + slot, slot_pos(lo, b, I, J),
                                             slot_pos(hi, b, I, J)));
+            }
             if (vb) {
                 // the other warps wait round by round: publish the rest of
                 // the pass as failed so none of them waits forever
@@ -725,7 +824,8 @@ __global__ void __launch_bounds__(inner2_threads<B2>()) k_inner(InnerArgs a)
             HSVD_STAMP(2)
             if (vb) break;
             // this pair's diagonal after the round (the bulk's diagonal-block
-            // formulas, so its bits; a skipped pair keeps its entries)
+            // formulas, so its bits; a skipped pair keeps its entries), then
+            // handed to the lanes that hold those positions next round
             const double st = inner_st(t, hyp > 0);
             double nci = a_ii, ncj = a_jj;
             if (act) {
@@ -734,19 +834,16 @@ __global__ void __launch_bounds__(inner2_threads<B2>()) k_inner(InnerArgs a)
                 nci = fma(st, y10, y00) * c;
                 ncj = fma(t, y01, y11) * c;
             }
-            // next round's pair and where its two diagonal entries are now
-            const int rdn = rd + 1 == rounds ? 0 : rd + 1;
-            inner_cols<B2, FULL>(q, rdn, i, j);
-            int pi, pj;
-            bool ri, rj;
-            inner_pair_of<B2, FULL>(i, rd, pi, ri);
-            inner_pair_of<B2, FULL>(j, rd, pj, rj);
-            const double xi = __shfl_sync(0xffffffffu, nci, pi), yi = __shfl_sync(0xffffffffu, ncj, pi);
-            const double xj = __shfl_sync(0xffffffffu, nci, pj), yj = __shfl_sync(0xffffffffu, ncj, pj);
+            const double xi = __shfl_sync(0xffffffffu, nci, si), yi = __shfl_sync(0xffffffffu, ncj, si);
+            const double xj = __shfl_sync(0xffffffffu, nci, sj), yj = __shfl_sync(0xffffffffu, ncj, sj);
             dci = ri ? yi : xi;
             dcj = rj ? yj : xj;
-            if (va) lbuf ^= 1;  // the bulk writes S_it into the other buffer
-            rd = rdn;
+            jpos = inner_next_mask<B2, FULL>(jpos);
+            if (va) {  // the bulk writes S_it into the other buffer, at epoch it+1
+                lbuf ^= 1;
+                ep = it + 1;
+            }
+            rd = rd + 1 == rounds ? 0 : rd + 1;
             HSVD_STAMP(6)
             // the last round's critical signal is consumed too (balanced barrier)
             if (it + 1 == total) named_bar_sync(kBarCrit, 32 + C::NCW * 32);
@@ -757,7 +854,7 @@ __global__ void __launch_bounds__(inner2_threads<B2>()) k_inner(InnerArgs a)
         // (the rest of the upper triangle's blocks), larger d are dead slots;
         // p is the same in every slot.  Slot 0 of groups 1 and 2 (d = 1, 2)
         // holds the blocks the leader's next pivots come from: it is done
-        // first and signalled (crit)
+        // first and signalled
         constexpr int G = C::G, NB = C::NB;
         static_assert(G >= 3, "k_inner: the critical blocks need d = 1, 2 in slot 0");
         const int bt = atid - 32;
@@ -767,14 +864,31 @@ __global__ void __launch_bounds__(inner2_threads<B2>()) k_inner(InnerArgs a)
         const bool critg = bt / 32 >= C::CW0 && bt / 32 < C::CW0 + C::NCW;
         int qk[NB];
         bool dg[NB], live[NB];
+        // positions of the slots' four entries (rows of pair p, columns of
+        // pair q; a diagonal block is (up,up) (up,vp) (vp,up) (vp,vp)), their
+        // offsets in this round's copy (no lag) and in the next round's
+        int up, vp;
+        inner_ppos<B2, FULL>(pk, up, vp);
+        int er[NB][4], ec[NB][4], orr[NB][4], ow[NB][4];
 #pragma unroll
         for (int k = 0; k < NB; ++k) {
             const int d = g + G * k;
             live[k] = d < b / 2 || (d == b / 2 && pk < b / 2);
-            qk[k] = (pk + (live[k] ? d : 0)) % b;  // dead slots reload block (p, p)
+            qk[k] = (pk + (live[k] ? d : 0)) % b;  // dead slots use block (p, p)
             dg[k] = qk[k] == pk;
+            int uq, vq;
+            inner_ppos<B2, FULL>(qk[k], uq, vq);
+            const int rr[4] = {up, up, vp, vp}, cc[4] = {uq, vq, uq, vq};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                er[k][e] = rr[e];
+                ec[k][e] = cc[e];
+                orr[k][e] = inner_canon<B2>(rr[e], cc[e]);
+                ow[k][e] = inner_canon<B2>(inner_next<B2, FULL>(rr[e]), inner_next<B2, FULL>(cc[e]));
+            }
         }
-        int cb = 0;  // buffer holding S_{it-1}
+        int cb = 0, ep = 0;  // buffer holding S_{it-1}, and its epoch
+        int orl[NB][4];      // read offsets of a lagging copy
         int rd = 0;
         long long *btr = (a.trace && blockIdx.x == 0 && tid == 32) ? a.trace + 1024 : nullptr;
         for (int it = 0; it < total; ++it, rd = rd + 1 == rounds ? 0 : rd + 1) {
@@ -789,23 +903,21 @@ __global__ void __launch_bounds__(inner2_threads<B2>()) k_inner(InnerArgs a)
                 // q); blocks whose two pairs both skipped are copied through
                 const double *Ar = S.A[cb];
                 double *Aw = S.A[cb ^ 1];
+                const bool lagging = it != ep;  // warp-uniform
+                if (lagging) {
+                    const int lag = inner_lag<B2, FULL>(it - ep);
+#pragma unroll
+                    for (int k = 0; k < NB; ++k)
+#pragma unroll
+                        for (int e = 0; e < 4; ++e)
+                            orl[k][e] = inner_canon<B2>(inner_prev<B2, FULL>(er[k][e], lag),
+                                                        inner_prev<B2, FULL>(ec[k][e], lag));
+                }
                 const unsigned hm = S.lhyp[rd];
-                int ip, jp;
-                inner_cols<B2, FULL>(pk, rd, ip, jp);
                 const double2 tcp = S.ltc[rd][pk];
                 const double tp = tcp.x, cp = tcp.y, sp = inner_st(tp, (hm >> pk) & 1u);
-                auto slot_offsets = [&](int k, int (&o)[4]) {
-                    int iq, jq;
-                    inner_cols<B2, FULL>(qk[k], rd, iq, jq);
-                    // canonical [min][max] offsets of (ip,iq) (ip,jq) (jp,iq) (jp,jq);
-                    // a diagonal block is (ip,ip) (ip,jp) (jp,ip) (jp,jp)
-                    o[0] = dg[k] ? ip * (LDA + 1) : min(ip, iq) * LDA + max(ip, iq);
-                    o[1] = min(ip, jq) * LDA + max(ip, jq);
-                    o[2] = min(jp, iq) * LDA + max(jp, iq);
-                    o[3] = dg[k] ? jp * (LDA + 1) : min(jp, jq) * LDA + max(jp, jq);
-                };
-                auto slot_apply = [&](int k, const int (&o)[4], const double (&x)[4], double tq,
-                                      double cq, double sq) {
+                auto read_off = [&](int k, int e) { return lagging ? orl[k][e] : orr[k][e]; };
+                auto slot_apply = [&](int k, const double (&x)[4], double tq, double cq, double sq) {
                     double n0 = x[0], n1 = x[1], n2 = x[2], n3 = x[3];
                     if (!(tp == 0.0 && tq == 0.0)) {
                         const double y00 = fma(sq, x[1], x[0]) * cq;
@@ -817,41 +929,38 @@ __global__ void __launch_bounds__(inner2_threads<B2>()) k_inner(InnerArgs a)
                         n1 = dg[k] ? 0.0 : fma(sp, y11, y01) * cp;  // the pair itself: annihilated
                         n2 = fma(tp, y00, y10) * cp;
                     }
-                    Aw[o[0]] = n0;
-                    Aw[o[3]] = n3;
-                    Aw[o[1]] = n1;
-                    if (!dg[k]) Aw[o[2]] = n2;
+                    Aw[ow[k][0]] = n0;
+                    Aw[ow[k][3]] = n3;
+                    Aw[ow[k][1]] = n1;
+                    if (!dg[k]) Aw[ow[k][2]] = n2;
                 };
                 // slot 0 first (the critical blocks), then the others batched
                 {
-                    int o[4];
                     double x[4];
-                    slot_offsets(0, o);
                     const double2 tcq = S.ltc[rd][qk[0]];
                     const double sq = inner_st(tcq.x, (hm >> qk[0]) & 1u);
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) x[u] = Ar[o[u]];
-                    if (live[0]) slot_apply(0, o, x, tcq.x, tcq.y, sq);
+                    for (int u = 0; u < 4; ++u) x[u] = Ar[read_off(0, u)];
+                    if (live[0]) slot_apply(0, x, tcq.x, tcq.y, sq);
                 }
                 if (critg) named_bar_arrive(kBarCrit, 32 + C::NCW * 32);  // release: S_it's critical blocks
-                int o[NB][4];
                 double x[NB][4], tq[NB], cq[NB], sq[NB];
 #pragma unroll
                 for (int k = 1; k < NB; ++k) {
-                    slot_offsets(k, o[k]);
                     const double2 tcq = S.ltc[rd][qk[k]];
                     tq[k] = tcq.x;
                     cq[k] = tcq.y;
                     sq[k] = inner_st(tcq.x, (hm >> qk[k]) & 1u);
                     if (live[k]) {
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) x[k][u] = Ar[o[k][u]];
+                        for (int u = 0; u < 4; ++u) x[k][u] = Ar[read_off(k, u)];
                     }
                 }
 #pragma unroll
                 for (int k = 1; k < NB; ++k)
-                    if (live[k]) slot_apply(k, o[k], x[k], tq[k], cq[k], sq[k]);
+                    if (live[k]) slot_apply(k, x[k], tq[k], cq[k], sq[k]);
                 cb ^= 1;
+                ep = it + 1;
             } else if (critg) {
                 named_bar_arrive(kBarCrit, 32 + C::NCW * 32);  // nothing moved: S_it = S_{it-1}
             }
