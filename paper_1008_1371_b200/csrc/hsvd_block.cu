@@ -444,7 +444,13 @@ static int block_drive_t(double *G, int64_t n, int64_t r, int64_t ldg, double *V
         return !(e && e[0] == '0');
     }();
     bool plan_now = false;
+    // dense (eager, split) sweeps may run more inner passes than the graphed
+    // late sweeps: HSVD_DENSE_PASSES (default: cfg->inner_passes everywhere)
+    hsvd_config cfg_dense = *cfg;
+    if (const char *e = getenv("HSVD_DENSE_PASSES")) cfg_dense.inner_passes = atoi(e) > 1 ? atoi(e) : 1;
+    bool capturing = false;
     auto enqueue_steps_split = [&]() -> int {
+        const hsvd_config *scfg = capturing ? cfg : &cfg_dense;
         cudaStream_t ss[2] = {s, s2};
         if (tl_on) {
             HSVD_CUDA(cudaEventCreate(&tl0));
@@ -466,7 +472,7 @@ static int block_drive_t(double *G, int64_t n, int64_t r, int64_t ldg, double *V
                 const std::string tag = std::string(h ? "B" : "A") + std::to_string(step);
                 int e = mark(tag + " start", ss[h]);
                 if (e) return e;
-                e = K::gram_inner(G, ldg, (int)n, hw, full, cfg, ss[h], T, (int)step, plan_now);
+                e = K::gram_inner(G, ldg, (int)n, hw, full, scfg, ss[h], T, (int)step, plan_now);
                 if (e) return e;
                 if (step == 0 && h == 0) HSVD_CUDA(cudaEventRecord(ev_stagger, ss[h]));
                 if ((e = mark(tag + " gram+inner done", ss[h]))) return e;
@@ -544,11 +550,13 @@ static int block_drive_t(double *G, int64_t n, int64_t r, int64_t ldg, double *V
         const bool keep = split_now;
         split_now = late_split;
         plan_now = reuse_ok;
+        capturing = true;
         HSVD_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
         int e = enqueue_sweep();
         cudaError_t ce = cudaStreamEndCapture(s, &graph);
         split_now = keep;
         plan_now = false;
+        capturing = false;
         if (e) return e;
         if (ce != cudaSuccess) return cuda_fail(ce, "cudaStreamEndCapture");
         HSVD_CUDA(cudaGraphInstantiate(&exec, graph, 0));
