@@ -39,6 +39,18 @@
 #ifndef HSVD_INNER_DIAG_NOUPD
 #define HSVD_INNER_DIAG_NOUPD 0
 #endif
+// HSVD_INNER_COMPACT: half-row W, 3 bulk warps, <= 128 registers per thread
+// (32k per CTA, ~99 KB shared): a k_update CTA fits beside the inner CTA
+#ifndef HSVD_INNER_COMPACT
+#define HSVD_INNER_COMPACT 0
+#endif
+#if HSVD_INNER_COMPACT
+#define HSVD_INNER_WHALF 1
+#define HSVD_INNER_BWARPS64H 3
+#define HSVD_INNER_MINB 2
+#else
+#define HSVD_INNER_MINB 1
+#endif
 #ifndef HSVD_INNER_WHALF
 #define HSVD_INNER_WHALF 0  // 1: W rows split over two threads (half rows; measured slower: 1600 vs 1470 cycles per round)
 #endif
@@ -560,7 +572,7 @@ __device__ __forceinline__ void inner_fold(const InnerArgs &a, double *A, int sl
 {
     using C = InnerCfg<B2>;
     constexpr int NT = C::NT, LDA = B2, b = B2 / 2;
-    constexpr int NCHUNK = B2 * B2 / 2, PER = (NCHUNK + NT - 1) / NT, BATCH = 4;
+    constexpr int NCHUNK = B2 * B2 / 2, PER = (NCHUNK + NT - 1) / NT, BATCH = HSVD_INNER_COMPACT ? 1 : 4;
     const double2 *P0 = reinterpret_cast<const double2 *>(a.Apart + (int64_t)slot * a.maxseg * (B2 * B2));
     const int nseg = (int)a.part.NSEG;
     // cross class: the two diagonal blocks come from the cache, only the
@@ -617,7 +629,7 @@ __device__ __forceinline__ void inner_fold(const InnerArgs &a, double *A, int sl
 }
 
 template <int B2, bool FAST, bool FULL>
-__global__ void __launch_bounds__(inner2_threads<B2>()) k_inner(InnerArgs a)
+__global__ void __launch_bounds__(inner2_threads<B2>(), HSVD_INNER_MINB) k_inner(InnerArgs a)
 {
     using C = InnerCfg<B2>;
     constexpr int NA = C::NA, NT = C::NT, LDA = C::LDA, b = C::b;
@@ -869,7 +881,7 @@ __global__ void __launch_bounds__(inner2_threads<B2>()) k_inner(InnerArgs a)
         // offsets in this round's copy (no lag) and in the next round's
         int up, vp;
         inner_ppos<B2, FULL>(pk, up, vp);
-        int er[NB][4], ec[NB][4], orr[NB][4], ow[NB][4];
+        int orr[NB][4], ow[NB][4];
 #pragma unroll
         for (int k = 0; k < NB; ++k) {
             const int d = g + G * k;
@@ -881,8 +893,6 @@ __global__ void __launch_bounds__(inner2_threads<B2>()) k_inner(InnerArgs a)
             const int rr[4] = {up, up, vp, vp}, cc[4] = {uq, vq, uq, vq};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-                er[k][e] = rr[e];
-                ec[k][e] = cc[e];
                 orr[k][e] = inner_canon<B2>(rr[e], cc[e]);
                 ow[k][e] = inner_canon<B2>(inner_next<B2, FULL>(rr[e]), inner_next<B2, FULL>(cc[e]));
             }
@@ -907,11 +917,15 @@ __global__ void __launch_bounds__(inner2_threads<B2>()) k_inner(InnerArgs a)
                 if (lagging) {
                     const int lag = inner_lag<B2, FULL>(it - ep);
 #pragma unroll
-                    for (int k = 0; k < NB; ++k)
+                    for (int k = 0; k < NB; ++k) {
+                        int uq, vq;
+                        inner_ppos<B2, FULL>(qk[k], uq, vq);
+                        const int rr[4] = {up, up, vp, vp}, cc[4] = {uq, vq, uq, vq};
 #pragma unroll
                         for (int e = 0; e < 4; ++e)
-                            orl[k][e] = inner_canon<B2>(inner_prev<B2, FULL>(er[k][e], lag),
-                                                        inner_prev<B2, FULL>(ec[k][e], lag));
+                            orl[k][e] = inner_canon<B2>(inner_prev<B2, FULL>(rr[e], lag),
+                                                        inner_prev<B2, FULL>(cc[e], lag));
+                    }
                 }
                 const unsigned hm = S.lhyp[rd];
                 const double2 tcp = S.ltc[rd][pk];
