@@ -286,6 +286,9 @@ __device__ __forceinline__ void chunk_update(double *x, double *y, int lo, int h
 // the chunk's sequential FMA chain in the reference's order.  The direct
 // per-lane loads of chunk_dot touch 32 sectors per instruction with half of
 // each used, and the second half is refetched once L1 has evicted it.
+#ifndef HSVD_PW_VBATCH  // V^{-T} elements per thread with loads in flight together
+#define HSVD_PW_VBATCH 8
+#endif
 #ifndef HSVD_PW_SLICE  // 8: 43.1 s at n = 8192; 4 (more CTAs per SM): 45.8 s
 #define HSVD_PW_SLICE 8
 #endif
@@ -433,12 +436,31 @@ __global__ void __launch_bounds__(NT) k_pointwise_stream(StepArgs a)
             }
         }
         if (a.V) {
+            // V^{-T} columns: a batch of loads in flight before its stores
+            // (one element at a time, each store had to wait for the next
+            // load: vi and vj may alias as far as the compiler knows)
             double *vi = a.V + ci * a.ldv;
             double *vj = a.V + cj * a.ldv;
-            for (int e = threadIdx.x; e < a.rv; e += NT) {
-                const double xi = vi[e], yi = vj[e];
-                vi[e] = __dmul_rn(__fma_rn(st, yi, xi), c);
-                vj[e] = __dmul_rn(__fma_rn(t, xi, yi), c);
+            const int rv = a.rv;
+            constexpr int VB = HSVD_PW_VBATCH;
+            for (int e0 = threadIdx.x; e0 < rv; e0 += NT * VB) {
+                double xs[VB], ys[VB];
+#pragma unroll
+                for (int u = 0; u < VB; ++u) {
+                    const int e = e0 + u * NT;
+                    if (e < rv) {
+                        xs[u] = vi[e];
+                        ys[u] = vj[e];
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < VB; ++u) {
+                    const int e = e0 + u * NT;
+                    if (e < rv) {
+                        vi[e] = __dmul_rn(__fma_rn(st, ys[u], xs[u]), c);
+                        vj[e] = __dmul_rn(__fma_rn(t, xs[u], ys[u]), c);
+                    }
+                }
             }
         }
         double di, dj;
