@@ -1021,6 +1021,43 @@ __device__ __forceinline__ int rotation_fast(double a_ii, double a_jj, double a_
     return 0;
 }
 
+// rotation_fast without branches, for a warp none of whose operands needs
+// the quotient forms (the caller checks rotation_fast_in_range with a vote):
+// the same operations and results as rotation_fast, with the zero,
+// definiteness and range exits turned into selects, so the operand-only part
+// (d, sm, base) can be scheduled before a_ij arrives
+__device__ __forceinline__ bool rotation_fast_in_range(double a_ii, double a_jj, double a_ij, int hyp)
+{
+    const double ae = fabs(2.0 * a_ij);
+    const double base = hyp > 0 ? a_ii + a_jj : fabs(a_jj - a_ii);
+    const double big = fmax(base, ae);
+    return a_ij == 0.0 || (big < 1e150 && big > 1e-140);
+}
+__device__ __forceinline__ int rotation_fast_sel(double a_ii, double a_jj, double a_ij, int hyp,
+                                                 double &t_out, double &c_out)
+{
+    const bool h = hyp > 0;
+    const double d = a_jj - a_ii, ad = fabs(d), sm = a_ii + a_jj;
+    const double base = h ? sm : ad;
+    const double e = 2.0 * a_ij, ae = fabs(e);
+    const double sg = (d == 0.0 || (d > 0.0) == (e > 0.0)) ? ae : -ae;
+    const double num = h ? -e : sg;
+    const double rad = h ? (sm - ae) * (sm + ae) : fma(d, d, e * e);
+    const bool radok = rad > 0.0;
+    const double w = base + fast_sqrt(radok ? rad : 1.0);
+    const double g = h ? (w - ae) * (w + ae) : fma(w, w, ae * ae);
+    const bool gok = g > 0.0;
+    const double rw = fast_rcp(w);
+    double t = num * rw;
+    t = fma(fma(-w, t, num), rw, t);  // one correction of the quotient
+    const double c = w * fast_rsqrt(gok ? g : 1.0);
+    const bool zero = a_ij == 0.0;
+    const bool bad = !zero && h && !(radok && gok);
+    t_out = zero || bad ? 0.0 : t;
+    c_out = zero || bad ? 1.0 : c;
+    return bad ? 1 : 0;
+}
+
 // k_inner_v1: the round-1 inner pass (both triangles of A and W in shared
 // memory, warp 0 forms the rotations, two barriers per round).  The product
 // runs k_inner (hsvd_inner.cuh); this kernel stays only as the A/B and

@@ -802,8 +802,14 @@ __global__ void __launch_bounds__(inner2_threads<B2>(), HSVD_INNER_MINB) k_inner
             const bool skip = a_ij == 0.0 || (a.use_skip && a_ij * a_ij < thr);
             HSVD_STAMP(5)
             double t, c;
-            const int status = FAST ? rotation_fast(a_ii, a_jj, a_ij, hyp, t, c)
-                                    : rotation_tc(a_ii, a_jj, a_ij, hyp, t, c);
+            int status;
+            if (!FAST) {
+                status = rotation_tc(a_ii, a_jj, a_ij, hyp, t, c);
+            } else if (__all_sync(0xffffffffu, rotation_fast_in_range(a_ii, a_jj, a_ij, hyp))) {
+                status = rotation_fast_sel(a_ii, a_jj, a_ij, hyp, t, c);
+            } else {
+                status = rotation_fast(a_ii, a_jj, a_ij, hyp, t, c);
+            }
             const bool bad = !skip && status != 0, act = !skip && status == 0;
             t = act ? t : 0.0;
             c = act ? c : 1.0;
