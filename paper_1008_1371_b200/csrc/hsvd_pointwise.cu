@@ -287,10 +287,10 @@ __device__ __forceinline__ void chunk_update(double *x, double *y, int lo, int h
 // per-lane loads of chunk_dot touch 32 sectors per instruction with half of
 // each used, and the second half is refetched once L1 has evicted it.
 #ifndef HSVD_PW_VBATCH  // V^{-T} elements per thread with loads in flight together
-#define HSVD_PW_VBATCH 8
+#define HSVD_PW_VBATCH 16
 #endif
-#ifndef HSVD_PW_SLICE  // 8: 43.1 s at n = 8192; 4 (more CTAs per SM): 45.8 s
-#define HSVD_PW_SLICE 8
+#ifndef HSVD_PW_SLICE  // with HSVD_PW_VBATCH 16 (sweep 0 at n = 8192): 16: 3.46 s, 8: 3.76 s, 32: 4.83 s
+#define HSVD_PW_SLICE 16
 #endif
 constexpr int kSlice = HSVD_PW_SLICE, kSliceLd = kSlice + 1;  // padded: conflict-free lane reads
 constexpr int kPpc = kSlice / 2;                              // double2 per chunk per slice
