@@ -449,6 +449,15 @@ static int block_drive_t(double *G, int64_t n, int64_t r, int64_t ldg, double *V
     hsvd_config cfg_dense = *cfg;
     if (const char *e = getenv("HSVD_DENSE_PASSES")) cfg_dense.inner_passes = atoi(e) > 1 ? atoi(e) : 1;
     bool capturing = false;
+    // the graphed late sweeps may use the oriented inner ordering (the full
+    // triangle only at a sweep's first step): HSVD_LATE_ORIENTED=1
+    const bool late_oriented = [] {
+        const char *e = getenv("HSVD_LATE_ORIENTED");
+        return e && e[0] == '1';
+    }();
+    auto inner_full = [&](int64_t step) {
+        return (cfg->inner_full && !(capturing && late_oriented)) || step == 0;
+    };
     auto enqueue_steps_split = [&]() -> int {
         const hsvd_config *scfg = capturing ? cfg : &cfg_dense;
         cudaStream_t ss[2] = {s, s2};
@@ -459,7 +468,7 @@ static int block_drive_t(double *G, int64_t n, int64_t r, int64_t ldg, double *V
         HSVD_CUDA(cudaEventRecord(ev_fork, s));
         HSVD_CUDA(cudaStreamWaitEvent(s2, ev_fork, 0));
         for (int64_t step = 0; step < nb; ++step) {
-            const int full = cfg->inner_full || step == 0;
+            const int full = inner_full(step);
             for (int h = 0; h < 2; ++h) {
                 const SlotWs &hw = w.half[h];
                 const int64_t m = hw.nslots;
@@ -499,7 +508,7 @@ static int block_drive_t(double *G, int64_t n, int64_t r, int64_t ldg, double *V
             if (e) return e;
         } else {
             for (int64_t step = 0; step < nb; ++step) {
-                const int full = cfg->inner_full || step == 0;
+                const int full = inner_full(step);
                 // profile mode plans its eager steps too, so the profiled
                 // sweep sees the Gram classes of a graphed sweep
                 int e = K::step(G, ldg, (int)n, V, ldv, (int)r, w.sl, full, cfg, s, T, (int)step,
