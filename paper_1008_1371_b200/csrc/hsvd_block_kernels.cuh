@@ -962,8 +962,12 @@ __device__ __forceinline__ int rotation_fast_wide(double a_ii, double a_jj, doub
 // two Newton steps (error ~2^-20 -> ~2^-80, i.e. within an ulp or so), for
 // positive normal operands in [1e-300, 1e300].  The library routines carry a
 // slow-path branch each, which keeps the compiler from overlapping them.
+#ifndef HSVD_ROT_LIBM  // 1: the library's correctly rounded sqrt / rsqrt / division
+#define HSVD_ROT_LIBM 0
+#endif
 __device__ __forceinline__ double fast_rcp(double x)
 {
+    if (HSVD_ROT_LIBM) return 1.0 / x;
     double y;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
     double e = fma(-x, y, 1.0);
@@ -973,6 +977,7 @@ __device__ __forceinline__ double fast_rcp(double x)
 }
 __device__ __forceinline__ double fast_rsqrt(double x)
 {
+    if (HSVD_ROT_LIBM) return rsqrt(x);
     double y;
     asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
     double e = fma(-x * y, y, 1.0);  // 1 - x y^2
@@ -982,6 +987,7 @@ __device__ __forceinline__ double fast_rsqrt(double x)
 }
 __device__ __forceinline__ double fast_sqrt(double x)
 {
+    if (HSVD_ROT_LIBM) return sqrt(x);
     const double y = fast_rsqrt(x);
     const double s = x * y;
     return fma(0.5 * y, fma(-s, s, x), s);  // one correction of x y
