@@ -993,6 +993,19 @@ __device__ __forceinline__ double fast_sqrt(double x)
     return fma(0.5 * y, fma(-s, s, x), s);  // one correction of x y
 }
 
+// c of the rotation.  HSVD_ROT_C_FROM_T=1: c = 1/sqrt(1 +- t^2) from the
+// rounded t with the library's reciprocal square root (the round-1 form:
+// each (t, c) pair J-orthogonal to the last bits); 0: c = w / sqrt(w^2 +- e^2)
+// beside the quotient (one long operation fewer on the chain)
+#ifndef HSVD_ROT_C_FROM_T
+#define HSVD_ROT_C_FROM_T 1
+#endif
+__device__ __forceinline__ double rot_c(double t, bool h, double w, double g)
+{
+    if (HSVD_ROT_C_FROM_T) return rsqrt(fma(h ? -t : t, t, 1.0));
+    return w * fast_rsqrt(g);
+}
+
 // The trigonometric and hyperbolic forms share one square root, one
 // reciprocal and one reciprocal square root, selected per lane: a warp whose
 // pairs mix both kinds (every pivot block that straddles the sign boundary)
@@ -1023,7 +1036,7 @@ __device__ __forceinline__ int rotation_fast(double a_ii, double a_jj, double a_
     double t = num * rw;
     t = fma(fma(-w, t, num), rw, t);  // one correction of the quotient
     t_out = t;
-    c_out = w * fast_rsqrt(g);
+    c_out = rot_c(t, h, w, g);
     return 0;
 }
 
@@ -1056,7 +1069,7 @@ __device__ __forceinline__ int rotation_fast_sel(double a_ii, double a_jj, doubl
     const double rw = fast_rcp(w);
     double t = num * rw;
     t = fma(fma(-w, t, num), rw, t);  // one correction of the quotient
-    const double c = w * fast_rsqrt(gok ? g : 1.0);
+    const double c = rot_c(t, h, w, gok ? g : 1.0);
     const bool zero = a_ij == 0.0;
     const bool bad = !zero && h && !(radok && gok);
     t_out = zero || bad ? 0.0 : t;
