@@ -975,6 +975,15 @@ __device__ __forceinline__ double fast_rcp(double x)
     e = fma(-x, y, 1.0);
     return fma(y, e, y);
 }
+// 1/x to ~2^-45 (seed + one Newton step): enough ahead of a quotient's
+// correction step, which squares the error
+__device__ __forceinline__ double rcp_nr1(double x)
+{
+    if (HSVD_ROT_LIBM) return 1.0 / x;
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    return fma(y, fma(-x, y, 1.0), y);
+}
 __device__ __forceinline__ double fast_rsqrt(double x)
 {
     if (HSVD_ROT_LIBM) return rsqrt(x);
@@ -992,7 +1001,11 @@ __device__ __forceinline__ double fast_rsqrt(double x)
 __device__ __forceinline__ double fast_sqrt(double x)
 {
     if (HSVD_ROT_LIBM) return sqrt(x);
-    const double y = fast_rsqrt(x);
+    // one Newton step of 1/sqrt(x) (~2^-45) suffices before the correction
+    // of x y (the correction squares the error)
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    y = fma(0.5 * y, fma(-x * y, y, 1.0), y);
     const double s = x * y;
     return fma(0.5 * y, fma(-s, s, x), s);  // one correction of x y
 }
@@ -1036,7 +1049,7 @@ __device__ __forceinline__ int rotation_fast(double a_ii, double a_jj, double a_
     const double w = base + fast_sqrt(rad);
     const double g = h ? (w - ae) * (w + ae) : fma(w, w, ae * ae);
     if (h && !(g > 0.0)) return 1;
-    const double rw = fast_rcp(w);
+    const double rw = rcp_nr1(w);
     double t = num * rw;
     t = fma(fma(-w, t, num), rw, t);  // one correction of the quotient
     t_out = t;
@@ -1070,7 +1083,7 @@ __device__ __forceinline__ int rotation_fast_sel(double a_ii, double a_jj, doubl
     const double w = base + fast_sqrt(radok ? rad : 1.0);
     const double g = h ? (w - ae) * (w + ae) : fma(w, w, ae * ae);
     const bool gok = g > 0.0;
-    const double rw = fast_rcp(w);
+    const double rw = rcp_nr1(w);
     double t = num * rw;
     t = fma(fma(-w, t, num), rw, t);  // one correction of the quotient
     const double c = rot_c(t, h, w, gok ? g : 1.0);
