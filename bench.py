@@ -53,7 +53,7 @@ def parse():
     ap.add_argument("--block-cols", type=int, default=32)
     ap.add_argument("--block-rotation", default="fast", choices=["fast", "dd"])
     ap.add_argument("--inner-ordering", default="full", choices=["oriented", "full"])
-    ap.add_argument("--inner-passes", type=int, default=1)
+    ap.add_argument("--inner-passes", type=int, default=0)
     ap.add_argument("--block-streams", type=int, default=2)
     ap.add_argument("--cpu-sample-s", type=float, default=12.0)
     ap.add_argument("--e2e-steps", type=int, default=1)

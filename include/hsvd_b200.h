@@ -69,8 +69,9 @@ typedef struct hsvd_config {
                              (no graph); fills hsvd_result.kernel_ms     */
     int32_t block_rotation; /* block mode: HSVD_ROTATION_*               */
     int32_t inner_passes;   /* block mode: passes of the inner ordering
-                               per step (1 = one pass, the paper's block-
-                               oriented scheme; more = toward full-block) */
+                               per step; 0 = auto (default): 2 in the dense
+                               sweeps, 1 once a sweep rotates < 5 % of its
+                               visits; >= 1: that count in every sweep    */
     int32_t block_streams;  /* block mode, one GPU: 2 = the slots run as two
                                halves on two streams, each half's step
                                waiting only for the other half's edge slots,

@@ -444,11 +444,12 @@ static int block_drive_t(double *G, int64_t n, int64_t r, int64_t ldg, double *V
         return !(e && e[0] == '0');
     }();
     bool plan_now = false;
-    // dense (eager, split) sweeps may run more inner passes than the graphed
-    // late sweeps: HSVD_DENSE_PASSES (default: cfg->inner_passes everywhere)
-    hsvd_config cfg_dense = *cfg;
-    if (const char *e = getenv("HSVD_DENSE_PASSES")) cfg_dense.inner_passes = atoi(e) > 1 ? atoi(e) : 1;
+    // inner passes: 2 in the dense sweeps, 1 in the late ones by default
+    // (PassPolicy); the late-sweep graph is captured with the late count
+    PassPolicy passes;
+    passes.init(cfg, nb);
     bool capturing = false;
+    auto scfg_now = [&]() { return capturing ? &passes.late : passes.now(); };
     // the graphed late sweeps may use the oriented inner ordering (the full
     // triangle only at a sweep's first step): HSVD_LATE_ORIENTED=1
     const bool late_oriented = [] {
@@ -459,7 +460,7 @@ static int block_drive_t(double *G, int64_t n, int64_t r, int64_t ldg, double *V
         return (cfg->inner_full && !(capturing && late_oriented)) || step == 0;
     };
     auto enqueue_steps_split = [&]() -> int {
-        const hsvd_config *scfg = capturing ? cfg : &cfg_dense;
+        const hsvd_config *scfg = scfg_now();
         cudaStream_t ss[2] = {s, s2};
         if (tl_on) {
             HSVD_CUDA(cudaEventCreate(&tl0));
@@ -511,8 +512,8 @@ static int block_drive_t(double *G, int64_t n, int64_t r, int64_t ldg, double *V
                 const int full = inner_full(step);
                 // profile mode plans its eager steps too, so the profiled
                 // sweep sees the Gram classes of a graphed sweep
-                int e = K::step(G, ldg, (int)n, V, ldv, (int)r, w.sl, full, cfg, s, T, (int)step,
-                                plan_now || (cfg->profile && reuse_ok));
+                int e = K::step(G, ldg, (int)n, V, ldv, (int)r, w.sl, full, scfg_now(), s, T,
+                                (int)step, plan_now || (cfg->profile && reuse_ok));
                 if (e) return e;
             }
         }
@@ -571,10 +572,7 @@ static int block_drive_t(double *G, int64_t n, int64_t r, int64_t ldg, double *V
         HSVD_CUDA(cudaGraphInstantiate(&exec, graph, 0));
         return HSVD_OK;
     };
-    if (graphs && !split) {
-        st = capture();
-        if (st) return st;
-    }
+
     const int64_t mv = V ? 4 : 2;  // k_move_cols launches per column move
     int64_t launches = (V ? 1 : 0) + 1 + 1 + 1 + (cfg->sort ? 2 : 0) + 1 + 2 + mv + 1 + mv;
     int64_t sweeps_used = 0, total_rot = 0, total_skip = 0;
@@ -586,18 +584,20 @@ static int block_drive_t(double *G, int64_t n, int64_t r, int64_t ldg, double *V
         {
             // kernels per step: split = 2 x (gram, inner, 3 updates), one
             // stream = gram, inner, update; graphed sweeps add k_plan per launch
-            const bool graphed = graphs && !split_now;
+            const bool graphed = graphs && !split_now && !passes.dense_now;
             const int64_t per_step = (split_now || (graphed && late_split)) ? 10 : 3;
             const int64_t plans = graphed && reuse_ok ? (late_split ? 2 : 1) : 0;
             launches += (per_step + plans) * nb + 1 + 1 + (cfg->sort ? 4 + mv : 0) + 1;
         }
-        if (split_now || !graphs) {
+        // the dense sweeps run eagerly (their inner passes differ from the
+        // late sweeps'); the late sweeps replay a graph
+        if (split_now || !graphs || passes.dense_now) {
             T.on = cfg->profile && sweep == profile_sweep();
             st = enqueue_sweep();
             if (st) return st;
-            // capture the one-stream graph for the late sweeps while the
-            // device works through this sweep
-            if (split_now && graphs && !exec) {
+            // capture the graph for the late sweeps while the device works
+            // through this sweep
+            if (graphs && !exec) {
                 st = capture();
                 if (st) return st;
             }
@@ -639,6 +639,7 @@ static int block_drive_t(double *G, int64_t n, int64_t r, int64_t ldg, double *V
         total_skip += host[2];
         // few rotations left: the remaining sweeps skip most updates
         if (split_now && host[1] < (host[1] + host[2]) / 20) split_now = false;
+        passes.after_sweep(host[1], host[2]);
         if (tele) {
             tele[sweep].sweep = sweep;
             tele[sweep].rotations = host[1];

@@ -426,7 +426,7 @@ void hsvd_default_config(hsvd_config *cfg)
     cfg->inner_full = 1;
     cfg->use_graph = 1;
     cfg->block_rotation = HSVD_ROTATION_FAST;
-    cfg->inner_passes = 1;
+    cfg->inner_passes = 0;  /* auto: 2 in the dense sweeps, 1 in the late ones */
     cfg->block_streams = 2;
 }
 

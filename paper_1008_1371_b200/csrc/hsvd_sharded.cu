@@ -492,6 +492,7 @@ struct ShardedDriver {
     ShardPlan pl;
     int64_t n, r, ldg, p;
     const hsvd_config *cfg;
+    PassPolicy passes;  // inner passes per sweep (the one-GPU driver's policy)
     bool withV;
     // pinned host memory: [0, rho_off) per-shard stats, [rho_off, stage_base)
     // a copy of rho, then the staging of the uploads of one sync epoch
@@ -861,7 +862,8 @@ struct ShardedDriver {
                         HSVD_CUDA(cudaStreamWaitEvent(ss[h], x.e_stag, 0));
                     }
                     double *V = withV ? x.w.Vs : nullptr;
-                    HSVD_CUDA_OK(K::gram_inner(x.w.Gs, n, (int)n, hw, full, cfg, ss[h], Toff, (int)step, false));
+                    HSVD_CUDA_OK(K::gram_inner(x.w.Gs, n, (int)n, hw, full, passes.now(), ss[h], Toff,
+                                               (int)step, false));
                     if (step == 0 && h == 0) HSVD_CUDA(cudaEventRecord(x.e_stag, ss[h]));
                     HSVD_CUDA_OK(K::update(x.w.Gs, n, (int)n, V, r, (int)r, hw, 0, 1, ss[h], Toff,
                                            true));
@@ -954,6 +956,7 @@ struct ShardedDriver {
     {
         const int64_t nb = r / b;
         HSVD_CUDA_OK(pl.init(nb, (int)(comm ? comm->nranks : sh.size())));
+        passes.init(cfg, nb);
         split = cfg->block_streams >= 2 && !cfg->profile;
         for (auto &x : sh)
             if (pl.m(x.g) < 4) split = false;
@@ -1088,7 +1091,7 @@ struct ShardedDriver {
                     for (auto &x : sh) {
                         HSVD_CUDA(cudaSetDevice(x.dev));
                         HSVD_CUDA_OK(K::step(x.w.Gs, n, (int)n, withV ? x.w.Vs : nullptr, r,
-                                             (int)r, x.w.sl, full, cfg, x.s,
+                                             (int)r, x.w.sl, full, passes.now(), x.s,
                                              &x == &sh[0] ? T : Toff, (int)step, false));
                         launches += 3;
                     }
@@ -1134,6 +1137,7 @@ struct ShardedDriver {
             sweeps_used = sweep + 1;
             total_rot += o[1];
             total_skip += o[2];
+            passes.after_sweep(o[1], o[2]);
             if (tele) {
                 tele[sweep].sweep = sweep;
                 tele[sweep].rotations = o[1];

@@ -63,8 +63,9 @@ class SolverConfig:
     #: block mode 2x2 rotation: "fast" (plain fp64) or "dd" (the reference's
     #: double-double rotation_tc, _kernels.py:128-173)
     block_rotation: str = "fast"
-    #: block mode: passes of the inner ordering per step
-    inner_passes: int = 1
+    #: block mode: passes of the inner ordering per step; 0 = auto (2 in the
+    #: dense sweeps, 1 once a sweep rotates < 5 % of its visits)
+    inner_passes: int = 0
     #: block mode on one GPU: 2 = two half-slot streams (inner passes overlap
     #: GEMMs), 1 = one stream
     block_streams: int = 2
@@ -84,8 +85,8 @@ class SolverConfig:
             raise ValueError("block_cols must be 16 or 32")
         if self.block_streams not in (1, 2):
             raise ValueError("block_streams must be 1 or 2")
-        if self.inner_passes < 1:
-            raise ValueError("inner_passes must be >= 1")
+        if self.inner_passes < 0:
+            raise ValueError("inner_passes must be >= 0 (0: auto)")
         if self.block_rotation not in ("fast", "dd"):
             raise ValueError(f"unknown block_rotation {self.block_rotation!r}")
 
