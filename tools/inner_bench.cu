@@ -115,7 +115,7 @@ int main(int argc, char **argv)
     ia.ip = dip; ia.jp = djp; ia.iblk = dib; ia.jblk = djb; ia.cur = dcur;
     ia.C = dC; ia.tset = dts; ia.rotk = drot; ia.skipk = dskip; ia.maxt = dmaxt; ia.err = derr;
     ia.nb = nb; ia.slot_base = 0; ia.eps = 0x1p-52; ia.teps = 0x1p-27;
-    ia.full = full; ia.use_skip = 1; ia.passes = 1; ia.trace = nullptr;
+    ia.full = full; ia.use_skip = 1; ia.passes = argc > 6 ? atoi(argv[6]) : 1; ia.trace = nullptr;
     ia.colmap = dcolmap; ia.colidx = dcolidx;
     ia.orig = dcolmap; ia.real_cols = r; ia.skipf = nullptr;
     const size_t smem = sizeof(InnerSmem<B2>), smem_reg = sizeof(InnerRegSmem);
@@ -191,6 +191,9 @@ int main(int argc, char **argv)
                 long long *t = &tr[8 * it];
                 s07 += t[7] - t[0]; s75 += t[5] - t[7]; s26 += t[6] - t[2];
             }
+            if (ia.passes > 1 && rounds < 64)
+                printf("  k_inner pass boundary: round %d start -> pivots %lld cycles (round 1: %lld)\n", rounds,
+                       tr[8 * rounds + 5] - tr[8 * rounds], tr[8 * 1 + 5] - tr[8 * 1]);
             printf("  k_inner leader: wait crit %.0f, a_ij + skip test %.0f, after publish %.0f\n",
                    s07 / (rounds - 1), s75 / (rounds - 1), s26 / (rounds - 1));
             double b01 = 0, b12 = 0, b23 = 0, bper = 0;
