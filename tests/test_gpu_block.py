@@ -253,3 +253,29 @@ def test_block_inner_schedules(ordering, passes, b):
                     H.SolverConfig(mode="block", block_cols=b, inner_ordering=ordering,
                                    inner_passes=passes))
     assert np.array_equal(again.U, res.U) and np.array_equal(again.sigma, res.sigma)
+
+
+def test_block_auto_inner_passes():
+    """inner_passes = 0 (auto, default): two passes per step in the dense
+    sweeps for >= 32 block columns, one pass for small problems.  At r = 256
+    (8 blocks) auto is exactly the one-pass solve; at r = 1024 (32 blocks) it
+    is not, and it meets the same sigma / residual gates against the oracle
+    in no more sweeps."""
+    def solve(n, r, p, passes):
+        G = make_case_input(n, r, 11, "gauss")
+        signs = np.array([1] * p + [-1] * (r - p), np.int8)
+        return G, signs, H.drive(G, H.SignatureVector(signs, p),
+                                 H.SolverConfig(mode="block", inner_passes=passes))
+
+    _, _, a = solve(256, 256, 100, 0)
+    _, _, one = solve(256, 256, 100, 1)
+    assert np.array_equal(a.U, one.U) and a.sweeps_used == one.sweeps_used
+    G, signs, auto = solve(1024, 1024, 400, 0)
+    _, _, one = solve(1024, 1024, 400, 1)
+    assert not np.array_equal(auto.U, one.U)
+    assert auto.sweeps_used <= one.sweeps_used
+    ref = O.drive(G, signs, 400)
+    assert sigma_class_reldiff(auto.sigma, auto.lam, ref.sigma, ref.lam) <= SIGMA_RTOL
+    rb, rr = residuals(G, auto, signs), residuals(G, ref, signs)
+    for k in rb:
+        assert rb[k] <= rr[k], (k, rb[k], rr[k])
