@@ -1859,11 +1859,13 @@ struct PassPolicy {
             late.inner_passes = 1;
         }
         if (const char *e = getenv("HSVD_DENSE_PASSES")) dense.inner_passes = atoi(e) > 1 ? atoi(e) : 1;
+        if (const char *e = getenv("HSVD_DENSE_DIV")) div = atoi(e) > 1 ? atoi(e) : 20;
     }
+    int64_t div = 20;  // dense while a sweep rotates >= 1/div of its visits
     const hsvd_config *now() const { return dense_now ? &dense : &late; }
     void after_sweep(int64_t rot, int64_t skip)
     {
-        if (dense_now && rot < (rot + skip) / 20) dense_now = false;
+        if (dense_now && rot < (rot + skip) / div) dense_now = false;
     }
 };
 
