@@ -51,6 +51,9 @@
 #else
 #define HSVD_INNER_MINB 1
 #endif
+#ifndef HSVD_INNER_PRE0  // bulk: the critical slot's entries loaded before the round's rotations
+#define HSVD_INNER_PRE0 1
+#endif
 #ifndef HSVD_INNER_WHALF
 #define HSVD_INNER_WHALF 0  // 1: W rows split over two threads (half rows; measured slower: 1600 vs 1470 cycles per round)
 #endif
@@ -909,6 +912,27 @@ __global__ void __launch_bounds__(inner2_threads<B2>(), HSVD_INNER_MINB) k_inner
         long long *btr = (a.trace && blockIdx.x == 0 && tid == 32) ? a.trace + 1024 : nullptr;
         for (int it = 0; it < total; ++it, rd = rd + 1 == rounds ? 0 : rd + 1) {
             if (btr && it < 64) btr[8 * it] = clock64();
+#if HSVD_INNER_PRE0
+            // the critical slot's four entries do not depend on the round's
+            // rotations: loaded before the leader publishes them
+            double x0[4];
+            {
+                const double *Ar = S.A[cb];
+                if (it == ep) {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) x0[e] = Ar[orr[0][e]];
+                } else {
+                    const int lag = inner_lag<B2, FULL>(it - ep);
+                    int uq, vq;
+                    inner_ppos<B2, FULL>(qk[0], uq, vq);
+                    const int rr[4] = {up, up, vp, vp}, cc[4] = {uq, vq, uq, vq};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                        x0[e] = Ar[inner_canon<B2>(inner_prev<B2, FULL>(rr[e], lag),
+                                                   inner_prev<B2, FULL>(cc[e], lag))];
+                }
+            }
+#endif
             named_bar_sync(kBarRound, 32 + C::NBT);  // the leader published round it
             if (btr && it < 64) btr[8 * it + 1] = clock64();
             if (btr && it < 64) btr[8 * it + 2] = clock64();
@@ -956,12 +980,16 @@ __global__ void __launch_bounds__(inner2_threads<B2>(), HSVD_INNER_MINB) k_inner
                 };
                 // slot 0 first (the critical blocks), then the others batched
                 {
-                    double x[4];
                     const double2 tcq = S.ltc[rd][qk[0]];
                     const double sq = inner_st(tcq.x, (hm >> qk[0]) & 1u);
+#if HSVD_INNER_PRE0
+                    if (live[0]) slot_apply(0, x0, tcq.x, tcq.y, sq);
+#else
+                    double x[4];
 #pragma unroll
                     for (int u = 0; u < 4; ++u) x[u] = Ar[read_off(0, u)];
                     if (live[0]) slot_apply(0, x, tcq.x, tcq.y, sq);
+#endif
                 }
                 if (critg) named_bar_arrive(kBarCrit, 32 + C::NCW * 32);  // release: S_it's critical blocks
                 double x[NB][4], tq[NB], cq[NB], sq[NB];
