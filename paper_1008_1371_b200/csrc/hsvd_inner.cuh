@@ -52,7 +52,7 @@
 #define HSVD_INNER_MINB 1
 #endif
 #ifndef HSVD_INNER_PRE0  // bulk: the critical slot's entries loaded before the round's rotations
-#define HSVD_INNER_PRE0 1
+#define HSVD_INNER_PRE0 1  // slots prefetched; 2: 1403, 4: 1455 cycles per round (1: 1392)
 #endif
 #ifndef HSVD_INNER_WHALF
 #define HSVD_INNER_WHALF 0  // 1: W rows split over two threads (half rows; measured slower: 1600 vs 1470 cycles per round)
@@ -913,23 +913,34 @@ __global__ void __launch_bounds__(inner2_threads<B2>(), HSVD_INNER_MINB) k_inner
         for (int it = 0; it < total; ++it, rd = rd + 1 == rounds ? 0 : rd + 1) {
             if (btr && it < 64) btr[8 * it] = clock64();
 #if HSVD_INNER_PRE0
-            // the critical slot's four entries do not depend on the round's
-            // rotations: loaded before the leader publishes them
-            double x0[4];
+            // the first HSVD_INNER_PRE0 slots' entries (the critical slot
+            // first) do not depend on the round's rotations: loaded before
+            // the leader publishes them
+            constexpr int NPRE = HSVD_INNER_PRE0 < NB ? HSVD_INNER_PRE0 : NB;
+            double xp[NPRE][4];
             {
                 const double *Ar = S.A[cb];
                 if (it == ep) {
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) x0[e] = Ar[orr[0][e]];
+                    for (int k = 0; k < NPRE; ++k)
+                        if (live[k]) {
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) xp[k][e] = Ar[orr[k][e]];
+                        }
                 } else {
                     const int lag = inner_lag<B2, FULL>(it - ep);
-                    int uq, vq;
-                    inner_ppos<B2, FULL>(qk[0], uq, vq);
-                    const int rr[4] = {up, up, vp, vp}, cc[4] = {uq, vq, uq, vq};
 #pragma unroll
-                    for (int e = 0; e < 4; ++e)
-                        x0[e] = Ar[inner_canon<B2>(inner_prev<B2, FULL>(rr[e], lag),
-                                                   inner_prev<B2, FULL>(cc[e], lag))];
+                    for (int k = 0; k < NPRE; ++k) {
+                        int uq, vq;
+                        inner_ppos<B2, FULL>(qk[k], uq, vq);
+                        const int rr[4] = {up, up, vp, vp}, cc[4] = {uq, vq, uq, vq};
+                        if (live[k]) {
+#pragma unroll
+                            for (int e = 0; e < 4; ++e)
+                                xp[k][e] = Ar[inner_canon<B2>(inner_prev<B2, FULL>(rr[e], lag),
+                                                              inner_prev<B2, FULL>(cc[e], lag))];
+                        }
+                    }
                 }
             }
 #endif
@@ -983,7 +994,7 @@ __global__ void __launch_bounds__(inner2_threads<B2>(), HSVD_INNER_MINB) k_inner
                     const double2 tcq = S.ltc[rd][qk[0]];
                     const double sq = inner_st(tcq.x, (hm >> qk[0]) & 1u);
 #if HSVD_INNER_PRE0
-                    if (live[0]) slot_apply(0, x0, tcq.x, tcq.y, sq);
+                    if (live[0]) slot_apply(0, xp[0], tcq.x, tcq.y, sq);
 #else
                     double x[4];
 #pragma unroll
@@ -1000,6 +1011,13 @@ __global__ void __launch_bounds__(inner2_threads<B2>(), HSVD_INNER_MINB) k_inner
                     cq[k] = tcq.y;
                     sq[k] = inner_st(tcq.x, (hm >> qk[k]) & 1u);
                     if (live[k]) {
+#if HSVD_INNER_PRE0
+                        if (k < NPRE) {
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) x[k][u] = xp[k < NPRE ? k : 0][u];
+                            continue;
+                        }
+#endif
 #pragma unroll
                         for (int u = 0; u < 4; ++u) x[k][u] = Ar[read_off(k, u)];
                     }
