@@ -54,6 +54,9 @@
 #ifndef HSVD_INNER_PRE0  // bulk: the critical slot's entries loaded before the round's rotations
 #define HSVD_INNER_PRE0 1  // slots prefetched; 2: 1403, 4: 1455 cycles per round (1: 1392)
 #endif
+#ifndef HSVD_W_SUSPEND_NS  // W warps' mbarrier wait: suspend-time hint
+#define HSVD_W_SUSPEND_NS 1000000
+#endif
 #ifndef HSVD_INNER_WHALF
 #define HSVD_INNER_WHALF 0  // 1: W rows split over two threads (half rows; measured slower: 1600 vs 1470 cycles per round)
 #endif
@@ -141,7 +144,7 @@ __device__ __forceinline__ void mbar_wait_parked(unsigned bar, unsigned parity)
         "{\n .reg .pred p;\n"
         "HSVD_MBP_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
         " @!p bra HSVD_MBP_%=;\n}\n" ::"r"(bar),
-        "r"(parity), "r"(1000000)
+        "r"(parity), "r"(HSVD_W_SUSPEND_NS)
         : "memory");
 }
 
