@@ -567,7 +567,9 @@ def run_ours(a, rank, world, local_rank):
             "config": {"workload": f"n={a.n} p={a.p} full HSVD with V^-T (SURVEY.md §8(d) cfg 5)",
                        "n": a.n, "p": a.p, "mode": a.mode,
                        **({"block_cols": a.block_cols, "block_rotation": a.block_rotation,
-                           "inner_ordering": a.inner_ordering, "inner_passes": a.inner_passes,
+                           "inner_ordering": a.inner_ordering,
+                           "inner_passes": (a.inner_passes if a.inner_passes > 0 else
+                                            "auto: 2 per step in the dense sweeps, 1 in the late ones"),
                            "block_streams": a.block_streams}
                           if a.mode == "block" else {}),
                        "parallelism": (f"{world} GPUs: block-column slots sharded, NCCL ring "
